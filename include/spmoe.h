@@ -1,0 +1,288 @@
+/*
+ * spmoe.h — C ABI of the B200-native SP-MoE verification-time expert path.
+ *
+ * The reference (arxiv 2510.10302, package `moesim`) is pure Python with no
+ * FFI; every entry point below realises one reference function on sm_100a
+ * and is called from the Python drop-in layer (paper_2510_10302_b200) via
+ * ctypes.  Each declaration cites the reference symbol it replaces.
+ *
+ * ABI conventions
+ *   - plain pointers and sizes only; all device memory is caller-owned, no
+ *     allocation happens inside a compute entry point;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream);
+ *   - every function returns an int status: 0 (cudaSuccess) or a
+ *     cudaError_t value (cudaErrorInvalidValue = 1 for bad arguments);
+ *   - no C++ exception crosses the ABI; everything is stream-ordered and
+ *     re-entrant per stream;
+ *   - bf16 tensors are passed as uint16_t* (raw bfloat16 bits).
+ *
+ * Determinism contract (what makes CPU-oracle parity bit-exact):
+ *   - every dot product multiplies bf16 x bf16 (exact in fp32) and adds in a
+ *     documented fixed order: lane j of a warp sums the 8-element chunks
+ *     c = j, j+32, j+64, ... in ascending order, elements 0..7 in order,
+ *     then a xor-butterfly over offsets 16,8,4,2,1;
+ *   - exp is spmoe's own range-reduced polynomial built from IEEE mul/add
+ *     (no FMA contraction, no SFU approximation), so softmax weights and
+ *     SiLU are reproducible on the CPU;
+ *   - top-k orders by (logit desc, expert index asc), the tie-break of
+ *     moesim.trace.top_k_indices (trace.py:28-37).
+ */
+#ifndef SPMOE_H
+#define SPMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* --------------------------------------------------------------------- */
+/* library                                                                */
+/* --------------------------------------------------------------------- */
+
+/* ABI version (major*100 + minor). */
+int spmoe_abi_version(void);
+
+/* Last CUDA error string for a status code (static storage). */
+const char* spmoe_status_string(int status);
+
+/* --------------------------------------------------------------------- */
+/* K1  router_topk                                                        */
+/*   replaces predictor.predict_scores + select_critical                  */
+/*   (predictor.py:79-106), trace.top_k_indices (trace.py:28-37), and     */
+/*   Algorithm 1 lines 2-3 Gates[l](s) / TopK_Index.   */
+/* --------------------------------------------------------------------- */
+/*
+ * x        [T, H]  bf16   layer MLP input (post-attention RMSNorm)
+ * w_gate   [E, H]  bf16   router weight of the target layer
+ * renorm   1: weights = softmax over the k selected logits (Mixtral);
+ *          0: weights = softmax over all E logits, picked at the top-k
+ *             (DeepSeek-V2 / Qwen1.5-MoE, norm_topk_prob = False)
+ * weights  [T, k]  f32    out
+ * idx      [T, k]  i32    out, descending logit, ties -> lowest index
+ * logits   [T, E]  f32    out, nullable
+ * host_idx [T, k]  i32    nullable; mapped pinned host memory also receiving
+ *                          idx (the predictor's zero-copy hand-off to the
+ *                          prefetch worker)
+ * shared_gate_w [H] bf16  nullable; when set, shared_gate[T] f32 receives
+ *                          sigmoid(x . shared_gate_w) (Qwen1.5-MoE)
+ * Constraints: H % 8 == 0, 1 <= k <= E <= 256, T >= 0.
+ */
+int spmoe_router_topk(const uint16_t* x, const uint16_t* w_gate, int T, int H, int E,
+                      int k, int renorm, float* weights, int32_t* idx, float* logits,
+                      int32_t* host_idx, const uint16_t* shared_gate_w, float* shared_gate,
+                      void* stream);
+
+/* --------------------------------------------------------------------- */
+/* K2  moe_permute                                                        */
+/*   replaces the union-of-required loop of Simulation._verify_stage      */
+/*   (simcore.py:365-372) with a device-side grouping of verify tokens.   */
+/* --------------------------------------------------------------------- */
+/*
+ * idx             [T, k] i32  routed experts per token
+ * expert_offsets  [E+1]  i32  out: exclusive prefix of per-expert counts
+ * perm_token      [T*k]  i32  out: token of each permuted row (grouped by
+ *                              expert ascending, then token ascending)
+ * inv_pos         [T*k]  i32  out: permuted row of (token t, choice i)
+ */
+int spmoe_moe_permute(const int32_t* idx, int T, int k, int E, int32_t* expert_offsets,
+                      int32_t* perm_token, int32_t* inv_pos, void* stream);
+
+/* --------------------------------------------------------------------- */
+/* K3  expert_ffn (grouped SwiGLU over the HBM slot pool)                 */
+/*   realises Eq. 1's E_i(x) for every routed expert,  */
+/*   charged as t_comp_target in Simulation._verify_stage (simcore.py:397)*/
+/* --------------------------------------------------------------------- */
+/*
+ * Expert blob layout (one slot, bf16, contiguous, 3*F*H elements):
+ *     W1 [F, H] (gate) | W3 [F, H] (up) | W2 [H, F] (down)
+ * pool            base of the slot pool [S, 3*F*H] bf16
+ * slot_of_expert  HOST array [E] of slot indices (copied into the kernel
+ *                 parameters; only experts in `expert_mask` are read)
+ * expert_mask     bit e set => process expert e in this launch (E <= 64);
+ *                 lets the caller run cache-resident experts first and the
+ *                 demand-loaded ones as their copies land
+ * x               [T, H] bf16 layer MLP input (unpermuted)
+ * expert_offsets, perm_token   from spmoe_moe_permute
+ * h_scratch       [T*k, F] bf16 scratch (SwiGLU activations, permuted rows)
+ * y               [T*k, H] f32  out: per-(token, choice) expert outputs
+ * max_tokens_per_expert  hint selecting the register tile (any value is
+ *                 correct; <=0 means unknown)
+ * Dense mode: E = 1, k = 1, expert_offsets = {0, T}, perm_token = identity
+ * runs a dense SwiGLU MLP (draft FFN, shared experts).
+ */
+int spmoe_expert_ffn(const uint16_t* pool, int64_t slot_elems, const int32_t* slot_of_expert,
+                     uint64_t expert_mask, const uint16_t* x, int T, int H, int F, int E,
+                     int k, const int32_t* expert_offsets, const int32_t* perm_token,
+                     uint16_t* h_scratch, float* y, int max_tokens_per_expert, void* stream);
+
+/* Phase entry points (exposed for profiling and the tcgen05 comparison). */
+int spmoe_expert_ffn_up(const uint16_t* pool, int64_t slot_elems, const int32_t* slot_of_expert,
+                        uint64_t expert_mask, const uint16_t* x, int T, int H, int F, int E,
+                        int k, const int32_t* expert_offsets, const int32_t* perm_token,
+                        uint16_t* h_scratch, int max_tokens_per_expert, void* stream);
+int spmoe_expert_ffn_down(const uint16_t* pool, int64_t slot_elems,
+                          const int32_t* slot_of_expert, uint64_t expert_mask, int T, int H,
+                          int F, int E, int k, const int32_t* expert_offsets,
+                          const uint16_t* h_scratch, float* y, int max_tokens_per_expert,
+                          void* stream);
+
+/* --------------------------------------------------------------------- */
+/* K4  moe_combine                                                        */
+/*   Eq. 1 weighted sum Output = sum_i G(x)_i E_i(x)  */
+/* --------------------------------------------------------------------- */
+/*
+ * out[t] = bf16( residual[t] + sum_{i<k} weights[t,i] * y[inv_pos[t,i]]
+ *                + shared_gate[t] * y_shared[t] )
+ * fp32, fixed order: i ascending with separate mul and add, then the
+ * shared term, then the residual.  residual, weights (NULL => 1.0),
+ * y_shared and shared_gate (NULL => 1.0) are nullable.  out may alias
+ * residual.
+ */
+int spmoe_moe_combine(const float* y, const int32_t* inv_pos, const float* weights, int T,
+                      int H, int k, const float* y_shared, const float* shared_gate,
+                      const uint16_t* residual, uint16_t* out, void* stream);
+
+/* --------------------------------------------------------------------- */
+/* K6  greedy_accept                                                      */
+/*   replaces the Bernoulli acceptance of Simulation.run                  */
+/*   (simcore.py:440-446) with the SD greedy rule:      */
+/*   longest prefix where draft[i] == argmax(target_logits[i]), plus one  */
+/*   correction / bonus token.                                           */
+/* --------------------------------------------------------------------- */
+/*
+ * logits  [B, N+1, V] f32 (row stride ld >= V)
+ * draft   [B, N]      i32
+ * argmax_out [B, N+1] i32 out (ties -> lowest index)
+ * result  [B, 2]      i32 out: {accepted, next_token}
+ */
+int spmoe_greedy_accept(const float* logits, int64_t ld, const int32_t* draft, int B, int N,
+                        int V, int32_t* argmax_out, int32_t* result, void* stream);
+
+/* Row argmax over bf16/f32 rows (draft-token selection). */
+int spmoe_argmax_rows(const float* logits, int64_t ld, int rows, int V, int32_t* out,
+                      void* stream);
+
+/* --------------------------------------------------------------------- */
+/* K5  h2d_batch                                                          */
+/*   IoChannel.transfer / worker_step batched copy (prefetch.py:60-74,    */
+/*   191-214); Algorithm 2 line 12 copy_non_blocking.     */
+/* --------------------------------------------------------------------- */
+int spmoe_h2d_batch(void* const* dst, const void* const* src, const size_t* bytes, int n,
+                    void* stream);
+
+/* --------------------------------------------------------------------- */
+/* Deterministic init: counter-hash N(0, std^2) bf16, identical on CPU.   */
+/* --------------------------------------------------------------------- */
+int spmoe_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, uint64_t offset,
+                           float std, void* stream);
+
+/* --------------------------------------------------------------------- */
+/* Native runtime: LRU slot cache + prefetch worker (prefetch.py,        */
+/* cache.py, Algorithm 2)                                */
+/* --------------------------------------------------------------------- */
+typedef struct spmoe_rt spmoe_rt;
+
+/*
+ * Create the expert-cache runtime.
+ *   capacity        HBM slots (cache_capacity_slots, config.py:234-242)
+ *   num_layers, num_experts   expert id space (layer, expert)
+ *   dev_pool        device slot pool base; slot s lives at
+ *                   dev_pool + s * slot_bytes
+ *   host_pool       pinned host pool; expert (l, e) lives at
+ *                   host_pool + host_index[l*E+e] * slot_bytes
+ *   host_index      [L*E] host-pool index of each expert (lets a bounded
+ *                   host pool alias experts; identity when NULL)
+ *   copy_stream     dedicated copy stream (cudaStream_t)
+ *   batched_io      PolicySpec.batched_io (config.py:190-221)
+ */
+spmoe_rt* spmoe_rt_create(int capacity, int num_layers, int num_experts, void* dev_pool,
+                          const void* host_pool, const int32_t* host_index, size_t slot_bytes,
+                          void* copy_stream, int batched_io);
+void spmoe_rt_destroy(spmoe_rt* rt);
+
+/* ExpertCache.lookup (cache.py:62-77).  Returns 1 hit / 0 miss. */
+int spmoe_rt_lookup(spmoe_rt* rt, int layer, int expert, int touch);
+/* Slot of a resident expert, -1 if absent. */
+int spmoe_rt_slot_of(spmoe_rt* rt, int layer, int expert);
+/* ExpertCache.insert_batch metadata only (cache.py:79-122), no copy.
+ * kind: 0 prefetch, 1 demand.  victims_out [2*n] receives (layer, expert)
+ * pairs; returns the number of victims, or -1 on CacheError. */
+int spmoe_rt_insert_batch(spmoe_rt* rt, const int32_t* layers, const int32_t* experts, int n,
+                          int kind, int32_t* victims_out);
+/* ExpertCache.pin / unpin (cache.py:124-133).  pin returns -1 if any id
+ * is not resident. */
+int spmoe_rt_pin(spmoe_rt* rt, const int32_t* layers, const int32_t* experts, int n);
+void spmoe_rt_unpin(spmoe_rt* rt, const int32_t* layers, const int32_t* experts, int n);
+/* LRU order, head (least recent) first; returns count written (<= cap). */
+int spmoe_rt_lru_order(spmoe_rt* rt, int32_t* layers, int32_t* experts, int cap);
+/* counters: hits, misses, evictions, prefetch_evictions,
+ * prefetch_insertions, demand_insertions, tasks_completed, tasks_aborted,
+ * prefetch_bytes, demand_bytes, n_resident, evictions_of_queued_targets */
+void spmoe_rt_counters(spmoe_rt* rt, int64_t* out12);
+void spmoe_rt_reset_stats(spmoe_rt* rt);
+
+/*
+ * Demand load (prefetch.on_demand_load, prefetch.py:276-301): insert the
+ * non-resident ids as one DEMAND batch, copy them on the copy stream behind
+ * whatever is queued there, and record each slot's ready event.  Slots are
+ * written to slots_out[n] (resident ids keep their slot).  Returns 0 or a
+ * status (-1: CacheError).
+ */
+int spmoe_rt_demand_load(spmoe_rt* rt, const int32_t* layers, const int32_t* experts, int n,
+                         int32_t* slots_out);
+
+/* Make `stream` wait until slot's pending copy (if any) has landed. */
+int spmoe_rt_wait_slot(spmoe_rt* rt, int slot, void* stream);
+/* Record that kernels on `stream` read `slot` (the copy stream waits on it
+ * before the slot is overwritten: slot-reuse hazard, SURVEY hard part 5). */
+int spmoe_rt_mark_read(spmoe_rt* rt, int slot, void* stream);
+/* 1 if slot's last copy has completed (cudaEventQuery), else 0. */
+int spmoe_rt_slot_ready(spmoe_rt* rt, int slot);
+
+/*
+ * Prefetch worker (Algorithm 1 enqueue + Algorithm 2 worker thread).
+ * push: one task = the top-k predicted experts of `layer`, whose indices
+ * the predictor kernel writes to mapped pinned memory `host_idx` [k];
+ * `ready_event` (cudaEvent_t) is recorded after that kernel.  The worker
+ * waits on the event, drops resident ids (non-touch probe,
+ * enqueue_critical prefetch.py:118-145 + pop-time re-check
+ * prefetch.py:186-189), picks LRU victims, issues the batched copy on the
+ * copy stream and installs the batch (move-to-end).  Tasks run FIFO.
+ */
+int spmoe_rt_worker_start(spmoe_rt* rt);
+int spmoe_rt_push_task(spmoe_rt* rt, int layer, const int32_t* host_idx, int k,
+                       void* ready_event, int issue_token);
+/* Block until every pushed task has been popped and its copies issued. */
+int spmoe_rt_drain(spmoe_rt* rt);
+/* Drop queued-but-unpopped tasks (end of inference); returns count. */
+int spmoe_rt_abort_pending(spmoe_rt* rt);
+int spmoe_rt_worker_stop(spmoe_rt* rt);
+
+/* Copy log: one record per issued copy batch. rec = {layer, n_experts,
+ * kind(0 prefetch / 1 demand), issue_seq}; t = {start_ms, end_ms} from CUDA
+ * events relative to the runtime epoch (valid after the copies complete).
+ * Returns number of records written. */
+int spmoe_rt_transfer_log(spmoe_rt* rt, int32_t* rec4, double* t2, int cap);
+/* Experts of record i (expert ids, up to cap). */
+int spmoe_rt_transfer_experts(spmoe_rt* rt, int i, int32_t* experts, int cap);
+/* Drop the transfer log (waits for logged copies to finish). */
+void spmoe_rt_clear_log(spmoe_rt* rt);
+
+/* --------------------------------------------------------------------- */
+/* Host memory helpers                                                    */
+/* --------------------------------------------------------------------- */
+/* Page-locked, portable, mapped host allocation; *dev receives the device
+ * alias (what a kernel writes to for zero-copy hand-off). */
+int spmoe_host_alloc_mapped(size_t bytes, void** host, void** dev);
+int spmoe_host_free(void* host);
+/* Pin an existing host range (e.g. a /dev/shm expert pool shared by the
+ * per-GPU processes of one box), portable + mapped. */
+int spmoe_host_register(void* host, size_t bytes);
+int spmoe_host_unregister(void* host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPMOE_H */

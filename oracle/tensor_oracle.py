@@ -1,0 +1,179 @@
+"""numpy front end of ``liboracle.so`` (oracle/spmoe_oracle.c).
+
+TEST INFRASTRUCTURE ONLY — the checker for the sm_100a kernels and the timed
+CPU restatement for bench.py's reference arm.  See spmoe_oracle.c for the
+reference anchors (Eq. 1, Alg. 1-2; trace.py:28-37 tie-break).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB = HERE / "liboracle.so"
+_lib = None
+
+_p = C.c_void_p
+_i = C.c_int
+_i64 = C.c_int64
+_u64 = C.c_uint64
+_f = C.c_float
+
+_SIGS = {
+    "oracle_det_exp": (_f, [_f]),
+    "oracle_det_silu": (_f, [_f]),
+    "oracle_dot_fixed": (_f, [_p, _p, _i]),
+    "oracle_router_topk": (None, [_p, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p]),
+    "oracle_moe_permute": (None, [_p, _i, _i, _i, _p, _p, _p]),
+    "oracle_expert_ffn": (None, [_p, _p, _i, _i, _i, _i, _p, _p, _p, _p]),
+    "oracle_moe_combine": (None, [_p, _p, _p, _i, _i, _i, _p, _p, _p, _p]),
+    "oracle_argmax_rows": (None, [_p, _i64, _i, _i, _p]),
+    "oracle_greedy_accept": (None, [_p, _i64, _p, _i, _i, _i, _p, _p]),
+    "oracle_fill_normal_bf16": (None, [_p, _i64, _u64, _u64, _f]),
+    "oracle_set_threads": (None, [_i]),
+    "oracle_num_threads": (_i, []),
+}
+
+
+def build() -> Path:
+    src = HERE / "spmoe_oracle.c"
+    if not LIB.exists() or LIB.stat().st_mtime < src.stat().st_mtime:
+        subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+    return LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(str(LIB))
+        for n, (r, a) in _SIGS.items():
+            f = getattr(L, n)
+            f.restype = r
+            f.argtypes = a
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def set_threads(n: int) -> None:
+    lib().oracle_set_threads(int(n))
+
+
+def det_exp(x: float) -> float:
+    return float(lib().oracle_det_exp(float(x)))
+
+
+def dot_fixed(a_bf16: np.ndarray, b_bf16: np.ndarray) -> float:
+    a = _c(a_bf16, np.uint16)
+    b = _c(b_bf16, np.uint16)
+    return float(lib().oracle_dot_fixed(_ptr(a), _ptr(b), a.size))
+
+
+def router_topk(x, wg, k, renorm=True, sg_w=None):
+    """x [T,H] uint16(bf16 bits), wg [E,H] -> (weights f32[T,k], idx i32[T,k],
+    logits f32[T,E], shared_gate f32[T] | None)."""
+    x = _c(x, np.uint16)
+    wg = _c(wg, np.uint16)
+    T, H = x.shape
+    E = wg.shape[0]
+    w = np.empty((T, k), np.float32)
+    idx = np.empty((T, k), np.int32)
+    lg = np.empty((T, E), np.float32)
+    sg = None
+    sgw = None
+    if sg_w is not None:
+        sgw = _c(sg_w, np.uint16)
+        sg = np.empty((T,), np.float32)
+    lib().oracle_router_topk(_ptr(x), _ptr(wg), T, H, E, k, 1 if renorm else 0, _ptr(w), _ptr(idx), _ptr(lg), _ptr(sgw), _ptr(sg))
+    return w, idx, lg, sg
+
+
+def moe_permute(idx, E):
+    idx = _c(idx, np.int32)
+    T, k = idx.shape
+    off = np.empty((E + 1,), np.int32)
+    perm = np.empty((T * k,), np.int32)
+    inv = np.full((T * k,), -1, np.int32)
+    lib().oracle_moe_permute(_ptr(idx), T, k, E, _ptr(off), _ptr(perm), _ptr(inv))
+    return off, perm, inv
+
+
+def expert_ffn(blobs, x, F, offsets, perm, h_out=None, y=None):
+    """blobs: list of E uint16 arrays (or None); returns (h [T*k,F] u16, y [T*k,H] f32)."""
+    x = _c(x, np.uint16)
+    T, H = x.shape
+    E = len(blobs)
+    n = int(offsets[-1])
+    if h_out is None:
+        h_out = np.zeros((max(n, 1), F), np.uint16)
+    if y is None:
+        y = np.zeros((max(n, 1), H), np.float32)
+    keep = [None if b is None else _c(b, np.uint16) for b in blobs]
+    arr = (C.c_void_p * E)(*[None if b is None else b.ctypes.data for b in keep])
+    offsets = _c(offsets, np.int32)
+    perm = _c(perm, np.int32)
+    lib().oracle_expert_ffn(arr, _ptr(x), T, H, F, E, _ptr(offsets), _ptr(perm), _ptr(h_out), _ptr(y))
+    return h_out, y
+
+
+def moe_combine(y, inv, w, T, H, k, ys=None, sg=None, residual=None):
+    out = np.empty((T, H), np.uint16)
+    y = _c(y, np.float32)
+    inv = _c(inv, np.int32)
+    w = None if w is None else _c(w, np.float32)
+    ys = None if ys is None else _c(ys, np.float32)
+    sg = None if sg is None else _c(sg, np.float32)
+    residual = None if residual is None else _c(residual, np.uint16)
+    lib().oracle_moe_combine(_ptr(y), _ptr(inv), _ptr(w), T, H, k, _ptr(ys), _ptr(sg), _ptr(residual), _ptr(out))
+    return out
+
+
+def greedy_accept(logits, draft):
+    logits = _c(logits, np.float32)
+    B, N1, V = logits.shape
+    N = N1 - 1
+    draft = _c(draft, np.int32).reshape(B, N) if N > 0 else np.zeros((B, 0), np.int32)
+    amax = np.empty((B, N1), np.int32)
+    res = np.empty((B, 2), np.int32)
+    lib().oracle_greedy_accept(_ptr(logits), V, _ptr(draft), B, N, V, _ptr(amax), _ptr(res))
+    return amax, res
+
+
+def argmax_rows(logits):
+    logits = _c(logits, np.float32)
+    R, V = logits.shape
+    out = np.empty((R,), np.int32)
+    lib().oracle_argmax_rows(_ptr(logits), V, R, V, _ptr(out))
+    return out
+
+
+def fill_normal_bf16(n, seed, offset=0, std=0.02):
+    out = np.empty((n,), np.uint16)
+    lib().oracle_fill_normal_bf16(_ptr(out), n, seed & 0xFFFFFFFFFFFFFFFF, offset & 0xFFFFFFFFFFFFFFFF, float(std))
+    return out
+
+
+# ---------------------------------------------------------------- bf16 utils
+def f32_to_bf16_bits(a: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even fp32 -> bf16 bits (same rule as the kernels)."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    nan = (u & 0x7FFFFFFF) > 0x7F800000
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    r[nan] = 0x7FC0
+    return r
+
+
+def bf16_bits_to_f32(a: np.ndarray) -> np.ndarray:
+    return (np.ascontiguousarray(a, np.uint16).astype(np.uint32) << 16).view(np.float32)

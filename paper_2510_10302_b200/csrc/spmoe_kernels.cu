@@ -1,0 +1,621 @@
+// spmoe_kernels.cu — sm_100a kernels of the SP-MoE verification-time expert
+// path: K1 router_topk, K2 moe_permute, K3 expert_ffn (weight-streaming
+// grouped SwiGLU over the HBM slot pool), K4 moe_combine, K6 greedy_accept,
+// plus the deterministic counter-hash weight init.  C ABI in include/spmoe.h.
+#include "spmoe_common.cuh"
+#include "../../include/spmoe.h"
+
+#include <stdio.h>
+
+using namespace spmoe;
+
+namespace {
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+inline int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return (int)e;
+}
+
+// ---------------------------------------------------------------------------
+// K1 router_topk: one CTA per token.  Warps compute the E logits with the
+// fixed-order dot product; thread 0 selects the top-k by (logit desc, index
+// asc) and forms the softmax weights with det_exp and sequential sums.
+// ---------------------------------------------------------------------------
+constexpr int kRouterThreads = 256;
+constexpr int kMaxExperts = 256;
+
+__global__ void __launch_bounds__(kRouterThreads)
+router_topk_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ wg, int H,
+                   int E, int k, int renorm, float* __restrict__ weights,
+                   int32_t* __restrict__ idx, float* __restrict__ logits_out,
+                   int32_t* __restrict__ host_idx, const uint16_t* __restrict__ sg_w,
+                   float* __restrict__ shared_gate) {
+  __shared__ float s_logit[kMaxExperts + 1];
+  const int t = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = kRouterThreads / 32;
+  const int nchunks = H >> 3;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (size_t)t * H);
+  const int nrows = E + (sg_w != nullptr ? 1 : 0);
+  for (int e = warp; e < nrows; e += nwarps) {
+    const uint16_t* wrow = (e < E) ? wg + (size_t)e * H : sg_w;
+    const uint4* wr = reinterpret_cast<const uint4*>(wrow);
+    float acc = 0.0f;
+    for (int c = lane; c < nchunks; c += 32) {
+      float a[8], b[8];
+      unpack8(__ldg(xr + c), a);
+      unpack8(__ldg(wr + c), b);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) acc = fmaf(a[v], b[v], acc);  // exact products
+    }
+    acc = warp_sum_fixed(acc);
+    if (lane == 0) s_logit[e] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (logits_out != nullptr)
+      for (int e = 0; e < E; ++e) logits_out[(size_t)t * E + e] = s_logit[e];
+    if (sg_w != nullptr && shared_gate != nullptr)
+      shared_gate[t] = __fdiv_rn(1.0f, __fadd_rn(1.0f, det_exp(-s_logit[E])));
+    // top-k selection: strictly-greater scan keeps the lowest index on ties
+    int sel[kMaxExperts];
+    uint32_t taken[kMaxExperts / 32] = {0};
+    for (int i = 0; i < k; ++i) {
+      int best = -1;
+      float bv = 0.0f;
+      for (int e = 0; e < E; ++e) {
+        if (taken[e >> 5] & (1u << (e & 31))) continue;
+        const float v = s_logit[e];
+        if (best < 0 || v > bv) { best = e; bv = v; }
+      }
+      sel[i] = best;
+      taken[best >> 5] |= 1u << (best & 31);
+    }
+    const float m = s_logit[sel[0]];
+    float sum = 0.0f;
+    if (renorm) {
+      for (int i = 0; i < k; ++i) sum = __fadd_rn(sum, det_exp(__fsub_rn(s_logit[sel[i]], m)));
+    } else {
+      for (int e = 0; e < E; ++e) sum = __fadd_rn(sum, det_exp(__fsub_rn(s_logit[e], m)));
+    }
+    for (int i = 0; i < k; ++i) {
+      const float ex = det_exp(__fsub_rn(s_logit[sel[i]], m));
+      weights[(size_t)t * k + i] = __fdiv_rn(ex, sum);
+      idx[(size_t)t * k + i] = sel[i];
+      if (host_idx != nullptr) host_idx[(size_t)t * k + i] = sel[i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2 moe_permute: single CTA; thread e owns expert e and scans the routed
+// (token, choice) pairs in order, so the permutation is stable by token.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+moe_permute_kernel(const int32_t* __restrict__ idx, int T, int k, int E,
+                   int32_t* __restrict__ offsets, int32_t* __restrict__ perm_token,
+                   int32_t* __restrict__ inv_pos) {
+  __shared__ int s_cnt[kMaxExperts + 1];
+  const int n = T * k;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int c = 0;
+    for (int j = 0; j < n; ++j) c += (idx[j] == e);
+    s_cnt[e] = c;
+  }
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const int e = idx[j];
+    if (e < 0 || e >= E) inv_pos[j] = -1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      const int c = s_cnt[e];
+      s_cnt[e] = acc;
+      offsets[e] = acc;
+      acc += c;
+    }
+    offsets[E] = acc;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int p = s_cnt[e];
+    for (int j = 0; j < n; ++j) {
+      if (idx[j] == e) {
+        perm_token[p] = j / k;
+        inv_pos[j] = p;
+        ++p;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3 expert_ffn.  Weight-streaming grouped SwiGLU: every warp owns whole
+// weight rows (one row of W1 and the matching row of W3 in the up phase, one
+// row of W2 in the down phase) and streams them once from HBM with 16-byte
+// no-allocate loads, UNR loads in flight per lane; the routed tokens'
+// activations are re-read through L1.  Rows of all active experts are laid
+// end to end and dealt round-robin to the global warp index, so the load is
+// balanced to one row across the 148 SMs.  Dot products follow the fixed
+// order of the determinism contract (lane-strided chunks, butterfly).
+// ---------------------------------------------------------------------------
+constexpr int kFfnThreads = 512;
+constexpr int kMaxFfnExperts = 64;
+
+struct FfnParams {
+  const uint16_t* pool;
+  int64_t slot_elems;
+  uint64_t mask;
+  const uint16_t* x;       // up: [T, H] activations
+  const uint16_t* h;       // down: [T*k, F] SwiGLU activations
+  uint16_t* h_out;         // up output
+  float* y;                // down output [T*k, H]
+  const int32_t* offsets;  // [E+1]
+  const int32_t* perm;     // [T*k]
+  int T, H, F, E, k;
+  int slot[kMaxFfnExperts];
+};
+
+// Collect the active experts (mask bit set and at least one routed row) into
+// shared memory; returns their count.
+__device__ __forceinline__ int gather_active(const FfnParams& p, int* s_active, int* s_off) {
+  __shared__ int s_n;
+  if (threadIdx.x < 32) {
+    int base = 0;
+    for (int e0 = 0; e0 < p.E; e0 += 32) {
+      const int e = e0 + threadIdx.x;
+      bool on = false;
+      int o0 = 0, o1 = 0;
+      if (e < p.E) {
+        o0 = p.offsets[e];
+        o1 = p.offsets[e + 1];
+        on = ((p.mask >> e) & 1ull) && (o1 > o0);
+      }
+      const unsigned b = __ballot_sync(SPMOE_FULL_MASK, on);
+      if (on) {
+        const int pos = base + __popc(b & ((1u << threadIdx.x) - 1u));
+        s_active[pos] = e;
+      }
+      if (e < p.E) { s_off[e] = o0; s_off[e + 1] = o1; }
+      base += __popc(b);
+    }
+    if (threadIdx.x == 0) s_n = base;
+  }
+  __syncthreads();
+  return s_n;
+}
+
+// acc[r][t] += dot(weight row r, activation row t) over nchunks 16-byte
+// chunks, lane-strided fixed order.
+template <int TT, int NR, int UNR>
+__device__ __forceinline__ void stream_rows(const uint4* const (&wr)[NR],
+                                            const uint4* const (&ar)[TT], int nt, int nchunks,
+                                            int lane, float (&acc)[NR][TT]) {
+  for (int base = 0; base < nchunks; base += 32 * UNR) {
+    uint4 w[NR][UNR];
+#pragma unroll
+    for (int i = 0; i < UNR; ++i) {
+      const int c = base + lane + 32 * i;
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        w[r][i] = (c < nchunks) ? ldg_stream(wr[r] + c) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int i = 0; i < UNR; ++i) {
+      const int c = base + lane + 32 * i;
+      if (c < nchunks) {
+        float wf[NR][8];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) unpack8(w[r][i], wf[r]);
+#pragma unroll
+        for (int t = 0; t < TT; ++t) {
+          if (t < nt) {
+            float af[8];
+            unpack8(ldg_act(ar[t] + c), af);
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+#pragma unroll
+              for (int r = 0; r < NR; ++r) acc[r][t] = fmaf(wf[r][v], af[v], acc[r][t]);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int TT>
+__global__ void __launch_bounds__(kFfnThreads, 1) ffn_up_kernel(const FfnParams p) {
+  __shared__ int s_active[kMaxFfnExperts];
+  __shared__ int s_off[kMaxFfnExperts + 1];
+  const int n_active = gather_active(p, s_active, s_off);
+  const int lane = threadIdx.x & 31;
+  const int gwarp = blockIdx.x * (kFfnThreads / 32) + (threadIdx.x >> 5);
+  const int nwarps = gridDim.x * (kFfnThreads / 32);
+  const int64_t total = (int64_t)n_active * p.F;
+  const int nchunks = p.H >> 3;
+  for (int64_t u = gwarp; u < total; u += nwarps) {
+    const int a = (int)(u / p.F);
+    const int f = (int)(u - (int64_t)a * p.F);
+    const int e = s_active[a];
+    const uint16_t* blob = p.pool + (int64_t)p.slot[e] * p.slot_elems;
+    const uint4* const wr[2] = {reinterpret_cast<const uint4*>(blob + (int64_t)f * p.H),
+                                reinterpret_cast<const uint4*>(blob + ((int64_t)p.F + f) * p.H)};
+    const int off = s_off[e];
+    const int cnt = s_off[e + 1] - off;
+    for (int t0 = 0; t0 < cnt; t0 += TT) {
+      const int nt = min(TT, cnt - t0);
+      const uint4* ar[TT];
+#pragma unroll
+      for (int t = 0; t < TT; ++t) {
+        const int tok = p.perm[off + t0 + min(t, nt - 1)];
+        ar[t] = reinterpret_cast<const uint4*>(p.x + (int64_t)tok * p.H);
+      }
+      float acc[2][TT];
+#pragma unroll
+      for (int t = 0; t < TT; ++t) { acc[0][t] = 0.0f; acc[1][t] = 0.0f; }
+      stream_rows<TT, 2, 8>(wr, ar, nt, nchunks, lane, acc);
+#pragma unroll
+      for (int t = 0; t < TT; ++t) {
+        if (t < nt) {
+          const float g = warp_sum_fixed(acc[0][t]);
+          const float v = warp_sum_fixed(acc[1][t]);
+          if (lane == t) {
+            const float hv = __fmul_rn(det_silu(g), v);
+            p.h_out[(int64_t)(off + t0 + t) * p.F + f] = f32_to_bf16(hv);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int TT>
+__global__ void __launch_bounds__(kFfnThreads, 1) ffn_down_kernel(const FfnParams p) {
+  __shared__ int s_active[kMaxFfnExperts];
+  __shared__ int s_off[kMaxFfnExperts + 1];
+  const int n_active = gather_active(p, s_active, s_off);
+  const int lane = threadIdx.x & 31;
+  const int gwarp = blockIdx.x * (kFfnThreads / 32) + (threadIdx.x >> 5);
+  const int nwarps = gridDim.x * (kFfnThreads / 32);
+  const int64_t total = (int64_t)n_active * p.H;
+  const int nchunks = p.F >> 3;
+  for (int64_t u = gwarp; u < total; u += nwarps) {
+    const int a = (int)(u / p.H);
+    const int hrow = (int)(u - (int64_t)a * p.H);
+    const int e = s_active[a];
+    const uint16_t* blob = p.pool + (int64_t)p.slot[e] * p.slot_elems;
+    const uint4* const wr[1] = {
+        reinterpret_cast<const uint4*>(blob + 2 * (int64_t)p.F * p.H + (int64_t)hrow * p.F)};
+    const int off = s_off[e];
+    const int cnt = s_off[e + 1] - off;
+    for (int t0 = 0; t0 < cnt; t0 += TT) {
+      const int nt = min(TT, cnt - t0);
+      const uint4* ar[TT];
+#pragma unroll
+      for (int t = 0; t < TT; ++t)
+        ar[t] = reinterpret_cast<const uint4*>(p.h + (int64_t)(off + t0 + min(t, nt - 1)) * p.F);
+      float acc[1][TT];
+#pragma unroll
+      for (int t = 0; t < TT; ++t) acc[0][t] = 0.0f;
+      stream_rows<TT, 1, 16>(wr, ar, nt, nchunks, lane, acc);
+#pragma unroll
+      for (int t = 0; t < TT; ++t) {
+        if (t < nt) {
+          const float yv = warp_sum_fixed(acc[0][t]);
+          if (lane == t) p.y[(int64_t)(off + t0 + t) * p.H + hrow] = yv;
+        }
+      }
+    }
+  }
+}
+
+int pick_tile(int hint) {
+  if (hint <= 0) return 8;
+  if (hint <= 1) return 1;
+  if (hint <= 2) return 2;
+  if (hint <= 4) return 4;
+  return 8;
+}
+
+bool fill_params(FfnParams& p, const uint16_t* pool, int64_t slot_elems,
+                 const int32_t* slot_of_expert, uint64_t mask, int T, int H, int F, int E, int k,
+                 const int32_t* offsets, const int32_t* perm) {
+  if (pool == nullptr || slot_of_expert == nullptr || offsets == nullptr) return false;
+  if (T < 0 || H <= 0 || F <= 0 || E <= 0 || E > kMaxFfnExperts || k <= 0) return false;
+  if ((H & 7) || (F & 7)) return false;
+  p.pool = pool;
+  p.slot_elems = slot_elems;
+  p.mask = mask;
+  p.offsets = offsets;
+  p.perm = perm;
+  p.T = T; p.H = H; p.F = F; p.E = E; p.k = k;
+  for (int e = 0; e < E; ++e) p.slot[e] = ((mask >> e) & 1ull) ? slot_of_expert[e] : 0;
+  for (int e = E; e < kMaxFfnExperts; ++e) p.slot[e] = 0;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// K4 moe_combine: one thread per 4 consecutive hidden elements.
+// ---------------------------------------------------------------------------
+__global__ void moe_combine_kernel(const float* __restrict__ y, const int32_t* __restrict__ inv_pos,
+                                   const float* __restrict__ w, int H, int k,
+                                   const float* __restrict__ ys, const float* __restrict__ sg,
+                                   const uint16_t* residual, uint16_t* out) {
+  const int t = blockIdx.y;
+  const int h0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (h0 >= H) return;
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  for (int i = 0; i < k; ++i) {
+    const int pos = inv_pos[t * k + i];
+    if (pos < 0) continue;
+    const float wi = (w != nullptr) ? w[t * k + i] : 1.0f;
+    const float4 v = *reinterpret_cast<const float4*>(y + (int64_t)pos * H + h0);
+    acc[0] = __fadd_rn(acc[0], __fmul_rn(wi, v.x));
+    acc[1] = __fadd_rn(acc[1], __fmul_rn(wi, v.y));
+    acc[2] = __fadd_rn(acc[2], __fmul_rn(wi, v.z));
+    acc[3] = __fadd_rn(acc[3], __fmul_rn(wi, v.w));
+  }
+  if (ys != nullptr) {
+    const float g = (sg != nullptr) ? sg[t] : 1.0f;
+    const float4 v = *reinterpret_cast<const float4*>(ys + (int64_t)t * H + h0);
+    acc[0] = __fadd_rn(acc[0], __fmul_rn(g, v.x));
+    acc[1] = __fadd_rn(acc[1], __fmul_rn(g, v.y));
+    acc[2] = __fadd_rn(acc[2], __fmul_rn(g, v.z));
+    acc[3] = __fadd_rn(acc[3], __fmul_rn(g, v.w));
+  }
+  uint16_t o[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float r = (residual != nullptr) ? bf16_to_f32(residual[(int64_t)t * H + h0 + j]) : 0.0f;
+    o[j] = f32_to_bf16(residual != nullptr ? __fadd_rn(r, acc[j]) : acc[j]);
+  }
+  uint2 packed;
+  packed.x = (uint32_t)o[0] | ((uint32_t)o[1] << 16);
+  packed.y = (uint32_t)o[2] | ((uint32_t)o[3] << 16);
+  *reinterpret_cast<uint2*>(out + (int64_t)t * H + h0) = packed;
+}
+
+// ---------------------------------------------------------------------------
+// K6 greedy acceptance: row argmax (ties -> lowest index), then the longest
+// matching prefix per sequence.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
+  // total order: larger value first, then lower index; NaN never wins
+  if (v != v) return false;
+  if (bv != bv) return true;
+  return (v > bv) || (v == bv && i < bi);
+}
+
+__global__ void __launch_bounds__(1024)
+argmax_rows_kernel(const float* __restrict__ logits, int64_t ld, int V, int32_t* __restrict__ out) {
+  __shared__ float s_v[32];
+  __shared__ int s_i[32];
+  const float* row = logits + (int64_t)blockIdx.x * ld;
+  float bv = __uint_as_float(0x7fc00000u);
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const float v = row[i];
+    if (better(v, i, bv, bi)) { bv = v; bi = i; }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const float ov = __shfl_xor_sync(SPMOE_FULL_MASK, bv, off);
+    const int oi = __shfl_xor_sync(SPMOE_FULL_MASK, bi, off);
+    if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { s_v[warp] = bv; s_i[warp] = bi; }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    bv = (lane < nw) ? s_v[lane] : __uint_as_float(0x7fc00000u);
+    bi = (lane < nw) ? s_i[lane] : 0x7fffffff;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const float ov = __shfl_xor_sync(SPMOE_FULL_MASK, bv, off);
+      const int oi = __shfl_xor_sync(SPMOE_FULL_MASK, bi, off);
+      if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) out[blockIdx.x] = (bi == 0x7fffffff) ? 0 : bi;
+  }
+}
+
+__global__ void accept_prefix_kernel(const int32_t* __restrict__ amax, const int32_t* __restrict__ draft,
+                                     int B, int N, int32_t* __restrict__ result) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int a = 0;
+  while (a < N && draft[b * N + a] == amax[b * (N + 1) + a]) ++a;
+  result[b * 2 + 0] = a;
+  result[b * 2 + 1] = amax[b * (N + 1) + a];
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic init: splitmix64 counter hash -> Irwin-Hall(4) normal.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_normal_kernel(uint16_t* __restrict__ dst, int64_t n, uint64_t seed,
+                                   uint64_t offset, float scale) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t hsh = splitmix64(seed ^ splitmix64(offset + (uint64_t)i));
+    const int s = (int)(hsh & 0xffff) + (int)((hsh >> 16) & 0xffff) +
+                  (int)((hsh >> 32) & 0xffff) + (int)(hsh >> 48);
+    dst[i] = f32_to_bf16(__fmul_rn((float)(s - 131070), scale));
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int spmoe_abi_version(void) { return 100; }
+
+const char* spmoe_status_string(int status) {
+  if (status == -1) return "spmoe: cache contract violation (CacheError)";
+  return cudaGetErrorString((cudaError_t)status);
+}
+
+int spmoe_router_topk(const uint16_t* x, const uint16_t* w_gate, int T, int H, int E, int k,
+                      int renorm, float* weights, int32_t* idx, float* logits, int32_t* host_idx,
+                      const uint16_t* shared_gate_w, float* shared_gate, void* stream) {
+  if (T < 0 || H <= 0 || (H & 7) || E <= 0 || E > kMaxExperts || k < 1 || k > E)
+    return (int)cudaErrorInvalidValue;
+  if (T == 0) return 0;
+  if (!x || !w_gate || !weights || !idx) return (int)cudaErrorInvalidValue;
+  router_topk_kernel<<<T, kRouterThreads, 0, (cudaStream_t)stream>>>(
+      x, w_gate, H, E, k, renorm, weights, idx, logits, host_idx, shared_gate_w, shared_gate);
+  return launch_status();
+}
+
+int spmoe_moe_permute(const int32_t* idx, int T, int k, int E, int32_t* expert_offsets,
+                      int32_t* perm_token, int32_t* inv_pos, void* stream) {
+  if (T < 0 || k < 1 || E < 1 || E > kMaxExperts) return (int)cudaErrorInvalidValue;
+  if (!expert_offsets) return (int)cudaErrorInvalidValue;
+  if (T > 0 && (!idx || !perm_token || !inv_pos)) return (int)cudaErrorInvalidValue;
+  moe_permute_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(idx, T, k, E, expert_offsets,
+                                                          perm_token, inv_pos);
+  return launch_status();
+}
+
+int spmoe_expert_ffn_up(const uint16_t* pool, int64_t slot_elems, const int32_t* slot_of_expert,
+                        uint64_t expert_mask, const uint16_t* x, int T, int H, int F, int E,
+                        int k, const int32_t* expert_offsets, const int32_t* perm_token,
+                        uint16_t* h_scratch, int max_tokens_per_expert, void* stream) {
+  FfnParams p{};
+  if (!fill_params(p, pool, slot_elems, slot_of_expert, expert_mask, T, H, F, E, k,
+                   expert_offsets, perm_token))
+    return (int)cudaErrorInvalidValue;
+  if (T == 0 || expert_mask == 0) return 0;
+  if (!x || !perm_token || !h_scratch) return (int)cudaErrorInvalidValue;
+  p.x = x;
+  p.h_out = h_scratch;
+  const int grid = num_sms();
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (pick_tile(max_tokens_per_expert)) {
+    case 1: ffn_up_kernel<1><<<grid, kFfnThreads, 0, s>>>(p); break;
+    case 2: ffn_up_kernel<2><<<grid, kFfnThreads, 0, s>>>(p); break;
+    case 4: ffn_up_kernel<4><<<grid, kFfnThreads, 0, s>>>(p); break;
+    default: ffn_up_kernel<8><<<grid, kFfnThreads, 0, s>>>(p); break;
+  }
+  return launch_status();
+}
+
+int spmoe_expert_ffn_down(const uint16_t* pool, int64_t slot_elems,
+                          const int32_t* slot_of_expert, uint64_t expert_mask, int T, int H,
+                          int F, int E, int k, const int32_t* expert_offsets,
+                          const uint16_t* h_scratch, float* y, int max_tokens_per_expert,
+                          void* stream) {
+  FfnParams p{};
+  if (!fill_params(p, pool, slot_elems, slot_of_expert, expert_mask, T, H, F, E, k,
+                   expert_offsets, nullptr))
+    return (int)cudaErrorInvalidValue;
+  if (T == 0 || expert_mask == 0) return 0;
+  if (!h_scratch || !y) return (int)cudaErrorInvalidValue;
+  p.h = h_scratch;
+  p.y = y;
+  const int grid = num_sms();
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (pick_tile(max_tokens_per_expert)) {
+    case 1: ffn_down_kernel<1><<<grid, kFfnThreads, 0, s>>>(p); break;
+    case 2: ffn_down_kernel<2><<<grid, kFfnThreads, 0, s>>>(p); break;
+    case 4: ffn_down_kernel<4><<<grid, kFfnThreads, 0, s>>>(p); break;
+    default: ffn_down_kernel<8><<<grid, kFfnThreads, 0, s>>>(p); break;
+  }
+  return launch_status();
+}
+
+int spmoe_expert_ffn(const uint16_t* pool, int64_t slot_elems, const int32_t* slot_of_expert,
+                     uint64_t expert_mask, const uint16_t* x, int T, int H, int F, int E, int k,
+                     const int32_t* expert_offsets, const int32_t* perm_token,
+                     uint16_t* h_scratch, float* y, int max_tokens_per_expert, void* stream) {
+  int st = spmoe_expert_ffn_up(pool, slot_elems, slot_of_expert, expert_mask, x, T, H, F, E, k,
+                               expert_offsets, perm_token, h_scratch, max_tokens_per_expert,
+                               stream);
+  if (st) return st;
+  return spmoe_expert_ffn_down(pool, slot_elems, slot_of_expert, expert_mask, T, H, F, E, k,
+                               expert_offsets, h_scratch, y, max_tokens_per_expert, stream);
+}
+
+int spmoe_moe_combine(const float* y, const int32_t* inv_pos, const float* weights, int T, int H,
+                      int k, const float* y_shared, const float* shared_gate,
+                      const uint16_t* residual, uint16_t* out, void* stream) {
+  if (T < 0 || H <= 0 || (H & 3) || k < 0) return (int)cudaErrorInvalidValue;
+  if (T == 0) return 0;
+  if (!out || (k > 0 && (!y || !inv_pos))) return (int)cudaErrorInvalidValue;
+  const int threads = 128;
+  dim3 grid((H / 4 + threads - 1) / threads, T);
+  moe_combine_kernel<<<grid, threads, 0, (cudaStream_t)stream>>>(y, inv_pos, weights, H, k,
+                                                                 y_shared, shared_gate, residual,
+                                                                 out);
+  return launch_status();
+}
+
+int spmoe_argmax_rows(const float* logits, int64_t ld, int rows, int V, int32_t* out,
+                      void* stream) {
+  if (rows < 0 || V <= 0 || ld < V) return (int)cudaErrorInvalidValue;
+  if (rows == 0) return 0;
+  if (!logits || !out) return (int)cudaErrorInvalidValue;
+  argmax_rows_kernel<<<rows, 1024, 0, (cudaStream_t)stream>>>(logits, ld, V, out);
+  return launch_status();
+}
+
+int spmoe_greedy_accept(const float* logits, int64_t ld, const int32_t* draft, int B, int N,
+                        int V, int32_t* argmax_out, int32_t* result, void* stream) {
+  if (B < 0 || N < 0 || V <= 0 || ld < V) return (int)cudaErrorInvalidValue;
+  if (B == 0) return 0;
+  if (!logits || !argmax_out || !result || (N > 0 && !draft)) return (int)cudaErrorInvalidValue;
+  int st = spmoe_argmax_rows(logits, ld, B * (N + 1), V, argmax_out, stream);
+  if (st) return st;
+  accept_prefix_kernel<<<(B + 127) / 128, 128, 0, (cudaStream_t)stream>>>(argmax_out, draft, B,
+                                                                          N, result);
+  return launch_status();
+}
+
+int spmoe_h2d_batch(void* const* dst, const void* const* src, const size_t* bytes, int n,
+                    void* stream) {
+  if (n < 0 || (n > 0 && (!dst || !src || !bytes))) return (int)cudaErrorInvalidValue;
+  for (int i = 0; i < n; ++i) {
+    cudaError_t e = cudaMemcpyAsync(dst[i], src[i], bytes[i], cudaMemcpyHostToDevice,
+                                    (cudaStream_t)stream);
+    if (e != cudaSuccess) return (int)e;
+  }
+  return 0;
+}
+
+int spmoe_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, uint64_t offset, float std,
+                           void* stream) {
+  if (n < 0 || (n > 0 && !dst)) return (int)cudaErrorInvalidValue;
+  if (n == 0) return 0;
+  const float scale = std * 0x1.bb67aep-16f;  // sqrt(3)/65536, Irwin-Hall(4) -> N(0,1)
+  const int threads = 256;
+  int64_t blocks = (n + threads - 1) / threads;
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  fill_normal_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(dst, n, seed, offset,
+                                                                              scale);
+  return launch_status();
+}
+
+}  // extern "C"

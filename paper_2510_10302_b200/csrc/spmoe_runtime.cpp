@@ -1,0 +1,591 @@
+// spmoe_runtime.cpp — native expert-cache runtime: the HBM slot table with
+// the reference's LRU semantics (moesim cache.py:34-143), the demand-load
+// path (prefetch.py:276-301) and the asynchronous prefetch worker thread of
+// Algorithm 2 (task protocol of prefetch.py:118-223,
+// live-thread model prefetch.py:316-371).
+//
+// Cache metadata is mutated only under `mu_`; the worker mutates it while
+// drafting and the verify stage mutates it after spmoe_rt_drain(), so the
+// sequence of cache operations — and therefore every prefetched / evicted
+// expert set — is a deterministic function of the predictor outputs.
+// Copies are tracked per slot: a ready event recorded on the copy stream
+// after the slot's copy, and a read event recorded on the compute stream
+// after kernels that read the slot (the copy stream waits on it before the
+// slot is overwritten).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "../../include/spmoe.h"
+
+namespace {
+
+struct Task {
+  int layer;
+  const int32_t* host_idx;
+  int k;
+  cudaEvent_t ready;
+  int issue_token;
+};
+
+struct Transfer {
+  int layer;
+  int kind;  // 0 prefetch, 1 demand
+  int seq;
+  std::vector<int> experts;
+  cudaEvent_t start, end;
+};
+
+}  // namespace
+
+struct spmoe_rt {
+  // identity
+  int capacity, L, E, device;
+  char* dev_pool;
+  const char* host_pool;
+  std::vector<int32_t> host_index;
+  size_t slot_bytes;
+  cudaStream_t copy_stream;
+  bool batched;
+
+  // LRU over keys (layer*E + expert): intrusive doubly linked list, head =
+  // least recently used
+  std::vector<int> prev, next, slot_of;
+  std::vector<char> pinned_flag;
+  int head = -1, tail = -1, n_resident = 0, n_pinned = 0;
+  std::vector<int> free_slots;  // kept sorted descending; pop_back = lowest
+
+  // per-slot events
+  std::vector<cudaEvent_t> ready_ev, read_ev;
+  std::vector<char> ready_rec, read_rec;
+
+  // counters
+  int64_t hits = 0, misses = 0, evictions = 0, prefetch_evictions = 0, prefetch_insertions = 0,
+          demand_insertions = 0, tasks_completed = 0, tasks_aborted = 0, prefetch_bytes = 0,
+          demand_bytes = 0, evictions_of_queued = 0;
+
+  // worker
+  std::mutex mu_;
+  std::mutex qmu_;
+  std::condition_variable qcv_, done_cv_;
+  std::deque<Task> queue_;
+  int64_t pushed_ = 0, processed_ = 0;
+  bool stop_ = false, running_ = false;
+  std::thread worker_;
+
+  // transfer log
+  std::vector<Transfer> log_;
+  cudaEvent_t epoch_ = nullptr;
+  int seq_ = 0;
+
+  // ---------------------------------------------------------------- LRU
+  void unlink(int key) {
+    const int p = prev[key], n = next[key];
+    if (p >= 0) next[p] = n; else head = n;
+    if (n >= 0) prev[n] = p; else tail = p;
+    prev[key] = next[key] = -1;
+  }
+  void append(int key) {
+    prev[key] = tail;
+    next[key] = -1;
+    if (tail >= 0) next[tail] = key; else head = key;
+    tail = key;
+  }
+  bool resident(int key) const { return slot_of[key] >= 0; }
+
+  bool lookup(int key, bool touch) {
+    const bool hit = resident(key);
+    if (touch) {
+      if (hit) {
+        ++hits;
+        unlink(key);
+        append(key);
+      } else {
+        ++misses;
+      }
+    }
+    return hit;
+  }
+
+  // insert_batch semantics of cache.py:79-122: dedupe keeping first
+  // occurrence, victims head-first skipping pinned and batch members, then
+  // every batch member moves to the tail in argument order.  New members
+  // take free slots (lowest index first) after the victims release theirs.
+  // Returns false (no mutation) on a contract violation.
+  bool insert_batch(const std::vector<int>& ids_in, int kind, std::vector<int>& victims) {
+    std::vector<int> batch;
+    batch.reserve(ids_in.size());
+    for (int k : ids_in)
+      if (std::find(batch.begin(), batch.end(), k) == batch.end()) batch.push_back(k);
+    if ((int)batch.size() > capacity - n_pinned) return false;
+    int n_new = 0;
+    for (int k : batch) n_new += resident(k) ? 0 : 1;
+    const int overflow = std::max(0, n_resident + n_new - capacity);
+    victims.clear();
+    if (overflow > 0) {
+      for (int k = head; k >= 0 && (int)victims.size() < overflow; k = next[k]) {
+        if (pinned_flag[k]) continue;
+        if (std::find(batch.begin(), batch.end(), k) != batch.end()) continue;
+        victims.push_back(k);
+      }
+      if ((int)victims.size() < overflow) {
+        victims.clear();
+        return false;
+      }
+    }
+    for (int v : victims) {
+      unlink(v);
+      free_slots.push_back(slot_of[v]);
+      slot_of[v] = -1;
+      --n_resident;
+    }
+    std::sort(free_slots.begin(), free_slots.end(), std::greater<int>());
+    evictions += (int64_t)victims.size();
+    if (kind == 0) {
+      prefetch_evictions += (int64_t)victims.size();
+      prefetch_insertions += n_new;
+    } else {
+      demand_insertions += n_new;
+    }
+    for (int k : batch) {
+      if (resident(k)) {
+        unlink(k);
+      } else {
+        slot_of[k] = free_slots.back();
+        free_slots.pop_back();
+        ++n_resident;
+      }
+      append(k);
+    }
+    return true;
+  }
+
+  // ------------------------------------------------------------- copies
+  cudaEvent_t new_timing_event() {
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+
+  // Issue the copies of `keys` (already installed) on the copy stream.
+  int issue_copies(const std::vector<int>& keys, int layer, int kind) {
+    if (keys.empty()) return 0;
+    Transfer tr;
+    tr.layer = layer;
+    tr.kind = kind;
+    tr.seq = seq_++;
+    for (int k : keys) tr.experts.push_back(k % E);
+    tr.start = new_timing_event();
+    tr.end = new_timing_event();
+    cudaError_t st = cudaEventRecord(tr.start, copy_stream);
+    for (size_t i = 0; i < keys.size() && st == cudaSuccess; ++i) {
+      const int k = keys[i];
+      const int s = slot_of[k];
+      if (read_rec[s]) st = cudaStreamWaitEvent(copy_stream, read_ev[s], 0);
+      if (st != cudaSuccess) break;
+      const int hidx = host_index.empty() ? k : host_index[k];
+      st = cudaMemcpyAsync(dev_pool + (size_t)s * slot_bytes,
+                           host_pool + (size_t)hidx * slot_bytes, slot_bytes,
+                           cudaMemcpyHostToDevice, copy_stream);
+      if (st != cudaSuccess) break;
+      st = cudaEventRecord(ready_ev[s], copy_stream);
+      ready_rec[s] = 1;
+      if (!batched && kind == 0 && i + 1 < keys.size()) {
+        // unbatched I/O (PolicySpec.batched_io = false): one copy launch at
+        // a time, each completed before the next is issued
+        st = cudaStreamSynchronize(copy_stream);
+      }
+    }
+    if (st == cudaSuccess) st = cudaEventRecord(tr.end, copy_stream);
+    const int64_t nbytes = (int64_t)keys.size() * (int64_t)slot_bytes;
+    if (kind == 0) prefetch_bytes += nbytes; else demand_bytes += nbytes;
+    log_.push_back(std::move(tr));
+    return (int)st;
+  }
+
+  // -------------------------------------------------------------- worker
+  void run_task(const Task& t) {
+    if (t.ready) cudaEventSynchronize(t.ready);
+    std::lock_guard<std::mutex> g(mu_);
+    // pop-time residency filter (enqueue_critical prefetch.py:131-135 and the
+    // worker re-check prefetch.py:186-189 collapse into one probe here,
+    // because the predicted ids live on the device until the event fires)
+    std::vector<int> load;
+    for (int i = 0; i < t.k; ++i) {
+      const int e = ((volatile const int32_t*)t.host_idx)[i];
+      if (e < 0 || e >= E) continue;
+      const int key = t.layer * E + e;
+      if (!resident(key) && std::find(load.begin(), load.end(), key) == load.end())
+        load.push_back(key);
+    }
+    if (load.empty()) return;  // nothing to move: no task materialises
+    std::vector<int> victims;
+    if (!insert_batch(load, 0, victims)) return;
+    // victims that are still queued targets of later tasks (simcore.py:275-278)
+    {
+      std::lock_guard<std::mutex> q(qmu_);
+      for (int v : victims) {
+        for (const Task& qt : queue_) {
+          bool hit = false;
+          if (qt.layer == v / E) {
+            // ids of queued tasks may not have landed yet; only count the
+            // ones whose event already completed
+            if (qt.ready == nullptr || cudaEventQuery(qt.ready) == cudaSuccess)
+              for (int i = 0; i < qt.k; ++i)
+                if (((volatile const int32_t*)qt.host_idx)[i] == v % E) hit = true;
+          }
+          if (hit) { ++evictions_of_queued; break; }
+        }
+      }
+    }
+    issue_copies(load, t.layer, 0);
+    ++tasks_completed;
+  }
+
+  void worker_loop() {
+    cudaSetDevice(device);
+    for (;;) {
+      Task t;
+      {
+        std::unique_lock<std::mutex> q(qmu_);
+        qcv_.wait(q, [&] { return stop_ || !queue_.empty(); });
+        if (queue_.empty()) return;  // stop requested and nothing left
+        t = queue_.front();
+        queue_.pop_front();
+      }
+      run_task(t);
+      {
+        std::lock_guard<std::mutex> q(qmu_);
+        ++processed_;
+      }
+      done_cv_.notify_all();
+    }
+  }
+};
+
+extern "C" {
+
+spmoe_rt* spmoe_rt_create(int capacity, int num_layers, int num_experts, void* dev_pool,
+                          const void* host_pool, const int32_t* host_index, size_t slot_bytes,
+                          void* copy_stream, int batched_io) {
+  if (capacity < 1 || num_layers < 1 || num_experts < 1) return nullptr;
+  spmoe_rt* rt = new spmoe_rt();
+  rt->capacity = capacity;
+  rt->L = num_layers;
+  rt->E = num_experts;
+  cudaGetDevice(&rt->device);
+  rt->dev_pool = (char*)dev_pool;
+  rt->host_pool = (const char*)host_pool;
+  const int n = num_layers * num_experts;
+  if (host_index) rt->host_index.assign(host_index, host_index + n);
+  rt->slot_bytes = slot_bytes;
+  rt->copy_stream = (cudaStream_t)copy_stream;
+  rt->batched = batched_io != 0;
+  rt->prev.assign(n, -1);
+  rt->next.assign(n, -1);
+  rt->slot_of.assign(n, -1);
+  rt->pinned_flag.assign(n, 0);
+  for (int s = capacity - 1; s >= 0; --s) rt->free_slots.push_back(s);
+  rt->ready_ev.resize(capacity);
+  rt->read_ev.resize(capacity);
+  rt->ready_rec.assign(capacity, 0);
+  rt->read_rec.assign(capacity, 0);
+  for (int s = 0; s < capacity; ++s) {
+    cudaEventCreateWithFlags(&rt->ready_ev[s], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&rt->read_ev[s], cudaEventDisableTiming);
+  }
+  rt->epoch_ = rt->new_timing_event();
+  cudaEventRecord(rt->epoch_, rt->copy_stream);
+  return rt;
+}
+
+void spmoe_rt_destroy(spmoe_rt* rt) {
+  if (!rt) return;
+  spmoe_rt_worker_stop(rt);
+  cudaStreamSynchronize(rt->copy_stream);
+  for (auto e : rt->ready_ev) cudaEventDestroy(e);
+  for (auto e : rt->read_ev) cudaEventDestroy(e);
+  for (auto& t : rt->log_) {
+    cudaEventDestroy(t.start);
+    cudaEventDestroy(t.end);
+  }
+  if (rt->epoch_) cudaEventDestroy(rt->epoch_);
+  delete rt;
+}
+
+static inline bool valid_id(spmoe_rt* rt, int layer, int expert) {
+  return layer >= 0 && layer < rt->L && expert >= 0 && expert < rt->E;
+}
+
+int spmoe_rt_lookup(spmoe_rt* rt, int layer, int expert, int touch) {
+  if (!rt || !valid_id(rt, layer, expert)) return 0;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  return rt->lookup(layer * rt->E + expert, touch != 0) ? 1 : 0;
+}
+
+int spmoe_rt_slot_of(spmoe_rt* rt, int layer, int expert) {
+  if (!rt || !valid_id(rt, layer, expert)) return -1;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  return rt->slot_of[layer * rt->E + expert];
+}
+
+int spmoe_rt_insert_batch(spmoe_rt* rt, const int32_t* layers, const int32_t* experts, int n,
+                          int kind, int32_t* victims_out) {
+  if (!rt || n < 0) return -1;
+  std::vector<int> ids;
+  for (int i = 0; i < n; ++i) {
+    if (!valid_id(rt, layers[i], experts[i])) return -1;
+    ids.push_back(layers[i] * rt->E + experts[i]);
+  }
+  std::lock_guard<std::mutex> g(rt->mu_);
+  std::vector<int> victims;
+  if (!rt->insert_batch(ids, kind, victims)) return -1;
+  if (victims_out)
+    for (size_t i = 0; i < victims.size(); ++i) {
+      victims_out[2 * i] = victims[i] / rt->E;
+      victims_out[2 * i + 1] = victims[i] % rt->E;
+    }
+  return (int)victims.size();
+}
+
+int spmoe_rt_pin(spmoe_rt* rt, const int32_t* layers, const int32_t* experts, int n) {
+  if (!rt) return -1;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  for (int i = 0; i < n; ++i) {
+    if (!valid_id(rt, layers[i], experts[i])) return -1;
+    const int key = layers[i] * rt->E + experts[i];
+    if (!rt->resident(key)) return -1;  // CacheError: pin non-resident
+    if (!rt->pinned_flag[key]) {
+      rt->pinned_flag[key] = 1;
+      ++rt->n_pinned;
+    }
+  }
+  return 0;
+}
+
+void spmoe_rt_unpin(spmoe_rt* rt, const int32_t* layers, const int32_t* experts, int n) {
+  if (!rt) return;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  for (int i = 0; i < n; ++i) {
+    if (!valid_id(rt, layers[i], experts[i])) continue;
+    const int key = layers[i] * rt->E + experts[i];
+    if (rt->pinned_flag[key]) {
+      rt->pinned_flag[key] = 0;
+      --rt->n_pinned;
+    }
+  }
+}
+
+int spmoe_rt_lru_order(spmoe_rt* rt, int32_t* layers, int32_t* experts, int cap) {
+  if (!rt) return 0;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  int n = 0;
+  for (int k = rt->head; k >= 0 && n < cap; k = rt->next[k], ++n) {
+    layers[n] = k / rt->E;
+    experts[n] = k % rt->E;
+  }
+  return n;
+}
+
+void spmoe_rt_counters(spmoe_rt* rt, int64_t* o) {
+  if (!rt || !o) return;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  o[0] = rt->hits; o[1] = rt->misses; o[2] = rt->evictions; o[3] = rt->prefetch_evictions;
+  o[4] = rt->prefetch_insertions; o[5] = rt->demand_insertions; o[6] = rt->tasks_completed;
+  o[7] = rt->tasks_aborted; o[8] = rt->prefetch_bytes; o[9] = rt->demand_bytes;
+  o[10] = rt->n_resident; o[11] = rt->evictions_of_queued;
+}
+
+void spmoe_rt_reset_stats(spmoe_rt* rt) {
+  if (!rt) return;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  rt->hits = rt->misses = rt->evictions = rt->prefetch_evictions = 0;
+  rt->prefetch_insertions = rt->demand_insertions = 0;
+  rt->tasks_completed = rt->tasks_aborted = 0;
+  rt->prefetch_bytes = rt->demand_bytes = rt->evictions_of_queued = 0;
+}
+
+int spmoe_rt_demand_load(spmoe_rt* rt, const int32_t* layers, const int32_t* experts, int n,
+                         int32_t* slots_out) {
+  if (!rt || n < 0) return -1;
+  std::vector<int> ids, missing;
+  for (int i = 0; i < n; ++i) {
+    if (!valid_id(rt, layers[i], experts[i])) return -1;
+    ids.push_back(layers[i] * rt->E + experts[i]);
+  }
+  std::lock_guard<std::mutex> g(rt->mu_);
+  for (int k : ids)
+    if (!rt->resident(k) && std::find(missing.begin(), missing.end(), k) == missing.end())
+      missing.push_back(k);
+  int st = 0;
+  if (!missing.empty()) {
+    std::vector<int> victims;
+    if (!rt->insert_batch(missing, 1, victims)) return -1;
+    st = rt->issue_copies(missing, missing[0] / rt->E, 1);
+  }
+  if (slots_out)
+    for (int i = 0; i < n; ++i) slots_out[i] = rt->slot_of[ids[i]];
+  return st;
+}
+
+int spmoe_rt_wait_slot(spmoe_rt* rt, int slot, void* stream) {
+  if (!rt || slot < 0 || slot >= rt->capacity) return (int)cudaErrorInvalidValue;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  if (!rt->ready_rec[slot]) return 0;
+  return (int)cudaStreamWaitEvent((cudaStream_t)stream, rt->ready_ev[slot], 0);
+}
+
+int spmoe_rt_mark_read(spmoe_rt* rt, int slot, void* stream) {
+  if (!rt || slot < 0 || slot >= rt->capacity) return (int)cudaErrorInvalidValue;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  rt->read_rec[slot] = 1;
+  return (int)cudaEventRecord(rt->read_ev[slot], (cudaStream_t)stream);
+}
+
+int spmoe_rt_slot_ready(spmoe_rt* rt, int slot) {
+  if (!rt || slot < 0 || slot >= rt->capacity) return 0;
+  if (!rt->ready_rec[slot]) return 1;
+  return cudaEventQuery(rt->ready_ev[slot]) == cudaSuccess ? 1 : 0;
+}
+
+int spmoe_rt_worker_start(spmoe_rt* rt) {
+  if (!rt) return (int)cudaErrorInvalidValue;
+  std::lock_guard<std::mutex> q(rt->qmu_);
+  if (rt->running_) return 0;
+  rt->stop_ = false;
+  rt->running_ = true;
+  rt->worker_ = std::thread([rt] { rt->worker_loop(); });
+  return 0;
+}
+
+int spmoe_rt_push_task(spmoe_rt* rt, int layer, const int32_t* host_idx, int k, void* ready_event,
+                       int issue_token) {
+  if (!rt || !host_idx || k < 1 || layer < 0 || layer >= rt->L) return (int)cudaErrorInvalidValue;
+  {
+    std::lock_guard<std::mutex> q(rt->qmu_);
+    rt->queue_.push_back(Task{layer, host_idx, k, (cudaEvent_t)ready_event, issue_token});
+    ++rt->pushed_;
+  }
+  rt->qcv_.notify_one();
+  return 0;
+}
+
+int spmoe_rt_drain(spmoe_rt* rt) {
+  if (!rt) return (int)cudaErrorInvalidValue;
+  std::unique_lock<std::mutex> q(rt->qmu_);
+  if (!rt->running_) {
+    // no thread: run the queue inline (deterministic single-thread mode)
+    while (!rt->queue_.empty()) {
+      Task t = rt->queue_.front();
+      rt->queue_.pop_front();
+      q.unlock();
+      rt->run_task(t);
+      q.lock();
+      ++rt->processed_;
+    }
+    return 0;
+  }
+  rt->done_cv_.wait(q, [&] { return rt->processed_ == rt->pushed_; });
+  return 0;
+}
+
+int spmoe_rt_abort_pending(spmoe_rt* rt) {
+  if (!rt) return 0;
+  int n = 0;
+  {
+    // lock order is always mu_ -> qmu_ (run_task), so never hold qmu_ here
+    // while taking mu_
+    std::lock_guard<std::mutex> q(rt->qmu_);
+    n = (int)rt->queue_.size();
+    rt->queue_.clear();
+    rt->pushed_ -= n;
+  }
+  rt->done_cv_.notify_all();
+  std::lock_guard<std::mutex> g(rt->mu_);
+  rt->tasks_aborted += n;
+  return n;
+}
+
+void spmoe_rt_clear_log(spmoe_rt* rt) {
+  if (!rt) return;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  for (auto& t : rt->log_) {
+    cudaEventSynchronize(t.end);
+    cudaEventDestroy(t.start);
+    cudaEventDestroy(t.end);
+  }
+  rt->log_.clear();
+}
+
+int spmoe_rt_worker_stop(spmoe_rt* rt) {
+  if (!rt) return 0;
+  {
+    std::lock_guard<std::mutex> q(rt->qmu_);
+    if (!rt->running_) return 0;
+    rt->stop_ = true;
+  }
+  rt->qcv_.notify_all();
+  if (rt->worker_.joinable()) rt->worker_.join();
+  std::lock_guard<std::mutex> q(rt->qmu_);
+  rt->running_ = false;
+  return 0;
+}
+
+int spmoe_rt_transfer_log(spmoe_rt* rt, int32_t* rec4, double* t2, int cap) {
+  if (!rt) return 0;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  int n = 0;
+  for (const auto& tr : rt->log_) {
+    if (n >= cap) break;
+    rec4[4 * n + 0] = tr.layer;
+    rec4[4 * n + 1] = (int32_t)tr.experts.size();
+    rec4[4 * n + 2] = tr.kind;
+    rec4[4 * n + 3] = tr.seq;
+    float a = -1.0f, b = -1.0f;
+    if (cudaEventQuery(tr.end) == cudaSuccess) {
+      cudaEventElapsedTime(&a, rt->epoch_, tr.start);
+      cudaEventElapsedTime(&b, rt->epoch_, tr.end);
+    }
+    t2[2 * n + 0] = a;
+    t2[2 * n + 1] = b;
+    ++n;
+  }
+  return n;
+}
+
+int spmoe_rt_transfer_experts(spmoe_rt* rt, int i, int32_t* experts, int cap) {
+  if (!rt) return 0;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  if (i < 0 || i >= (int)rt->log_.size()) return 0;
+  const auto& v = rt->log_[i].experts;
+  int n = 0;
+  for (; n < (int)v.size() && n < cap; ++n) experts[n] = v[n];
+  return n;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int spmoe_host_alloc_mapped(size_t bytes, void** host, void** dev) {
+  if (!host || !dev) return (int)cudaErrorInvalidValue;
+  cudaError_t e = cudaHostAlloc(host, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
+  if (e != cudaSuccess) return (int)e;
+  return (int)cudaHostGetDevicePointer(dev, *host, 0);
+}
+
+int spmoe_host_free(void* host) { return (int)cudaFreeHost(host); }
+
+int spmoe_host_register(void* host, size_t bytes) {
+  return (int)cudaHostRegister(host, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
+}
+
+int spmoe_host_unregister(void* host) { return (int)cudaHostUnregister(host); }
+
+}  // extern "C"

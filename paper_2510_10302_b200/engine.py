@@ -1,0 +1,586 @@
+"""The real draft/verify decode loop on one B200 (replaces moesim.simcore).
+
+One :class:`SpecMoEEngine` owns, for B independent sequences on one GPU:
+
+* the HBM slot pool ``[capacity, 3*F*H]`` and the native slot-table runtime
+  (LRU metadata, copy stream, per-slot events, prefetch worker thread);
+* the pinned host expert pool (the offload tier);
+* target and draft KV caches and the deterministic random weights.
+
+Per iteration (``Simulation.run`` of ``simcore.py:426-465``):
+
+1. drafting (``_draft_stage`` ``simcore.py:323-354``): N draft steps; at every
+   draft layer l <= cutoff the draft's MLP input is projected through the
+   *target* router l by K1, whose indices land in mapped pinned memory; an
+   event is recorded and the task is pushed to the worker thread
+   (Algorithm 1), which waits on the event, filters resident experts, picks
+   LRU victims and issues batched H2D copies on the copy stream
+   (Algorithm 2).  The draft token chain stays on the device.
+2. verification (``_verify_stage`` ``simcore.py:356-422``) of the N+1 tokens
+   ``[last committed, d_0..d_{N-1}]``: per layer, K1 routes on the GPU, the
+   host reads the indices (zero-copy), touches the union of required experts
+   in ascending order, demand-loads the misses behind queued prefetches
+   (``on_demand_load``), then runs K2 permute, K3 for cache-resident experts
+   first and for each late expert after its slot's ready event (PAPER.md
+   §4.3 cached-first order), and K4 combine + residual.
+3. K6 greedy acceptance: longest matching prefix + correction/bonus token;
+   KV caches roll back by length bookkeeping.
+
+Accounting follows ``SimReport`` (``simcore.py:79-170,467-502``) with device
+times from CUDA events: ``expert_load`` is the time the compute stream sat in
+``cudaStreamWaitEvent`` on slot copies, ``draft`` the drafting span,
+``attention_and_other`` the rest of verification.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .cache import ExpertId, NativeExpertCache
+from .config import HardwareSpec, Policy, PolicySpec, ProfiledTimings, ValidationError, cache_capacity_slots
+from .cutoff import cutoff_input_from_specs, solve_cutoff
+from .model import ArchSpec, HostExpertPool, KVCache, attention, build_weights, model_spec_for, rms_norm
+from .predictor import DraftGuidedPredictor, HistoryCounter, top_k_indices
+from .report import ComputeSlot, IterationRecord, SimReport, TransferKind, TransferRecord
+
+
+def effective_cutoff(model, hw, timings, policy, window_tokens: int = 1) -> int | None:
+    """Cutoff honoured by the engine: explicit override, else the solver's
+    answer (None = infeasible -> no drafting-stage prefetch), clamped to both
+    depths (``simcore.py:182-197``)."""
+    if policy.cutoff_layer is not None:
+        layer = policy.cutoff_layer
+    else:
+        res = solve_cutoff(cutoff_input_from_specs(model, hw, timings, policy.prefetch_k, window_tokens=window_tokens))
+        if not res.feasible:
+            return None
+        layer = res.layer
+    return min(layer, model.draft_layers - 1, model.num_layers - 1)
+
+
+@dataclass
+class _Stall:
+    kind: str  # "prefetch" (waited on an in-flight prefetch) | "demand"
+    layer: int
+    a: torch.cuda.Event
+    b: torch.cuda.Event
+
+
+class _Scratch:
+    """Preallocated per-layer MoE buffers for up to ``T`` tokens."""
+
+    def __init__(self, arch: ArchSpec, T: int, device):
+        H, k = arch.hidden, arch.top_k
+        f32, i32, bf = torch.float32, torch.int32, torch.bfloat16
+        self.T = T
+        self.w = torch.empty((T, k), dtype=f32, device=device)
+        self.idx = torch.empty((T, k), dtype=i32, device=device)
+        self.offsets = torch.empty((arch.num_experts + 1,), dtype=i32, device=device)
+        self.perm = torch.empty((T * k,), dtype=i32, device=device)
+        self.inv = torch.empty((T * k,), dtype=i32, device=device)
+        self.h = torch.empty((T * k, arch.ffn), dtype=bf, device=device)
+        self.y = torch.empty((T * k, H), dtype=f32, device=device)
+        self.hd = torch.empty((T, max(arch.d_ffn, arch.shared_ffn)), dtype=bf, device=device)
+        self.yd = torch.empty((T, H), dtype=f32, device=device)
+        self.pw = torch.empty((T, 64), dtype=f32, device=device)
+        self.pidx = torch.empty((T, 64), dtype=i32, device=device)
+        self._dense: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
+        self.device = device
+
+    def dense(self, T: int):
+        """offsets {0, T} and identity permutation for a dense (1-expert) run."""
+        if T not in self._dense:
+            self._dense[T] = (
+                torch.tensor([0, T], dtype=torch.int32, device=self.device),
+                torch.arange(T, dtype=torch.int32, device=self.device),
+            )
+        return self._dense[T]
+
+
+class SpecMoEEngine:
+    def __init__(
+        self,
+        arch: ArchSpec,
+        hw: HardwareSpec,
+        timings: ProfiledTimings,
+        policy: PolicySpec,
+        *,
+        batch: int = 1,
+        seed: int | None = None,
+        device=None,
+        host_distinct: int | None = None,
+        draft_perturb: float = 0.0,
+        window_tokens: int = 1,
+        max_tokens: int = 1024,
+        record_timeline: bool = False,
+    ):
+        if not torch.cuda.is_available():
+            raise RuntimeError("SpecMoEEngine needs a CUDA device (there is no CPU fallback)")
+        self.arch = arch
+        self.model = model_spec_for(arch)
+        self.hw, self.timings, self.policy = hw, timings, policy
+        self.batch = batch
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.seed = policy.seed if seed is None else seed
+        self.capacity = cache_capacity_slots(self.model, hw, policy)
+        if self.capacity < arch.num_experts:
+            raise ValidationError(
+                f"cache capacity {self.capacity} is below experts_per_layer {arch.num_experts}; "
+                "a single layer could not be loaded"
+            )
+        self.capacity = min(self.capacity, arch.num_layers * arch.num_experts)
+        torch.cuda.set_device(self.device)
+        self.host_pool = HostExpertPool(arch, host_distinct)
+        self.weights = build_weights(arch, self.seed, self.device, self.host_pool, draft_perturb=draft_perturb)
+        self.pool = torch.empty((self.capacity, arch.expert_elems), dtype=torch.bfloat16, device=self.device)
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+        self.cache = NativeExpertCache(
+            self.capacity,
+            arch.num_layers,
+            arch.num_experts,
+            dev_pool_ptr=self.pool.data_ptr(),
+            host_pool_ptr=self.host_pool.ptr,
+            host_index=self.host_pool.index,
+            slot_bytes=arch.expert_bytes,
+            copy_stream_ptr=self.copy_stream.cuda_stream,
+            batched_io=policy.batched_io,
+        )
+        self.cutoff = (
+            effective_cutoff(self.model, hw, timings, policy, window_tokens)
+            if policy.policy is Policy.DRAFT_PREFETCH
+            else None
+        )
+        N = policy.draft_length
+        self.max_tokens = max_tokens
+        self.draft_kv = KVCache(arch, batch, self.device, max_seq=min(arch.max_seq, max_tokens + N + 8))
+        self.target_kv = KVCache(arch, batch, self.device, max_seq=min(arch.max_seq, max_tokens + N + 8))
+        T_max = max(batch * (N + 1), batch * 2, 1)
+        self.scratch = _Scratch(arch, T_max, self.device)
+        self.prefill_scratch: _Scratch | None = None
+        pk = policy.prefetch_k
+        self.predictor = DraftGuidedPredictor(entries=max(N, 1) * arch.num_layers + 1, width=batch * pk)
+        self.pred_w = torch.empty((batch, pk), dtype=torch.float32, device=self.device)
+        self.pred_idx = torch.empty((batch, pk), dtype=torch.int32, device=self.device)
+        # mapped host buffer receiving verify routing (zero-copy hand-off)
+        self.route_ring = DraftGuidedPredictor(entries=1, width=max(T_max * arch.top_k, 1))
+        self._route_ev = torch.cuda.Event()
+        self.history = HistoryCounter(arch.num_layers, arch.num_experts)
+        self._history_bufs: list[np.ndarray] = []
+        self.use_worker = policy.worker_prefetch and policy.policy in (Policy.DRAFT_PREFETCH, Policy.COARSE_HISTORY)
+        if self.use_worker:
+            self.cache.start_worker()
+        self.record_timeline = record_timeline
+        self._reset_run_state()
+
+    # ------------------------------------------------------------------ utils
+    def _reset_run_state(self) -> None:
+        self.stalls: list[_Stall] = []
+        self.iter_records: list[IterationRecord] = []
+        self.slots: list[ComputeSlot] = []
+        self.iter_events: list[tuple[torch.cuda.Event, torch.cuda.Event, torch.cuda.Event]] = []
+        self.draft_ms = 0.0
+        self.verify_ms = 0.0
+        self.stall_ms = {"prefetch": 0.0, "demand": 0.0}
+        self.accepted_total = 0
+        self.drafted_total = 0
+        self.emitted_total = 0
+        self._pending_gating: list[tuple[int, int]] = []  # (layer, slot) waits for gating_next_layer
+
+    @property
+    def stream(self):
+        return torch.cuda.current_stream(self.device)
+
+    def close(self) -> None:
+        try:
+            self.cache.stop_worker()
+            torch.cuda.synchronize(self.device)
+            self.cache.close()
+        finally:
+            self.predictor.close()
+            self.route_ring.close()
+            self.host_pool.close()
+
+    # ------------------------------------------------------------- MoE layers
+    def _dense_ffn(self, blob: torch.Tensor, F: int, xn: torch.Tensor, resid: torch.Tensor, s: _Scratch, out=None):
+        T = xn.shape[0]
+        off, perm = s.dense(T)
+        K.expert_ffn(blob, [0], 1, xn, F, 1, off, perm, s.hd, s.yd, max_tokens_per_expert=T)
+        return K.moe_combine(s.yd, perm, None, T, self.arch.hidden, 1, residual=resid, out=out)
+
+    def _moe_verify(self, l: int, xn: torch.Tensor, resid: torch.Tensor, s: _Scratch) -> torch.Tensor:
+        a = self.arch
+        lw = self.weights.layers[l]
+        T, H = xn.shape
+        k, E = a.top_k, a.num_experts
+        w, idx, _, sg = K.router_topk(
+            xn,
+            lw.router,
+            k,
+            a.renorm,
+            host_idx_dev_ptr=self.route_ring.dev_ptr,
+            shared_gate_w=lw.shared_gate,
+            out=(s.w[:T], s.idx[:T]),
+        )
+        self._route_ev.record()
+        if self.policy.policy is Policy.GATING_NEXT_LAYER and l + 1 < a.num_layers:
+            self._gating_predict(l + 1, xn)
+        self._route_ev.synchronize()
+        ids = self.route_ring.view[0, : T * k].copy()
+        self.history.record_many(l, ids)
+        required = sorted(set(int(e) for e in ids))
+        stream_ptr = self.stream.cuda_stream
+        hits, missing = [], []
+        for e in required:
+            (hits if self.cache.lookup(ExpertId(l, e), touch=True) else missing).append(e)
+        slot = {}
+        ready, late_prefetch = [], []
+        for e in hits:
+            slot[e] = self.cache.slot_of(l, e)
+            (ready if self.cache.slot_ready(slot[e]) else late_prefetch).append(e)
+        if missing:
+            for e, sl in zip(missing, self.cache.demand_load([ExpertId(l, e) for e in missing])):
+                slot[e] = sl
+        offsets, perm, inv = K.moe_permute(idx, E, out=(s.offsets, s.perm[: T * k], s.inv[: T * k]))
+        counts = np.bincount(ids, minlength=E)
+        slots = [slot.get(e, 0) for e in range(E)]
+        maxtok = int(counts.max()) if counts.size else 0
+        if ready:
+            mask = sum(1 << e for e in ready)
+            K.expert_ffn(self.pool, slots, mask, xn, a.ffn, k, offsets, perm, s.h, s.y, maxtok)
+        for kind, group in (("prefetch", late_prefetch), ("demand", missing)):
+            for e in group:
+                ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ea.record()
+                self.cache.wait_slot(slot[e], stream_ptr)
+                eb.record()
+                self.stalls.append(_Stall(kind, l, ea, eb))
+                K.expert_ffn(self.pool, slots, 1 << e, xn, a.ffn, k, offsets, perm, s.h, s.y, int(counts[e]))
+        for e in required:
+            self.cache.mark_read(slot[e], stream_ptr)
+        ys = None
+        if lw.shared is not None:
+            off, pm = s.dense(T)
+            K.expert_ffn(lw.shared, [0], 1, xn, a.shared_ffn, 1, off, pm, s.hd, s.yd, T)
+            ys = s.yd
+        return K.moe_combine(s.y, inv, w, T, H, k, residual=resid, y_shared=ys, shared_gate=sg, out=resid)
+
+    def _gating_predict(self, layer: int, xn: torch.Tensor) -> None:
+        """gating_next_layer baseline: predict layer+1 from this layer's MLP
+        input, blocking prefetch (``vanilla_prefetch_step``, prefetch.py:241-273)."""
+        pk = self.policy.prefetch_k
+        B = self.batch
+        # one token per sequence (the verify position, as simcore.py:407 uses
+        # ``position``): the first of each sequence's verify tokens
+        x_pos = xn.view(B, -1, xn.shape[-1])[:, 0, :].contiguous()
+        i, hptr, ev = self.predictor.predict(
+            x_pos, self.weights.layers[layer].router, pk, True, self.scratch.pw[:B, :pk], self.scratch.pidx[:B, :pk]
+        )
+        self.cache.push_task(layer, hptr, B * pk, ev.cuda_event)
+        self.cache.drain()
+        for e in set(int(v) for v in self.predictor.view[i][: B * pk] if v >= 0):
+            sl = self.cache.slot_of(layer, e)
+            if sl >= 0:
+                self._pending_gating.append((layer, sl))
+
+    # -------------------------------------------------------------- forwards
+    def _embed(self, tokens: torch.Tensor) -> torch.Tensor:
+        return self.weights.embed[tokens]
+
+    def _draft_forward(self, tokens: torch.Tensor, start: torch.Tensor, kv_len_max: int, predict_step: int | None):
+        """Draft pass over ``tokens`` [B, T]; returns last-token logits [B, V] f32.
+        ``predict_step`` (iteration-local draft step index) enables Algorithm 1
+        at layers <= cutoff."""
+        a, w = self.arch, self.weights
+        B, T = tokens.shape
+        x = self._embed(tokens)
+        s = self.scratch if B * T <= self.scratch.T else self._prefill_scratch(B * T)
+        spmoe = predict_step is not None and self.cutoff is not None
+        for l in range(a.num_layers):
+            lw = w.layers[l]
+            h = rms_norm(x, lw.attn_norm, a.rms_eps)
+            x = x + attention(w, l, h, self.draft_kv, start, kv_len_max)
+            hn = rms_norm(x, lw.ffn_norm, a.rms_eps)
+            if spmoe and l <= self.cutoff:
+                self._predict_and_enqueue(l, hn[:, -1, :].contiguous(), predict_step)
+            x = self._dense_ffn(lw.draft_ffn, a.d_ffn, hn.reshape(B * T, -1), x.reshape(B * T, -1), s).view(B, T, -1)
+        hn = rms_norm(x[:, -1, :], w.final_norm, a.rms_eps)
+        return torch.matmul(hn, w.lm_head.t()).float()
+
+    def _predict_and_enqueue(self, l: int, x_last: torch.Tensor, step: int) -> None:
+        pk = self.policy.prefetch_k
+        i, hptr, ev = self.predictor.predict(x_last, self.weights.layers[l].router, pk, True, self.pred_w, self.pred_idx)
+        self.cache.push_task(l, hptr, self.predictor.width, ev.cuda_event, step)
+        if not self.policy.worker_prefetch:
+            # vanilla executor: block until the copies are issued, and make the
+            # next layer wait for them (prefetch.py:241-273)
+            self.cache.drain()
+            sp = self.stream.cuda_stream
+            for e in sorted(set(int(v) for v in self.predictor.view[i] if v >= 0)):
+                sl = self.cache.slot_of(l, e)
+                if sl >= 0 and not self.cache.slot_ready(sl):
+                    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    ea.record()
+                    self.cache.wait_slot(sl, sp)
+                    eb.record()
+                    self.stalls.append(_Stall("prefetch", l, ea, eb))
+
+    def _target_forward(self, tokens: torch.Tensor, start: torch.Tensor, kv_len_max: int, s: _Scratch) -> torch.Tensor:
+        a, w = self.arch, self.weights
+        B, T = tokens.shape
+        x = self._embed(tokens)
+        sp = self.stream.cuda_stream
+        for l in range(a.num_layers):
+            if self._pending_gating:
+                waits = [sl for (ly, sl) in self._pending_gating if ly == l]
+                self._pending_gating = [(ly, sl) for (ly, sl) in self._pending_gating if ly != l]
+                for sl in waits:
+                    if not self.cache.slot_ready(sl):
+                        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        ea.record()
+                        self.cache.wait_slot(sl, sp)
+                        eb.record()
+                        self.stalls.append(_Stall("prefetch", l, ea, eb))
+            lw = w.layers[l]
+            h = rms_norm(x, lw.attn_norm, a.rms_eps)
+            x = x + attention(w, l, h, self.target_kv, start, kv_len_max)
+            hn = rms_norm(x, lw.ffn_norm, a.rms_eps)
+            x = self._moe_verify(l, hn.reshape(B * T, -1).contiguous(), x.reshape(B * T, -1).contiguous(), s).view(B, T, -1)
+        hn = rms_norm(x, w.final_norm, a.rms_eps)
+        return torch.matmul(hn, w.lm_head.t()).float()
+
+    def _prefill_scratch(self, T: int) -> _Scratch:
+        if self.prefill_scratch is None or self.prefill_scratch.T < T:
+            self.prefill_scratch = _Scratch(self.arch, T, self.device)
+            if self.route_ring.width < T * self.arch.top_k:
+                self.route_ring.close()
+                self.route_ring = DraftGuidedPredictor(entries=1, width=T * self.arch.top_k)
+        return self.prefill_scratch
+
+    # ------------------------------------------------------------- SD loop
+    def prefill(self, prompts: torch.Tensor) -> None:
+        """Fill both KV caches with ``prompts[:, :-1]`` (not timed); the last
+        prompt token is processed by the first draft step and verify."""
+        B, P = prompts.shape
+        if B != self.batch or P < 2:
+            raise ValueError("prompts must be [batch, >=2]")
+        self.seqs = [list(map(int, row)) for row in prompts.tolist()]
+        self.draft_len = [P - 1] * B  # positions held by the draft KV
+        ctx = prompts[:, :-1].to(self.device)
+        start = torch.zeros((B,), dtype=torch.int64, device=self.device)
+        s = self._prefill_scratch(B * (P - 1))
+        self._draft_forward(ctx, start, P - 1, None)
+        self._target_forward(ctx, start, P - 1, s)
+        self.cache.drain()
+        torch.cuda.synchronize(self.device)
+        self.cache.reset_stats()
+        self.cache.clear_log()
+        self.history = HistoryCounter(self.arch.num_layers, self.arch.num_experts)
+        self._reset_run_state()
+
+    def _coarse_history_enqueue(self) -> None:
+        pk = self.policy.prefetch_k
+        self._history_bufs = []
+        for l in range(self.arch.num_layers):
+            buf = np.array(top_k_indices(self.history.scores(l), pk), dtype=np.int32)
+            self._history_bufs.append(buf)
+            self.cache.push_task(l, buf.ctypes.data, pk, 0)
+
+    def step(self, remaining: list[int] | None = None) -> list[int]:
+        """One SD iteration for every sequence; returns tokens emitted per
+        sequence (the accepted drafts plus one correction/bonus token)."""
+        a, pol = self.arch, self.policy
+        B = self.batch
+        N = pol.draft_length
+        if remaining is not None and B == 1:
+            N = max(1, min(N, remaining[0]))
+        dev = self.device
+        st = self.stream
+        ev0, ev1, ev2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        self.predictor.reset()
+        ev0.record(st)
+        if pol.policy is Policy.COARSE_HISTORY:
+            self._coarse_history_enqueue()
+        # ---- drafting
+        P = [len(sq) for sq in self.seqs]
+        first = torch.tensor([[sq[-2], sq[-1]] for sq in self.seqs], dtype=torch.int64, device=dev)
+        start = torch.tensor([p - 2 for p in P], dtype=torch.int64, device=dev)
+        drafts = []
+        inp = first
+        for d in range(N):
+            logits = self._draft_forward(inp, start, max(P) + d, d)
+            tok = K.argmax_rows(logits)
+            drafts.append(tok)
+            start = (start + inp.shape[1]) if d == 0 else start + 1
+            inp = tok.long().view(B, 1)
+        draft_tok = torch.stack(drafts, dim=1).contiguous()  # [B, N] int32
+        ev1.record(st)
+        # ---- verification
+        if self.use_worker:
+            self.cache.drain()
+        last = torch.tensor([[sq[-1]] for sq in self.seqs], dtype=torch.int64, device=dev)
+        vtok = torch.cat([last, draft_tok.long()], dim=1)  # [B, N+1]
+        vstart = torch.tensor([p - 1 for p in P], dtype=torch.int64, device=dev)
+        s = self.scratch if B * (N + 1) <= self.scratch.T else self._prefill_scratch(B * (N + 1))
+        logits = self._target_forward(vtok, vstart, max(P) + N, s)
+        _, res = K.greedy_accept(logits.contiguous(), draft_tok)
+        ev2.record(st)
+        res_h = res.cpu().tolist()  # syncs
+        draft_h = draft_tok.cpu().tolist()
+        emitted = []
+        for b in range(B):
+            acc, nxt = res_h[b]
+            new = draft_h[b][:acc] + [nxt]
+            if remaining is not None:
+                new = new[: max(0, remaining[b])]
+            self.seqs[b].extend(new)
+            emitted.append(len(new))
+            self.emitted_total += len(new)
+            self.accepted_total += acc
+        self.drafted_total += N * B
+        self.iter_events.append((ev0, ev1, ev2))
+        self.iter_records.append(
+            IterationRecord(
+                index=len(self.iter_records), start=0.0, draft_end=0.0, verify_end=0.0,
+                position=P[0], drafted=N, accepted=res_h[0][0], emitted=emitted[0],
+            )
+        )
+        return emitted
+
+    def generate(self, prompts: torch.Tensor, max_new_tokens: int) -> SimReport:
+        """Prefill, then SD iterations until every sequence has
+        ``max_new_tokens`` new tokens; returns the SimReport."""
+        self.prefill(prompts)
+        torch.cuda.synchronize(self.device)
+        t0 = time.perf_counter()
+        remaining = [max_new_tokens] * self.batch
+        while any(r > 0 for r in remaining):
+            em = self.step(remaining)
+            remaining = [r - e for r, e in zip(remaining, em)]
+        torch.cuda.synchronize(self.device)
+        wall = time.perf_counter() - t0
+        return self.report(wall_s=wall)
+
+    # -------------------------------------------------------------- report
+    def timing_summary(self) -> dict:
+        torch.cuda.synchronize(self.device)
+        draft = verify = 0.0
+        iters = []
+        t = 0.0
+        for i, (e0, e1, e2) in enumerate(self.iter_events):
+            d = e0.elapsed_time(e1)
+            v = e1.elapsed_time(e2)
+            draft += d
+            verify += v
+            iters.append((t, t + d, t + d + v))
+            t += d + v
+        stall = {"prefetch": 0.0, "demand": 0.0}
+        for s_ in self.stalls:
+            stall[s_.kind] += s_.a.elapsed_time(s_.b)
+        return {"draft_ms": draft, "verify_ms": verify, "stall_ms": stall, "iters": iters}
+
+    def transfers(self) -> list[TransferRecord]:
+        out = []
+        for r in self.cache.transfer_log():
+            if r["end_ms"] < 0:
+                continue
+            out.append(
+                TransferRecord(
+                    start=r["start_ms"] / 1e3,
+                    end=r["end_ms"] / 1e3,
+                    nbytes=r["n_experts"] * self.arch.expert_bytes,
+                    kind=TransferKind.PREFETCH if r["kind"] == "prefetch" else TransferKind.ON_DEMAND,
+                    layer=r["layer"],
+                    experts=r["experts"],
+                )
+            )
+        return out
+
+    def report(self, wall_s: float | None = None) -> SimReport:
+        ts = self.timing_summary()
+        total_ms = ts["draft_ms"] + ts["verify_ms"]
+        stall_total = ts["stall_ms"]["prefetch"] + ts["stall_ms"]["demand"]
+        if total_ms > 0:
+            breakdown = {
+                "draft": ts["draft_ms"] / total_ms,
+                "expert_load": stall_total / total_ms,
+                "attention_and_other": (ts["verify_ms"] - stall_total) / total_ms,
+            }
+        else:
+            breakdown = {"draft": 0.0, "expert_load": 0.0, "attention_and_other": 1.0}
+        c = self.cache.counters()
+        transfers = self.transfers()
+        pre = [t for t in transfers if t.kind is TransferKind.PREFETCH]
+        dem = [t for t in transfers if t.kind is TransferKind.ON_DEMAND]
+        pre_ms = sum(t.duration for t in pre) * 1e3
+        h2d_bytes = sum(t.nbytes for t in transfers)
+        h2d_ms = sum(t.duration for t in transfers) * 1e3
+        iters = [
+            IterationRecord(r.index, it[0] / 1e3, it[1] / 1e3, it[2] / 1e3, r.position, r.drafted, r.accepted, r.emitted)
+            for r, it in zip(self.iter_records, ts["iters"])
+        ]
+        n_emit = self.emitted_total
+        extras = {
+            "batch": self.batch,
+            "acceptance_rate": (self.accepted_total / self.drafted_total) if self.drafted_total else 0.0,
+            "mean_accepted_per_iter": (self.accepted_total / len(self.iter_records)) if self.iter_records else 0.0,
+            "stall_prefetch_ms": ts["stall_ms"]["prefetch"],
+            "stall_demand_ms": ts["stall_ms"]["demand"],
+            "prefetch_copy_ms": pre_ms,
+            "hidden_prefetch_fraction": (1.0 - ts["stall_ms"]["prefetch"] / pre_ms) if pre_ms > 0 else None,
+            "h2d_bytes": h2d_bytes,
+            "h2d_gbs": (h2d_bytes / (h2d_ms / 1e3) / 1e9) if h2d_ms > 0 else None,
+            "n_prefetch_transfers": len(pre),
+            "n_demand_transfers": len(dem),
+            "wall_s": wall_s,
+            "tokens_per_s": n_emit / (total_ms / 1e3) if total_ms > 0 else 0.0,
+            "device_ms": total_ms,
+        }
+        counters = {k_: c[k_] for k_ in (
+            "hits", "misses", "evictions", "prefetch_insertions", "prefetch_evictions",
+            "demand_insertions", "tasks_completed", "tasks_aborted", "evictions_of_queued_targets")}
+        return SimReport(
+            policy=self.policy,
+            seed=self.policy.seed,
+            tpot=(total_ms / 1e3) / n_emit if n_emit else 0.0,
+            hit_rate=self.cache.hit_rate(),
+            eviction_rate=self.cache.eviction_rate(),
+            latency_breakdown=breakdown,
+            total_time=total_ms / 1e3,
+            emitted_tokens=n_emit,
+            cutoff_effective=self.cutoff,
+            cache_capacity=self.capacity,
+            iterations=iters,
+            transfers=transfers,
+            compute_slots=self.slots,
+            counters=counters,
+            extras=extras,
+        )
+
+
+def simulate(model, hw, timings, policy, trace=None, predictor=None, warm_start=False, *, arch=None,
+             prompts=None, max_new_tokens: int = 32, batch: int = 1, **engine_kw) -> SimReport:
+    """``moesim.simulate``-shaped entry point running the real B200 engine.
+
+    ``trace`` and ``predictor`` must be None: routing and prediction come from
+    the model's hidden states (the draft-guided predictor).  ``arch`` gives
+    the shapes (default: inferred preset by name, else 'tiny')."""
+    from .model import ARCH_PRESETS
+
+    if trace is not None or predictor is not None:
+        raise ValidationError("the B200 engine computes routing from hidden states; pass trace=None")
+    if arch is None:
+        arch = ARCH_PRESETS.get(getattr(model, "name", ""), ARCH_PRESETS["tiny"])
+    eng = SpecMoEEngine(arch, hw, timings, policy, batch=batch, **engine_kw)
+    try:
+        if prompts is None:
+            g = torch.Generator().manual_seed(policy.seed)
+            prompts = torch.randint(0, arch.vocab, (batch, 16), generator=g)
+        return eng.generate(prompts, max_new_tokens)
+    finally:
+        eng.close()

@@ -1,0 +1,293 @@
+"""Torch-tensor front end of the sm_100a kernels (K1-K6 of SURVEY.md §2.1).
+
+Thin: validates dtypes/shapes/devices, passes raw pointers and the current
+CUDA stream to the C ABI (:mod:`._native`), returns torch tensors.  No
+computation happens here and there is no fallback path.
+"""
+
+from __future__ import annotations
+
+from typing import Sequence
+
+import torch
+
+from . import _native
+
+BF16 = torch.bfloat16
+F32 = torch.float32
+I32 = torch.int32
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _need(t: torch.Tensor, dtype, name: str, ndim: int | None = None) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if ndim is not None and t.dim() != ndim:
+        raise ValueError(f"{name} must have {ndim} dims, got {t.dim()}")
+
+
+# ---------------------------------------------------------------------------
+# K1
+# ---------------------------------------------------------------------------
+def router_topk(
+    x: torch.Tensor,
+    w_gate: torch.Tensor,
+    k: int,
+    renorm: bool = True,
+    *,
+    want_logits: bool = False,
+    host_idx_dev_ptr: int | None = None,
+    shared_gate_w: torch.Tensor | None = None,
+    out: tuple[torch.Tensor, torch.Tensor] | None = None,
+    stream=None,
+):
+    """Fused router projection + top-k + softmax weights.
+
+    Returns ``(weights f32[T,k], idx i32[T,k], logits f32[T,E] | None,
+    shared_gate f32[T] | None)``.
+    """
+    _need(x, BF16, "x", 2)
+    _need(w_gate, BF16, "w_gate", 2)
+    T, H = x.shape
+    E = w_gate.shape[0]
+    if w_gate.shape[1] != H:
+        raise ValueError("router weight hidden size mismatch")
+    if out is None:
+        weights = torch.empty((T, k), dtype=F32, device=x.device)
+        idx = torch.empty((T, k), dtype=I32, device=x.device)
+    else:
+        weights, idx = out
+    logits = torch.empty((T, E), dtype=F32, device=x.device) if want_logits else None
+    sg = None
+    if shared_gate_w is not None:
+        _need(shared_gate_w, BF16, "shared_gate_w")
+        sg = torch.empty((T,), dtype=F32, device=x.device)
+    _native.call(
+        "spmoe_router_topk",
+        x.data_ptr(),
+        w_gate.data_ptr(),
+        T,
+        H,
+        E,
+        k,
+        1 if renorm else 0,
+        weights.data_ptr(),
+        idx.data_ptr(),
+        _ptr(logits),
+        host_idx_dev_ptr,
+        _ptr(shared_gate_w),
+        _ptr(sg),
+        _stream(stream),
+    )
+    return weights, idx, logits, sg
+
+
+# ---------------------------------------------------------------------------
+# K2
+# ---------------------------------------------------------------------------
+def moe_permute(idx: torch.Tensor, num_experts: int, out=None, stream=None):
+    """Group routed (token, choice) pairs by expert, stable by token."""
+    _need(idx, I32, "idx", 2)
+    T, k = idx.shape
+    if out is None:
+        offsets = torch.empty((num_experts + 1,), dtype=I32, device=idx.device)
+        perm = torch.empty((T * k,), dtype=I32, device=idx.device)
+        inv = torch.empty((T * k,), dtype=I32, device=idx.device)
+    else:
+        offsets, perm, inv = out
+    _native.call(
+        "spmoe_moe_permute",
+        idx.data_ptr(),
+        T,
+        k,
+        num_experts,
+        offsets.data_ptr(),
+        perm.data_ptr(),
+        inv.data_ptr(),
+        _stream(stream),
+    )
+    return offsets, perm, inv
+
+
+# ---------------------------------------------------------------------------
+# K3
+# ---------------------------------------------------------------------------
+def _slot_array(slots: Sequence[int], E: int):
+    import ctypes
+
+    arr = (ctypes.c_int32 * max(E, 1))()
+    for e in range(E):
+        arr[e] = int(slots[e]) if slots[e] is not None and slots[e] >= 0 else 0
+    return arr
+
+
+def expert_ffn(
+    pool: torch.Tensor,
+    slot_of_expert: Sequence[int],
+    expert_mask: int,
+    x: torch.Tensor,
+    ffn_dim: int,
+    top_k: int,
+    offsets: torch.Tensor,
+    perm: torch.Tensor,
+    h_scratch: torch.Tensor,
+    y: torch.Tensor,
+    max_tokens_per_expert: int = 0,
+    phase: str = "both",
+    stream=None,
+) -> None:
+    """Grouped SwiGLU of the experts in ``expert_mask`` reading the slot pool.
+
+    ``pool`` is ``[S, 3*F*H]`` bf16 (one expert blob per slot); ``y`` receives
+    ``[T*k, H]`` fp32 rows in permuted order.
+    """
+    _need(pool, BF16, "pool", 2)
+    _need(x, BF16, "x", 2)
+    T, H = x.shape
+    E = len(slot_of_expert)
+    slot_elems = pool.shape[1]
+    if slot_elems < 3 * ffn_dim * H:
+        raise ValueError("slot too small for the expert blob")
+    slots = _slot_array(slot_of_expert, E)
+    st = _stream(stream)
+    if phase in ("both", "up"):
+        _native.call(
+            "spmoe_expert_ffn_up",
+            pool.data_ptr(),
+            slot_elems,
+            slots,
+            expert_mask,
+            x.data_ptr(),
+            T,
+            H,
+            ffn_dim,
+            E,
+            top_k,
+            offsets.data_ptr(),
+            perm.data_ptr(),
+            h_scratch.data_ptr(),
+            max_tokens_per_expert,
+            st,
+        )
+    if phase in ("both", "down"):
+        _native.call(
+            "spmoe_expert_ffn_down",
+            pool.data_ptr(),
+            slot_elems,
+            slots,
+            expert_mask,
+            T,
+            H,
+            ffn_dim,
+            E,
+            top_k,
+            offsets.data_ptr(),
+            h_scratch.data_ptr(),
+            y.data_ptr(),
+            max_tokens_per_expert,
+            st,
+        )
+
+
+# ---------------------------------------------------------------------------
+# K4
+# ---------------------------------------------------------------------------
+def moe_combine(
+    y: torch.Tensor | None,
+    inv_pos: torch.Tensor | None,
+    weights: torch.Tensor | None,
+    T: int,
+    H: int,
+    k: int,
+    *,
+    residual: torch.Tensor | None = None,
+    y_shared: torch.Tensor | None = None,
+    shared_gate: torch.Tensor | None = None,
+    out: torch.Tensor | None = None,
+    device=None,
+    stream=None,
+) -> torch.Tensor:
+    dev = device or (y.device if y is not None else residual.device)
+    if out is None:
+        out = torch.empty((T, H), dtype=BF16, device=dev)
+    _native.call(
+        "spmoe_moe_combine",
+        _ptr(y),
+        _ptr(inv_pos),
+        _ptr(weights),
+        T,
+        H,
+        k,
+        _ptr(y_shared),
+        _ptr(shared_gate),
+        _ptr(residual),
+        out.data_ptr(),
+        _stream(stream),
+    )
+    return out
+
+
+# ---------------------------------------------------------------------------
+# K6
+# ---------------------------------------------------------------------------
+def greedy_accept(logits: torch.Tensor, draft: torch.Tensor, stream=None):
+    """logits f32 [B, N+1, V]; draft i32 [B, N] -> (argmax [B,N+1], result [B,2])."""
+    _need(logits, F32, "logits", 3)
+    B, N1, V = logits.shape
+    N = N1 - 1
+    if N > 0:
+        _need(draft, I32, "draft", 2)
+    amax = torch.empty((B, N1), dtype=I32, device=logits.device)
+    res = torch.empty((B, 2), dtype=I32, device=logits.device)
+    _native.call(
+        "spmoe_greedy_accept",
+        logits.data_ptr(),
+        V,
+        draft.data_ptr() if N > 0 else None,
+        B,
+        N,
+        V,
+        amax.data_ptr(),
+        res.data_ptr(),
+        _stream(stream),
+    )
+    return amax, res
+
+
+def argmax_rows(logits: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    _need(logits, F32, "logits", 2)
+    R, V = logits.shape
+    if out is None:
+        out = torch.empty((R,), dtype=I32, device=logits.device)
+    _native.call("spmoe_argmax_rows", logits.data_ptr(), V, R, V, out.data_ptr(), _stream(stream))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# init
+# ---------------------------------------------------------------------------
+def fill_normal_(t: torch.Tensor, seed: int, offset: int = 0, std: float = 0.02, stream=None):
+    """Deterministic counter-hash N(0, std^2) fill (bit-identical on CPU)."""
+    _need(t, BF16, "t")
+    _native.call(
+        "spmoe_fill_normal_bf16",
+        t.data_ptr(),
+        t.numel(),
+        seed & 0xFFFFFFFFFFFFFFFF,
+        offset & 0xFFFFFFFFFFFFFFFF,
+        float(std),
+        _stream(stream),
+    )
+    return t

@@ -1,0 +1,425 @@
+"""Model shapes, deterministic random weights, the pinned host expert pool and
+the non-MoE transformer pieces of the draft/target pair.
+
+The reference simulates model behaviour with activation traces
+(``trace.py:103-173``); the B200 build runs real (random-init) weights of the
+named shapes so that routing, prediction and acceptance come out of actual
+hidden states.  Everything here is plumbing around the hot path:
+
+* :class:`ArchSpec` — hidden size, heads, expert width ... plus presets for
+  the BASELINE.json configs (tiny, Mixtral-8x7B, DeepSeek-V2-Lite,
+  Qwen1.5-MoE-A2.7B).  Attention is standard GQA/MHA for every preset (the
+  verify-time expert path does not depend on DeepSeek's MLA).
+* :class:`HostExpertPool` — every routed expert of every layer as one
+  contiguous bf16 blob ``W1[F,H] | W3[F,H] | W2[H,F]`` in page-locked host
+  memory (the offload tier), generated on the GPU with the counter-hash init
+  and copied down.
+* :class:`ModelWeights` — device-resident embedding, attention, norms, router,
+  shared experts, lm_head, and the draft's dense FFN.  The draft shares the
+  target's embedding, attention and lm_head (SURVEY.md §7 hard part 2) and
+  uses the mean of the layer's experts as its FFN, optionally perturbed.
+* attention / RoPE / RMSNorm in torch (cuBLAS GEMMs + SDPA): not on the hot
+  path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import asdict, dataclass, replace
+from pathlib import Path
+
+import numpy as np
+import torch
+import yaml
+
+from .config import ModelSpec, ValidationError
+
+MASK64 = (1 << 64) - 1
+
+
+# ---------------------------------------------------------------------------
+# shapes
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class ArchSpec:
+    name: str
+    vocab: int
+    hidden: int
+    num_layers: int
+    num_heads: int
+    num_kv_heads: int
+    head_dim: int
+    ffn: int  # routed expert intermediate size
+    num_experts: int  # routed experts per layer
+    top_k: int
+    renorm: bool = True  # Mixtral: renormalise top-k; DeepSeek/Qwen: no
+    shared_ffn: int = 0  # total intermediate size of the shared expert(s)
+    shared_gate: bool = False  # Qwen1.5-MoE sigmoid gate on the shared expert
+    draft_ffn: int = 0  # draft dense FFN width (0 -> ffn)
+    rope_theta: float = 1e6
+    rms_eps: float = 1e-5
+    max_seq: int = 2048
+    init_std: float = 0.02
+    expert_out_scale: float = 1.0  # scales W2 std (residual-branch scaling)
+
+    def __post_init__(self):
+        if self.hidden % 8 or self.ffn % 8 or (self.shared_ffn % 8):
+            raise ValidationError("hidden and ffn sizes must be multiples of 8")
+        if not 1 <= self.top_k <= self.num_experts <= 64:
+            raise ValidationError("need 1 <= top_k <= num_experts <= 64")
+        if self.num_heads % self.num_kv_heads:
+            raise ValidationError("num_heads must be a multiple of num_kv_heads")
+
+    @property
+    def expert_elems(self) -> int:
+        return 3 * self.ffn * self.hidden
+
+    @property
+    def expert_bytes(self) -> int:
+        return 2 * self.expert_elems
+
+    @property
+    def d_ffn(self) -> int:
+        return self.draft_ffn or self.ffn
+
+    @property
+    def qkv_dim(self) -> int:
+        return (self.num_heads + 2 * self.num_kv_heads) * self.head_dim
+
+
+ARCH_PRESETS: dict[str, ArchSpec] = {
+    # BASELINE config #1: tiny Mixtral-style target (4 layers, 8 experts top-2,
+    # hidden 256); vocab kept small so the CPU oracle finishes in seconds.
+    "tiny": ArchSpec(
+        name="tiny", vocab=512, hidden=256, num_layers=4, num_heads=4, num_kv_heads=2,
+        head_dim=64, ffn=512, num_experts=8, top_k=2, max_seq=512,
+    ),
+    # BASELINE config #2: Mixtral-8x7B shapes (HF config)
+    "mixtral_8x7b": ArchSpec(
+        name="mixtral_8x7b", vocab=32000, hidden=4096, num_layers=32, num_heads=32,
+        num_kv_heads=8, head_dim=128, ffn=14336, num_experts=8, top_k=2, rope_theta=1e6,
+        max_seq=1024,
+    ),
+    # BASELINE config #3: DeepSeek-V2-Lite MoE shapes (64 routed + 2 shared of
+    # 1408, top-6, no top-k renorm); 27 MoE layers as in the reference ModelSpec
+    "deepseek_v2_lite": ArchSpec(
+        name="deepseek_v2_lite", vocab=102400, hidden=2048, num_layers=27, num_heads=16,
+        num_kv_heads=16, head_dim=128, ffn=1408, num_experts=64, top_k=6, renorm=False,
+        shared_ffn=2 * 1408, rope_theta=1e4, rms_eps=1e-6, max_seq=1024,
+    ),
+    # BASELINE config #4: Qwen1.5-MoE-A2.7B shapes (60 routed top-4, shared
+    # expert 5632 with sigmoid gate)
+    "qwen15_moe_a27b": ArchSpec(
+        name="qwen15_moe_a27b", vocab=151936, hidden=2048, num_layers=24, num_heads=16,
+        num_kv_heads=16, head_dim=128, ffn=1408, num_experts=60, top_k=4, renorm=False,
+        shared_ffn=5632, shared_gate=True, rope_theta=1e6, rms_eps=1e-6, max_seq=1024,
+    ),
+}
+
+
+def get_arch(name_or_spec, **overrides) -> ArchSpec:
+    a = ARCH_PRESETS[name_or_spec] if isinstance(name_or_spec, str) else name_or_spec
+    return replace(a, **overrides) if overrides else a
+
+
+def load_arch(path: str | Path) -> ArchSpec | None:
+    """The optional ``arch`` section of an experiment file (None if absent).
+    ``arch: {preset: mixtral_8x7b, ...overrides}`` or a full field list."""
+    doc = yaml.safe_load(Path(path).read_text())
+    sec = (doc or {}).get("arch")
+    if sec is None:
+        return None
+    sec = dict(sec)
+    preset = sec.pop("preset", None)
+    if preset is not None:
+        return get_arch(preset, **sec)
+    return ArchSpec(**sec)
+
+
+def model_spec_for(arch: ArchSpec, draft_layers: int | None = None) -> ModelSpec:
+    """The reference ModelSpec of an arch (routed experts only: shared experts
+    stay resident outside the cache budget, SURVEY.md §7 hard part 8)."""
+    return ModelSpec(
+        name=arch.name,
+        num_layers=arch.num_layers,
+        experts_per_layer=arch.num_experts,
+        topk_activated=arch.top_k,
+        shared_experts=0,
+        expert_size=arch.expert_bytes,
+        draft_layers=draft_layers or arch.num_layers,
+        draft_topk=0,
+    )
+
+
+def arch_dict(arch: ArchSpec) -> dict:
+    return asdict(arch)
+
+
+# ---------------------------------------------------------------------------
+# deterministic init
+# ---------------------------------------------------------------------------
+def _splitmix64(x: int) -> int:
+    x = (x + 0x9E3779B97F4A7C15) & MASK64
+    z = x
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+    return z ^ (z >> 31)
+
+
+def tensor_seed(base: int, *ids: int) -> int:
+    """64-bit seed of one named tensor (ids: kind code, layer, expert ...)."""
+    h = _splitmix64(base & MASK64)
+    for v in ids:
+        h = _splitmix64(h ^ (v & MASK64))
+    return h
+
+
+# kind codes for tensor_seed
+K_EMBED, K_QKV, K_WO, K_ROUTER, K_EXPERT, K_SHARED, K_SGATE, K_LMHEAD, K_PERTURB = range(9)
+
+
+# ---------------------------------------------------------------------------
+# host expert pool
+# ---------------------------------------------------------------------------
+class HostExpertPool:
+    """Page-locked host memory holding every routed expert blob.
+
+    ``index[l*E + e]`` is the pool row of expert (l, e); with ``distinct`` <
+    L*E rows, experts alias rows (bounded host RAM; the bytes moved per copy
+    are unchanged).  Allocated with cudaHostAlloc (exact size, portable,
+    mapped) through the native library.
+    """
+
+    def __init__(self, arch: ArchSpec, distinct: int | None = None):
+        from . import _native
+
+        self.arch = arch
+        n = arch.num_layers * arch.num_experts
+        self.rows = n if not distinct else min(int(distinct), n)
+        self.index = [i % self.rows for i in range(n)]
+        self.slot_bytes = arch.expert_bytes
+        self.nbytes = self.rows * self.slot_bytes
+        self._lib = _native.load()
+        host = C.c_void_p()
+        dev = C.c_void_p()
+        _native.check(
+            "spmoe_host_alloc_mapped",
+            self._lib.spmoe_host_alloc_mapped(self.nbytes, C.byref(host), C.byref(dev)),
+        )
+        self.ptr = host.value
+        buf = (C.c_uint16 * (self.rows * arch.expert_elems)).from_address(self.ptr)
+        self.array = np.ctypeslib.as_array(buf).reshape(self.rows, arch.expert_elems)
+        self.tensor = torch.from_numpy(self.array.view(np.int16)).view(torch.bfloat16)
+
+    def row_of(self, layer: int, expert: int) -> int:
+        return self.index[layer * self.arch.num_experts + expert]
+
+    def blob(self, layer: int, expert: int) -> torch.Tensor:
+        return self.tensor[self.row_of(layer, expert)]
+
+    def close(self) -> None:
+        if getattr(self, "ptr", None):
+            self.tensor = None
+            self.array = None
+            self._lib.spmoe_host_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+
+# ---------------------------------------------------------------------------
+# device weights
+# ---------------------------------------------------------------------------
+@dataclass
+class LayerWeights:
+    attn_norm: torch.Tensor
+    wqkv: torch.Tensor
+    wo: torch.Tensor
+    ffn_norm: torch.Tensor
+    router: torch.Tensor
+    shared: torch.Tensor | None  # [1, 3*Fs*H] blob
+    shared_gate: torch.Tensor | None  # [H]
+    draft_ffn: torch.Tensor  # [1, 3*Fd*H] blob
+
+
+@dataclass
+class ModelWeights:
+    arch: ArchSpec
+    embed: torch.Tensor
+    layers: list[LayerWeights]
+    final_norm: torch.Tensor
+    lm_head: torch.Tensor
+    rope_cos: torch.Tensor
+    rope_sin: torch.Tensor
+
+
+def _fill(t: torch.Tensor, seed: int, std: float) -> torch.Tensor:
+    from .kernels import fill_normal_
+
+    return fill_normal_(t, seed, 0, std)
+
+
+def build_weights(
+    arch: ArchSpec,
+    seed: int,
+    device: torch.device,
+    host_pool: HostExpertPool | None,
+    draft_perturb: float = 0.0,
+    chunk_experts: int = 8,
+) -> ModelWeights:
+    """Generate every tensor on the GPU with the counter-hash init; routed
+    experts stream to ``host_pool`` (if given) in chunks while their fp32 mean
+    accumulates into the draft FFN."""
+    H, E, F = arch.hidden, arch.num_experts, arch.ffn
+    bf = torch.bfloat16
+    std = arch.init_std
+    embed = _fill(torch.empty((arch.vocab, H), dtype=bf, device=device), tensor_seed(seed, K_EMBED), std)
+    lm_head = _fill(torch.empty((arch.vocab, H), dtype=bf, device=device), tensor_seed(seed, K_LMHEAD), std)
+    layers = []
+    stage = torch.empty((min(chunk_experts, E), arch.expert_elems), dtype=bf, device=device)
+    for l in range(arch.num_layers):
+        wqkv = _fill(torch.empty((arch.qkv_dim, H), dtype=bf, device=device), tensor_seed(seed, K_QKV, l), std)
+        wo = _fill(
+            torch.empty((H, arch.num_heads * arch.head_dim), dtype=bf, device=device),
+            tensor_seed(seed, K_WO, l),
+            std,
+        )
+        router = _fill(torch.empty((E, H), dtype=bf, device=device), tensor_seed(seed, K_ROUTER, l), 1.0 / math.sqrt(H))
+        acc = torch.zeros((arch.expert_elems,), dtype=torch.float32, device=device)
+        for e0 in range(0, E, stage.shape[0]):
+            n = min(stage.shape[0], E - e0)
+            for j in range(n):
+                row = host_pool.row_of(l, e0 + j) if host_pool is not None else l * E + e0 + j
+                fill_expert_blob(stage[j], arch, seed, row)
+                acc += stage[j].float()
+            if host_pool is not None:
+                for j in range(n):
+                    host_pool.blob(l, e0 + j).copy_(stage[j], non_blocking=False)
+        mean = (acc / E).to(bf)
+        del acc
+        if arch.d_ffn != F:
+            draft = torch.empty((1, 3 * arch.d_ffn * H), dtype=bf, device=device)
+            fill_blob_generic(draft[0], arch.d_ffn, H, tensor_seed(seed, K_EXPERT, l, 10_000), std, arch.expert_out_scale)
+        else:
+            draft = mean.view(1, -1).clone()
+        if draft_perturb > 0.0:
+            noise = torch.empty_like(draft)
+            _fill(noise, tensor_seed(seed, K_PERTURB, l), std * draft_perturb)
+            draft = (draft.float() + noise.float()).to(bf)
+        shared = None
+        sgate = None
+        if arch.shared_ffn:
+            shared = torch.empty((1, 3 * arch.shared_ffn * H), dtype=bf, device=device)
+            fill_blob_generic(shared[0], arch.shared_ffn, H, tensor_seed(seed, K_SHARED, l), std, arch.expert_out_scale)
+            if arch.shared_gate:
+                sgate = _fill(torch.empty((H,), dtype=bf, device=device), tensor_seed(seed, K_SGATE, l), 1.0 / math.sqrt(H))
+        layers.append(
+            LayerWeights(
+                attn_norm=torch.ones((H,), dtype=bf, device=device),
+                wqkv=wqkv,
+                wo=wo,
+                ffn_norm=torch.ones((H,), dtype=bf, device=device),
+                router=router,
+                shared=shared,
+                shared_gate=sgate,
+                draft_ffn=draft,
+            )
+        )
+    del stage
+    cos, sin = rope_tables(arch, device)
+    return ModelWeights(
+        arch=arch,
+        embed=embed,
+        layers=layers,
+        final_norm=torch.ones((H,), dtype=bf, device=device),
+        lm_head=lm_head,
+        rope_cos=cos,
+        rope_sin=sin,
+    )
+
+
+def fill_blob_generic(blob: torch.Tensor, F: int, H: int, seed: int, std: float, out_scale: float) -> None:
+    """W1|W3 ~ N(0, std^2), W2 ~ N(0, (std*out_scale)^2), each with its own
+    counter stream (offset 0 of three sub-seeds)."""
+    n13 = F * H
+    _fill(blob[:n13], _splitmix64(seed ^ 1), std)
+    _fill(blob[n13 : 2 * n13], _splitmix64(seed ^ 3), std)
+    _fill(blob[2 * n13 : 3 * n13], _splitmix64(seed ^ 2), std * out_scale)
+
+
+def fill_expert_blob(blob: torch.Tensor, arch: ArchSpec, seed: int, row: int) -> None:
+    """Routed expert content is a function of its host-pool row (row =
+    layer*E + expert unless the pool aliases)."""
+    fill_blob_generic(
+        blob, arch.ffn, arch.hidden, tensor_seed(seed, K_EXPERT, row), arch.init_std, arch.expert_out_scale
+    )
+
+
+# ---------------------------------------------------------------------------
+# transformer pieces (torch; off the hot path)
+# ---------------------------------------------------------------------------
+def rope_tables(arch: ArchSpec, device) -> tuple[torch.Tensor, torch.Tensor]:
+    d = arch.head_dim
+    inv = 1.0 / (arch.rope_theta ** (torch.arange(0, d, 2, dtype=torch.float64, device=device) / d))
+    pos = torch.arange(arch.max_seq, dtype=torch.float64, device=device)
+    ang = torch.outer(pos, inv)
+    ang = torch.cat([ang, ang], dim=-1)
+    return ang.cos().float(), ang.sin().float()
+
+
+def rms_norm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
+    xf = x.float()
+    y = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)
+    return (y * w.float()).to(x.dtype)
+
+
+def _rotate_half(x: torch.Tensor) -> torch.Tensor:
+    h = x.shape[-1] // 2
+    return torch.cat([-x[..., h:], x[..., :h]], dim=-1)
+
+
+class KVCache:
+    """Per-model KV cache ``[L, B, S, n_kv, hd]`` with per-sequence lengths."""
+
+    def __init__(self, arch: ArchSpec, batch: int, device, max_seq: int | None = None):
+        S = max_seq or arch.max_seq
+        shape = (arch.num_layers, batch, S, arch.num_kv_heads, arch.head_dim)
+        self.k = torch.zeros(shape, dtype=torch.bfloat16, device=device)
+        self.v = torch.zeros(shape, dtype=torch.bfloat16, device=device)
+        self.max_seq = S
+
+
+def attention(
+    w: ModelWeights,
+    layer: int,
+    x_norm: torch.Tensor,  # [B, T, H]
+    kv: KVCache,
+    start: torch.Tensor,  # [B] int64 position of the first of the T tokens
+    kv_len_max: int,  # max over b of start[b] + T
+) -> torch.Tensor:
+    a = w.arch
+    B, T, H = x_norm.shape
+    lw = w.layers[layer]
+    qkv = torch.matmul(x_norm, lw.wqkv.t())
+    nh, nkv, hd = a.num_heads, a.num_kv_heads, a.head_dim
+    q, k, v = torch.split(qkv, [nh * hd, nkv * hd, nkv * hd], dim=-1)
+    q = q.view(B, T, nh, hd)
+    k = k.view(B, T, nkv, hd)
+    v = v.view(B, T, nkv, hd)
+    pos = start.view(B, 1) + torch.arange(T, device=x_norm.device).view(1, T)  # [B, T]
+    cos = w.rope_cos[pos].unsqueeze(2)  # [B, T, 1, hd]
+    sin = w.rope_sin[pos].unsqueeze(2)
+    q = (q.float() * cos + _rotate_half(q.float()) * sin).to(torch.bfloat16)
+    k = (k.float() * cos + _rotate_half(k.float()) * sin).to(torch.bfloat16)
+    bidx = torch.arange(B, device=x_norm.device).view(B, 1).expand(B, T)
+    kv.k[layer][bidx, pos] = k
+    kv.v[layer][bidx, pos] = v
+    Lk = kv_len_max
+    keys = kv.k[layer][:, :Lk].permute(0, 2, 1, 3)  # [B, nkv, Lk, hd]
+    vals = kv.v[layer][:, :Lk].permute(0, 2, 1, 3)
+    kpos = torch.arange(Lk, device=x_norm.device).view(1, 1, Lk)
+    mask = (kpos <= pos.view(B, T, 1)).unsqueeze(1)  # [B, 1, T, Lk]
+    o = torch.nn.functional.scaled_dot_product_attention(
+        q.permute(0, 2, 1, 3), keys, vals, attn_mask=mask, enable_gqa=(nkv != nh)
+    )
+    o = o.permute(0, 2, 1, 3).reshape(B, T, nh * hd)
+    return torch.matmul(o, lw.wo.t())

@@ -1,0 +1,5 @@
+import sys
+
+import paper_2510_10302_b200.cache as _impl
+
+sys.modules[__name__] = _impl

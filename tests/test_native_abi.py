@@ -1,0 +1,120 @@
+"""C-ABI library checks that need no GPU: libspmoe.so loads, exports every
+function include/spmoe.h declares (and the ctypes binding covers them), the
+oracle library builds, and the native LRU slot cache honours the reference
+cache contract (metadata path only, no copies)."""
+
+from __future__ import annotations
+
+import random
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_functions() -> list[str]:
+    text = (ROOT / "include" / "spmoe.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(spmoe_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_hot_path_entry_points():
+    names = declared_functions()
+    for required in ("spmoe_router_topk", "spmoe_moe_permute", "spmoe_expert_ffn", "spmoe_moe_combine",
+                     "spmoe_greedy_accept", "spmoe_h2d_batch", "spmoe_rt_push_task", "spmoe_rt_demand_load"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(native):
+    from paper_2510_10302_b200 import _native
+
+    for name in declared_functions():
+        assert hasattr(native, name), f"libspmoe.so does not export {name}"
+        assert name in _native.SIGNATURES, f"ctypes binding lacks {name}"
+    assert native.spmoe_abi_version() == 100
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    lib = ROOT / "paper_2510_10302_b200" / "libspmoe.so"
+    out = subprocess.run(["cuobjdump", "--list-elf", str(lib)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_invalid_arguments_return_status_not_crash(native):
+    # bad shapes are rejected before any launch (no GPU needed)
+    assert native.spmoe_router_topk(None, None, 4, 12, 8, 2, 1, None, None, None, None, None, None, None) == 1
+    assert native.spmoe_moe_permute(None, 4, 0, 8, None, None, None, None) == 1
+    assert native.spmoe_moe_combine(None, None, None, 2, 6, 1, None, None, None, None, None) == 1
+
+
+def test_oracle_library_builds(oracle):
+    assert oracle.lib().oracle_num_threads() >= 1
+
+
+def test_native_lru_matches_reference_contract(native):
+    from paper_2510_10302_b200.cache import CacheError, ExpertCache, ExpertId, InsertKind, NativeExpertCache
+
+    rng = random.Random(7)
+    for trial in range(8):
+        cap = rng.randint(1, 10)
+        ref = ExpertCache(cap)
+        nat = NativeExpertCache(cap, 4, 16)
+        try:
+            for _ in range(400):
+                r = rng.random()
+                if r < 0.45:
+                    e = ExpertId(rng.randrange(4), rng.randrange(16))
+                    t = rng.random() < 0.7
+                    assert nat.lookup(e, t) == ref.lookup(e, t)
+                elif r < 0.85:
+                    ids = [ExpertId(rng.randrange(4), rng.randrange(16)) for _ in range(rng.randint(1, 4))]
+                    kind = InsertKind.PREFETCH if rng.random() < 0.5 else InsertKind.DEMAND
+                    try:
+                        want = ref.insert_batch(ids, kind)
+                    except CacheError:
+                        with pytest.raises(CacheError):
+                            nat.insert_batch(ids, kind)
+                        continue
+                    assert nat.insert_batch(ids, kind) == want
+                elif r < 0.93 and ref.lru_order:
+                    e = ref.lru_order[rng.randrange(len(ref.lru_order))]
+                    ref.pin([e])
+                    nat.pin([e])
+                else:
+                    if ref.pinned:
+                        e = sorted(ref.pinned)[0]
+                        ref.unpin([e])
+                        nat.unpin([e])
+                assert nat.lru_order == ref.lru_order
+            c = nat.counters()
+            for k in ("hits", "misses", "evictions", "prefetch_evictions", "prefetch_insertions", "demand_insertions"):
+                assert c[k] == getattr(ref, k)
+            # every resident expert holds a distinct slot in [0, cap)
+            slots = [nat.slot_of(*e) for e in nat.lru_order]
+            assert sorted(slots) == sorted(set(slots)) and all(0 <= s < cap for s in slots)
+        finally:
+            nat.close()
+
+
+def test_native_slot_assignment_matches_policy_oracle(native):
+    from oracle.policy_oracle import NaiveLRU
+    from paper_2510_10302_b200.cache import ExpertId, InsertKind, NativeExpertCache
+
+    rng = random.Random(11)
+    cap = 6
+    ora = NaiveLRU(cap)
+    nat = NativeExpertCache(cap, 4, 8)
+    try:
+        for _ in range(300):
+            ids = [(rng.randrange(4), rng.randrange(8)) for _ in range(rng.randint(1, 3))]
+            kind = "prefetch" if rng.random() < 0.5 else "demand"
+            ora.insert_batch(ids, kind)
+            nat.insert_batch([ExpertId(*e) for e in ids], InsertKind(kind))
+            for e in ora.order:
+                assert nat.slot_of(*e) == ora.slot[e]
+    finally:
+        nat.close()
