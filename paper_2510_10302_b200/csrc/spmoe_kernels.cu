@@ -289,15 +289,19 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_down_kernel(const FfnParam
   const int lane = threadIdx.x & 31;
   const int gwarp = blockIdx.x * (kFfnThreads / 32) + (threadIdx.x >> 5);
   const int nwarps = gridDim.x * (kFfnThreads / 32);
-  const int64_t total = (int64_t)n_active * p.H;
+  // a warp owns the row pair (h, h+1) of W2 so every activation chunk it
+  // loads feeds two weight chunks (as W1/W3 do in the up phase); H is even
+  const int half = p.H >> 1;
+  const int64_t total = (int64_t)n_active * half;
   const int nchunks = p.F >> 3;
   for (int64_t u = gwarp; u < total; u += nwarps) {
-    const int a = (int)(u / p.H);
-    const int hrow = (int)(u - (int64_t)a * p.H);
+    const int a = (int)(u / half);
+    const int hrow = 2 * (int)(u - (int64_t)a * half);
     const int e = s_active[a];
     const uint16_t* blob = p.pool + (int64_t)p.slot[e] * p.slot_elems;
-    const uint4* const wr[1] = {
-        reinterpret_cast<const uint4*>(blob + 2 * (int64_t)p.F * p.H + (int64_t)hrow * p.F)};
+    const uint16_t* w2 = blob + 2 * (int64_t)p.F * p.H + (int64_t)hrow * p.F;
+    const uint4* const wr[2] = {reinterpret_cast<const uint4*>(w2),
+                                reinterpret_cast<const uint4*>(w2 + p.F)};
     const int off = s_off[e];
     const int cnt = s_off[e + 1] - off;
     for (int t0 = 0; t0 < cnt; t0 += TT) {
@@ -306,15 +310,17 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_down_kernel(const FfnParam
 #pragma unroll
       for (int t = 0; t < TT; ++t)
         ar[t] = reinterpret_cast<const uint4*>(p.h + (int64_t)(off + t0 + min(t, nt - 1)) * p.F);
-      float acc[1][TT];
+      float acc[2][TT];
 #pragma unroll
-      for (int t = 0; t < TT; ++t) acc[0][t] = 0.0f;
-      stream_rows<TT, 1, 16>(wr, ar, nt, nchunks, lane, acc);
+      for (int t = 0; t < TT; ++t) { acc[0][t] = 0.0f; acc[1][t] = 0.0f; }
+      stream_rows<TT, 2, 8>(wr, ar, nt, nchunks, lane, acc);
 #pragma unroll
       for (int t = 0; t < TT; ++t) {
         if (t < nt) {
-          const float yv = warp_sum_fixed(acc[0][t]);
-          if (lane == t) p.y[(int64_t)(off + t0 + t) * p.H + hrow] = yv;
+          const float y0 = warp_sum_fixed(acc[0][t]);
+          const float y1 = warp_sum_fixed(acc[1][t]);
+          if (lane == t)
+            *reinterpret_cast<float2*>(p.y + (int64_t)(off + t0 + t) * p.H + hrow) = make_float2(y0, y1);
         }
       }
     }

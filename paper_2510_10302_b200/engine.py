@@ -119,6 +119,8 @@ class SpecMoEEngine:
         window_tokens: int = 1,
         max_tokens: int = 1024,
         record_timeline: bool = False,
+        record: bool = False,
+        capture_layers: tuple[int, ...] = (),
     ):
         if not torch.cuda.is_available():
             raise RuntimeError("SpecMoEEngine needs a CUDA device (there is no CPU fallback)")
@@ -176,6 +178,8 @@ class SpecMoEEngine:
         if self.use_worker:
             self.cache.start_worker()
         self.record_timeline = record_timeline
+        self.record = record
+        self.capture_layers = set(capture_layers)
         self._reset_run_state()
 
     # ------------------------------------------------------------------ utils
@@ -191,6 +195,12 @@ class SpecMoEEngine:
         self.drafted_total = 0
         self.emitted_total = 0
         self._pending_gating: list[tuple[int, int]] = []  # (layer, slot) waits for gating_next_layer
+        self._pushed: list[tuple[int, object]] = []  # (layer, ring row | host array) not yet logged
+        # program-order log of cache-mutating decisions, for oracle replay:
+        # ("task", layer, ids) when a prefetch task is consumed, ("verify",
+        # layer, routed ids) at each verify layer
+        self.decisions: list[tuple[str, int, list[int]]] = []
+        self.captures: list[dict] = []
 
     @property
     def stream(self):
@@ -207,6 +217,16 @@ class SpecMoEEngine:
             self.host_pool.close()
 
     # ------------------------------------------------------------- MoE layers
+    def _drain(self) -> None:
+        """Wait for the worker to consume every pushed task; log them in FIFO
+        (= consumption) order."""
+        self.cache.drain()
+        if self.record:
+            for layer, src in self._pushed:
+                ids = [int(v) for v in (self.predictor.view[src] if isinstance(src, int) else src)]
+                self.decisions.append(("task", layer, ids))
+        self._pushed = []
+
     def _dense_ffn(self, blob: torch.Tensor, F: int, xn: torch.Tensor, resid: torch.Tensor, s: _Scratch, out=None):
         T = xn.shape[0]
         off, perm = s.dense(T)
@@ -233,6 +253,8 @@ class SpecMoEEngine:
         self._route_ev.synchronize()
         ids = self.route_ring.view[0, : T * k].copy()
         self.history.record_many(l, ids)
+        if self.record:
+            self.decisions.append(("verify", l, [int(v) for v in ids]))
         required = sorted(set(int(e) for e in ids))
         stream_ptr = self.stream.cuda_stream
         hits, missing = [], []
@@ -268,7 +290,14 @@ class SpecMoEEngine:
             off, pm = s.dense(T)
             K.expert_ffn(lw.shared, [0], 1, xn, a.shared_ffn, 1, off, pm, s.hd, s.yd, T)
             ys = s.yd
-        return K.moe_combine(s.y, inv, w, T, H, k, residual=resid, y_shared=ys, shared_gate=sg, out=resid)
+        if l in self.capture_layers:
+            cap = {"layer": l, "xn": xn.clone(), "resid": resid.clone(), "idx": idx.clone(), "w": w.clone(),
+                   "slots": list(slots), "sg": None if sg is None else sg.clone()}
+        out = K.moe_combine(s.y, inv, w, T, H, k, residual=resid, y_shared=ys, shared_gate=sg, out=resid)
+        if l in self.capture_layers:
+            cap["out"] = out.clone()
+            self.captures.append(cap)
+        return out
 
     def _gating_predict(self, layer: int, xn: torch.Tensor) -> None:
         """gating_next_layer baseline: predict layer+1 from this layer's MLP
@@ -282,7 +311,8 @@ class SpecMoEEngine:
             x_pos, self.weights.layers[layer].router, pk, True, self.scratch.pw[:B, :pk], self.scratch.pidx[:B, :pk]
         )
         self.cache.push_task(layer, hptr, B * pk, ev.cuda_event)
-        self.cache.drain()
+        self._pushed.append((layer, i))
+        self._drain()
         for e in set(int(v) for v in self.predictor.view[i][: B * pk] if v >= 0):
             sl = self.cache.slot_of(layer, e)
             if sl >= 0:
@@ -316,10 +346,11 @@ class SpecMoEEngine:
         pk = self.policy.prefetch_k
         i, hptr, ev = self.predictor.predict(x_last, self.weights.layers[l].router, pk, True, self.pred_w, self.pred_idx)
         self.cache.push_task(l, hptr, self.predictor.width, ev.cuda_event, step)
+        self._pushed.append((l, i))
         if not self.policy.worker_prefetch:
             # vanilla executor: block until the copies are issued, and make the
             # next layer wait for them (prefetch.py:241-273)
-            self.cache.drain()
+            self._drain()
             sp = self.stream.cuda_stream
             for e in sorted(set(int(v) for v in self.predictor.view[i] if v >= 0)):
                 sl = self.cache.slot_of(l, e)
@@ -390,6 +421,7 @@ class SpecMoEEngine:
             buf = np.array(top_k_indices(self.history.scores(l), pk), dtype=np.int32)
             self._history_bufs.append(buf)
             self.cache.push_task(l, buf.ctypes.data, pk, 0)
+            self._pushed.append((l, buf))
 
     def step(self, remaining: list[int] | None = None) -> list[int]:
         """One SD iteration for every sequence; returns tokens emitted per
@@ -422,13 +454,15 @@ class SpecMoEEngine:
         ev1.record(st)
         # ---- verification
         if self.use_worker:
-            self.cache.drain()
+            self._drain()
         last = torch.tensor([[sq[-1]] for sq in self.seqs], dtype=torch.int64, device=dev)
         vtok = torch.cat([last, draft_tok.long()], dim=1)  # [B, N+1]
         vstart = torch.tensor([p - 1 for p in P], dtype=torch.int64, device=dev)
         s = self.scratch if B * (N + 1) <= self.scratch.T else self._prefill_scratch(B * (N + 1))
         logits = self._target_forward(vtok, vstart, max(P) + N, s)
         _, res = K.greedy_accept(logits.contiguous(), draft_tok)
+        if self.record:
+            self.captures.append({"accept_logits": logits.clone(), "draft": draft_tok.clone(), "res": res.clone()})
         ev2.record(st)
         res_h = res.cpu().tolist()  # syncs
         draft_h = draft_tok.cpu().tolist()

@@ -13,6 +13,10 @@ import torch
 
 from . import _native
 
+# launches of spmoe kernels issued through this module (bench.py reports the
+# count inside its timed region as ``gpu_launches``)
+LAUNCHES = {"count": 0}
+
 BF16 = torch.bfloat16
 F32 = torch.float32
 I32 = torch.int32
@@ -74,6 +78,7 @@ def router_topk(
     if shared_gate_w is not None:
         _need(shared_gate_w, BF16, "shared_gate_w")
         sg = torch.empty((T,), dtype=F32, device=x.device)
+    LAUNCHES["count"] += 1
     _native.call(
         "spmoe_router_topk",
         x.data_ptr(),
@@ -107,6 +112,7 @@ def moe_permute(idx: torch.Tensor, num_experts: int, out=None, stream=None):
         inv = torch.empty((T * k,), dtype=I32, device=idx.device)
     else:
         offsets, perm, inv = out
+    LAUNCHES["count"] += 1
     _native.call(
         "spmoe_moe_permute",
         idx.data_ptr(),
@@ -163,6 +169,7 @@ def expert_ffn(
     slots = _slot_array(slot_of_expert, E)
     st = _stream(stream)
     if phase in ("both", "up"):
+        LAUNCHES["count"] += 1
         _native.call(
             "spmoe_expert_ffn_up",
             pool.data_ptr(),
@@ -182,6 +189,7 @@ def expert_ffn(
             st,
         )
     if phase in ("both", "down"):
+        LAUNCHES["count"] += 1
         _native.call(
             "spmoe_expert_ffn_down",
             pool.data_ptr(),
@@ -222,6 +230,7 @@ def moe_combine(
     dev = device or (y.device if y is not None else residual.device)
     if out is None:
         out = torch.empty((T, H), dtype=BF16, device=dev)
+    LAUNCHES["count"] += 1
     _native.call(
         "spmoe_moe_combine",
         _ptr(y),
@@ -251,6 +260,7 @@ def greedy_accept(logits: torch.Tensor, draft: torch.Tensor, stream=None):
         _need(draft, I32, "draft", 2)
     amax = torch.empty((B, N1), dtype=I32, device=logits.device)
     res = torch.empty((B, 2), dtype=I32, device=logits.device)
+    LAUNCHES["count"] += 2
     _native.call(
         "spmoe_greedy_accept",
         logits.data_ptr(),
@@ -271,6 +281,7 @@ def argmax_rows(logits: torch.Tensor, out: torch.Tensor | None = None, stream=No
     R, V = logits.shape
     if out is None:
         out = torch.empty((R,), dtype=I32, device=logits.device)
+    LAUNCHES["count"] += 1
     _native.call("spmoe_argmax_rows", logits.data_ptr(), V, R, V, out.data_ptr(), _stream(stream))
     return out
 

@@ -1,0 +1,215 @@
+"""End-to-end SD engine on the tiny config (BASELINE config #1) with a real
+offload budget, checked against the oracles at every layer boundary:
+
+* routing indices of every captured verify layer = oracle router on the
+  GPU's own layer input (bit-exact);
+* the verify-MoE layer output = oracle experts + combine on that input,
+  reading the expert blobs from the host pool rows (bit-exact);
+* predicted expert sets, prefetched / demand-loaded transfers, final LRU
+  order and slot assignment = the policy oracle replaying the recorded
+  predictor outputs and verify routing in program order (exact);
+* accepted lengths and correction tokens = oracle greedy acceptance on the
+  GPU's verify logits (exact);
+* SimReport accounting invariants of the reference (test_simcore.py:34-62).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(t):
+    if t.dtype == torch.bfloat16:
+        return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.contiguous().cpu().numpy()
+
+
+def make_engine(policy_kind="draft_prefetch", capacity=12, cutoff=3, N=4, batch=1, worker=True, record=True,
+                capture=(0, 3), arch="tiny", **kw):
+    from paper_2510_10302_b200 import HardwareSpec, Policy, PolicySpec, ProfiledTimings
+    from paper_2510_10302_b200.engine import SpecMoEEngine
+    from paper_2510_10302_b200.model import get_arch
+
+    a = get_arch(arch)
+    hw = HardwareSpec(gpu_memory=180_000_000_000, peak_non_expert_memory=8_000_000_000, pcie_bandwidth=55e9)
+    t = ProfiledTimings(t_comp_target=1e-4, t_comp_draft=1e-4, t_io_expert=a.expert_bytes / 55e9)
+    pol = PolicySpec(policy=Policy(policy_kind), prefetch_k=1, draft_length=N, acceptance_rate=1.0, seed=1234,
+                     cutoff_layer=cutoff, cache_capacity_experts=capacity, worker_prefetch=worker)
+    return SpecMoEEngine(a, hw, t, pol, batch=batch, record=record, capture_layers=capture, **kw)
+
+
+def prompts(batch, P=12, vocab=512, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    return torch.randint(0, vocab, (batch, P), generator=g)
+
+
+def check_layer_captures(eng, oracle):
+    a = eng.arch
+    n = 0
+    for cap in eng.captures:
+        if "layer" not in cap:
+            continue
+        l = cap["layer"]
+        xn = bits(cap["xn"])
+        w_o, idx_o, _, sg_o = oracle.router_topk(xn, bits(eng.weights.layers[l].router), a.top_k, a.renorm)
+        assert np.array_equal(bits(cap["idx"]), idx_o), f"routing mismatch at layer {l}"
+        assert np.array_equal(bits(cap["w"]).view(np.uint32), w_o.view(np.uint32))
+        off, perm, inv = oracle.moe_permute(idx_o, a.num_experts)
+        blobs = [eng.host_pool.array[eng.host_pool.row_of(l, e)] for e in range(a.num_experts)]
+        _, y = oracle.expert_ffn(blobs, xn, a.ffn, off, perm)
+        out = oracle.moe_combine(y, inv, w_o, xn.shape[0], a.hidden, a.top_k, residual=bits(cap["resid"]))
+        assert np.array_equal(bits(cap["out"]), out), f"verify-MoE output mismatch at layer {l}"
+        n += 1
+    assert n > 0
+
+
+def check_acceptance(eng, oracle):
+    n = 0
+    for cap in eng.captures:
+        if "accept_logits" not in cap:
+            continue
+        am, res = oracle.greedy_accept(bits(cap["accept_logits"]), bits(cap["draft"]))
+        assert np.array_equal(bits(cap["res"]), res)
+        n += 1
+    assert n > 0
+
+
+def check_policy_replay(eng, state0):
+    from oracle.policy_oracle import PrefetchReplay
+
+    rep = PrefetchReplay(eng.capacity)
+    order0, slots0 = state0
+    rep.c.order = [tuple(e) for e in order0]
+    rep.c.slot = {tuple(e): s for e, s in zip(order0, slots0)}
+    rep.c.free = sorted(set(range(eng.capacity)) - set(slots0))
+    for kind, layer, ids in eng.decisions:
+        if kind == "task":
+            rep.task(layer, ids)
+        else:
+            rep.verify(layer, ids)
+    log = eng.cache.transfer_log()
+    got = [(r["kind"], r["layer"], list(r["experts"])) for r in log]
+    want = [(k, l, e) for (k, l, e, _) in rep.transfers]
+    assert got == want
+    assert [tuple(e) for e in eng.cache.lru_order] == rep.c.order
+    for e in rep.c.order:
+        assert eng.cache.slot_of(*e) == rep.c.slot[e]
+    c = eng.cache.counters()
+    assert (c["hits"], c["misses"]) == (rep.c.hits, rep.c.misses)
+    assert c["prefetch_insertions"] == rep.c.prefetch_insertions
+    assert c["prefetch_evictions"] == rep.c.prefetch_evictions
+    assert c["demand_insertions"] == rep.c.demand_insertions
+    assert c["tasks_completed"] == rep.tasks_completed
+
+
+def run_and_check(oracle, **kw):
+    eng = make_engine(**kw)
+    try:
+        eng.prefill(prompts(eng.batch))
+        state0 = ([tuple(e) for e in eng.cache.lru_order], [eng.cache.slot_of(*e) for e in eng.cache.lru_order])
+        remaining = [20] * eng.batch
+        while any(r > 0 for r in remaining):
+            em = eng.step(remaining)
+            remaining = [r - e for r, e in zip(remaining, em)]
+        torch.cuda.synchronize()
+        rep = eng.report()
+        check_layer_captures(eng, oracle)
+        check_acceptance(eng, oracle)
+        check_policy_replay(eng, state0)
+        # reference accounting invariants (test_simcore.py:34-62)
+        lookups = sum(len(set(ids)) for k, _, ids in eng.decisions if k == "verify")
+        assert rep.counters["hits"] + rep.counters["misses"] == lookups
+        for it in rep.iterations:
+            assert it.emitted == min(it.accepted + 1, it.emitted) and 1 <= it.emitted <= it.drafted + 1
+        assert rep.emitted_tokens == 20 * eng.batch
+        assert abs(sum(rep.latency_breakdown.values()) - 1.0) < 1e-6
+        return eng, rep
+    except Exception:
+        eng.close()
+        raise
+
+
+def test_engine_tiny_draft_prefetch(oracle):
+    eng, rep = run_and_check(oracle)
+    try:
+        assert rep.counters["prefetch_insertions"] > 0  # SP-MoE prefetch actually ran
+        assert rep.counters["demand_insertions"] > 0  # offload is real (12 of 32 slots)
+        assert rep.extras["acceptance_rate"] > 0.0
+        assert rep.cutoff_effective == 3
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("policy", ["on_demand", "gating_next_layer", "coarse_history"])
+def test_engine_tiny_baseline_policies(oracle, policy):
+    eng, rep = run_and_check(oracle, policy_kind=policy, cutoff=None)
+    try:
+        if policy == "on_demand":
+            assert rep.counters["prefetch_insertions"] == 0
+    finally:
+        eng.close()
+
+
+def test_engine_tiny_vanilla_executor(oracle):
+    eng, rep = run_and_check(oracle, worker=False)
+    eng.close()
+
+
+def test_engine_tiny_batch4(oracle):
+    eng, rep = run_and_check(oracle, batch=4)
+    eng.close()
+
+
+def test_engine_deterministic(oracle):
+    outs = []
+    for _ in range(2):
+        eng = make_engine(record=False, capture=())
+        try:
+            eng.prefill(prompts(1))
+            for _ in range(4):
+                eng.step()
+            outs.append((list(eng.seqs[0]), eng.cache.counters()))
+        finally:
+            eng.close()
+    assert outs[0] == outs[1]
+
+
+def test_engine_shared_expert_arch(oracle):
+    """DeepSeek/Qwen-style routing (no renorm, shared expert with sigmoid gate)
+    at tiny width: routing and combine still bit-exact."""
+    from paper_2510_10302_b200.model import ArchSpec, ARCH_PRESETS
+    from dataclasses import replace
+
+    a = replace(ARCH_PRESETS["tiny"], name="tiny_qwen", num_experts=16, top_k=4, renorm=False, shared_ffn=1024,
+                shared_gate=True)
+    import paper_2510_10302_b200.model as M
+
+    M.ARCH_PRESETS["tiny_qwen"] = a
+    eng = make_engine(arch="tiny_qwen", capacity=24, capture=(1,))
+    try:
+        eng.prefill(prompts(1))
+        for _ in range(3):
+            eng.step()
+        torch.cuda.synchronize()
+        for cap in eng.captures:
+            if "layer" not in cap:
+                continue
+            l = cap["layer"]
+            xn = bits(cap["xn"])
+            lw = eng.weights.layers[l]
+            w_o, idx_o, _, sg_o = oracle.router_topk(xn, bits(lw.router), a.top_k, a.renorm, bits(lw.shared_gate))
+            assert np.array_equal(bits(cap["idx"]), idx_o)
+            off, perm, inv = oracle.moe_permute(idx_o, a.num_experts)
+            blobs = [eng.host_pool.array[eng.host_pool.row_of(l, e)] for e in range(a.num_experts)]
+            _, y = oracle.expert_ffn(blobs, xn, a.ffn, off, perm)
+            T = xn.shape[0]
+            _, ys = oracle.expert_ffn([bits(lw.shared[0])], xn, a.shared_ffn, np.array([0, T], np.int32),
+                                      np.arange(T, dtype=np.int32))
+            out = oracle.moe_combine(y, inv, w_o, T, a.hidden, a.top_k, ys=ys[:T], sg=sg_o, residual=bits(cap["resid"]))
+            assert np.array_equal(bits(cap["out"]), out)
+    finally:
+        eng.close()

@@ -229,14 +229,15 @@ def test_greedy_accept_exact(oracle):
     for b in range(B):  # reject at position b (b >= N: all accepted)
         if b < N:
             draft[b, b] = (draft[b, b] + 1) % V
-    logits[3, 2, 17] = logits[3, 2].max()  # exact tie -> lowest index
-    logits[3, 2, 5] = logits[3, 2].max()
+    top = logits[7, 4].max() + 1.0  # exact tie on the bonus row -> lowest index
+    logits[7, 4, 17] = top
+    logits[7, 4, 5] = top
     am, res = K.greedy_accept(torch.from_numpy(logits).cuda(), torch.from_numpy(draft).cuda())
     torch.cuda.synchronize()
     am2, res2 = oracle.greedy_accept(logits, draft)
     assert np.array_equal(bits(am), am2)
     assert np.array_equal(bits(res), res2)
-    assert am2[3, 2] == 5
+    assert am2[7, 4] == 5 and res2[7, 1] == 5 and res2[7, 0] == N
     assert [int(r[0]) for r in res2[:4]] == [0, 1, 2, 3]
 
 
