@@ -1,0 +1,432 @@
+#!/usr/bin/env python
+"""Benchmark of the SP-MoE verification-time expert path on B200.
+
+Default workload (BASELINE.json configs[1]): Mixtral-8x7B-shaped target
+(random init, bf16) with a small dense draft (shares the target's embedding,
+attention and lm_head; FFN = mean of the layer's experts), expert-cache budget
+25 % of the routed experts (64 of 256 slots) with the other 75 % offloaded to
+pinned host memory, draft length N=4, batch 1, SP-MoE draft_prefetch policy.
+
+A *step* is one SD iteration (draft N tokens with draft-guided prediction +
+asynchronous prefetch, verify N+1 tokens through all 32 layers with
+demand loads, greedy acceptance).  ``value`` = emitted tokens/s over the
+timed steps (device time by CUDA events, max over ranks; weak scaling: one
+independent request stream per GPU); ``e2e`` = the same through the public
+``SpecMoEEngine.step`` API by wall clock, including per-step host->device
+token inputs and the device->host read of the accepted tokens.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config mixtral|deepseek|qwen|tiny] [--batch B] [--draft-length N]
+
+Multi-GPU: launched by torch.distributed.run, one rank per GPU over NCCL
+(barrier + max-over-ranks timing only; there is no data-path collective).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "TPOT ms and tokens/s, Mixtral-8x7B SD+offload; verify-MoE HBM GB/s; H2D GB/s"
+UNIT = "tokens/s"
+
+CONFIGS = {
+    # configs[1]: the headline
+    "mixtral": dict(arch="mixtral_8x7b", budget=0.25, N=4, batch=1, prompt=64),
+    "deepseek": dict(arch="deepseek_v2_lite", budget=0.25, N=4, batch=1, prompt=64),
+    "qwen": dict(arch="qwen15_moe_a27b", budget=0.25, N=4, batch=1, prompt=64),
+    "tiny": dict(arch="tiny", budget=0.375, N=4, batch=1, prompt=16),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        self.f.flush()
+        rows = [r.split(",") for r in Path(self.f.name).read_text().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for n, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def h2d_peak_gbs(torch, nbytes=1 << 30, reps=5) -> float:
+    """Pinned host -> HBM copy bandwidth on this box (best of ``reps``)."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    best = 0.0
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            a.record(s)
+            d.copy_(h, non_blocking=True)
+            b.record(s)
+        b.synchronize()
+        best = max(best, nbytes / (a.elapsed_time(b) / 1e3) / 1e9)
+    del h, d
+    return best
+
+
+# ---------------------------------------------------------------------------
+# CPU restatement (oracle port) of the same path: the reference arm and the
+# cpu_baseline leg.  Executes oracle/ only here, as the timed CPU baseline.
+# ---------------------------------------------------------------------------
+def cpu_path_iteration(arch, seed, N, B, prefetch_k, cutoff, sample_layers, threads, blob_rows=None):
+    """Time one SD iteration of the verify-time expert path on the host cores:
+    for ``sample_layers`` target layers, K1 router + K2 permute + K3 SwiGLU
+    experts + K4 combine at T = B*(N+1) tokens, plus the drafting-stage
+    predictor projections (K1, k = prefetch_k) of those layers for N draft
+    steps, scaled to all layers; plus K6 acceptance.  Returns seconds."""
+    import numpy as np
+
+    from oracle import tensor_oracle as O
+    from paper_2510_10302_b200.model import K_EXPERT, K_ROUTER, _splitmix64, tensor_seed
+
+    O.set_threads(threads)
+    H, F, E, k = arch.hidden, arch.ffn, arch.num_experts, arch.top_k
+    T = B * (N + 1)
+    rng = np.random.default_rng(seed)
+    x = O.f32_to_bf16_bits(rng.standard_normal((T, H)).astype(np.float32))
+    resid = O.f32_to_bf16_bits(rng.standard_normal((T, H)).astype(np.float32) * 0.1)
+    layers = list(range(sample_layers))
+    # expert blobs for the sampled layers (same counter-hash bits the GPU uses)
+    blobs = {}
+    n13 = F * H
+    for l in layers:
+        rw = O.fill_normal_bf16(E * H, tensor_seed(seed, K_ROUTER, l), 0, 1.0 / np.sqrt(H)).reshape(E, H)
+        eb = []
+        for e in range(E):
+            if blob_rows is not None:
+                eb.append(blob_rows(l, e))
+                continue
+            s0 = tensor_seed(seed, K_EXPERT, l * E + e)
+            b = np.empty(3 * n13, np.uint16)
+            b[:n13] = O.fill_normal_bf16(n13, _splitmix64(s0 ^ 1), 0, arch.init_std)
+            b[n13:2 * n13] = O.fill_normal_bf16(n13, _splitmix64(s0 ^ 3), 0, arch.init_std)
+            b[2 * n13:] = O.fill_normal_bf16(n13, _splitmix64(s0 ^ 2), 0, arch.init_std * arch.expert_out_scale)
+            eb.append(b)
+        blobs[l] = (rw, eb)
+    logits = rng.standard_normal((B, N + 1, 4096)).astype(np.float32)
+    draft = rng.integers(0, 4096, (B, N)).astype(np.int32)
+    xd = x[:B]
+    t0 = time.perf_counter()
+    for l in layers:
+        rw, eb = blobs[l]
+        w, idx, _, _ = O.router_topk(x, rw, k, arch.renorm)
+        off, perm, inv = O.moe_permute(idx, E)
+        used = set(int(v) for v in idx.ravel())
+        _, y = O.expert_ffn([eb[e] if e in used else None for e in range(E)], x, F, off, perm)
+        O.moe_combine(y, inv, w, T, H, k, residual=resid)
+        if cutoff is not None and l <= cutoff:
+            for _ in range(N):
+                O.router_topk(xd, rw, prefetch_k, True)
+    t_layers = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    O.greedy_accept(logits, draft)
+    t_acc = (time.perf_counter() - t1) * arch.vocab / 4096
+    return t_layers * arch.num_layers / len(layers) + t_acc
+
+
+def calibration(cfg_name: str) -> dict:
+    p = ROOT / "profiles" / "bench_calibration.json"
+    if p.exists():
+        return json.loads(p.read_text()).get(cfg_name, {})
+    return {}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU restatement of the path (oracle port; the
+    reference package is a Python simulator with no tensor path and cannot
+    travel to the GPU box), all host threads, bounded samples."""
+    import numpy as np
+
+    from paper_2510_10302_b200.model import get_arch
+
+    if rank != 0:
+        return
+    arch = get_arch(cfg["arch"])
+    threads = os.cpu_count() or 1
+    cal = calibration(args.config)
+    emitted = cal.get("emitted_per_iter", cfg["N"] + 1) * cfg["batch"]
+    sample_layers = 2 if arch.hidden >= 4096 else 4
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = cpu_path_iteration(arch, 1234, cfg["N"], cfg["batch"], 1, cal.get("cutoff"), sample_layers, threads)
+        if i >= args.warmup:
+            times.append(t)
+    it_s = float(np.mean(times))
+    value = emitted / it_s
+    sample = (f"per step: {sample_layers} of {arch.num_layers} verify-MoE layers (K1 router, permute, SwiGLU "
+              f"experts, combine) at T={cfg['batch'] * (cfg['N'] + 1)} + drafting-stage predictor projections, "
+              f"scaled to {arch.num_layers} layers; {emitted:.3f} emitted tokens/iteration "
+              f"({'calibrated from our GPU run' if cal else 'upper bound N+1'})")
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": it_s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16 weights, fp32 accumulate", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {arch.name} SD verify path, N={cfg['N']}, batch {cfg['batch']}"},
+        "tpot_ms": it_s * 1e3 / emitted,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--draft-length", type=int, default=None)
+    ap.add_argument("--budget", type=float, default=None, help="fraction of routed experts resident in HBM")
+    ap.add_argument("--policy", default="draft_prefetch")
+    ap.add_argument("--cutoff", type=int, default=None, help="explicit cutoff layer (default: solver)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--write-calibration", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.batch:
+        cfg["batch"] = args.batch
+    if args.draft_length:
+        cfg["N"] = args.draft_length
+    if args.budget:
+        cfg["budget"] = args.budget
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_10302_b200 import HardwareSpec, Policy, PolicySpec, ProfiledTimings
+    from paper_2510_10302_b200 import kernels as K
+    from paper_2510_10302_b200.calibrate import b200_timings
+    from paper_2510_10302_b200.engine import SpecMoEEngine
+    from paper_2510_10302_b200.model import get_arch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    arch = get_arch(cfg["arch"])
+    E_all = arch.num_layers * arch.num_experts
+    capacity = max(arch.num_experts, int(round(cfg["budget"] * E_all)))
+    peak_h2d = h2d_peak_gbs(torch)
+    hw = HardwareSpec(gpu_memory=183_359 * 2**20, peak_non_expert_memory=24 * 10**9, pcie_bandwidth=peak_h2d * 1e9,
+                      name="b200")
+    timings = b200_timings(arch, hw)
+    policy = PolicySpec(policy=Policy(args.policy), prefetch_k=1 if arch.num_experts <= 16 else arch.top_k,
+                        draft_length=cfg["N"], acceptance_rate=1.0, seed=1234, cutoff_layer=args.cutoff,
+                        cache_capacity_experts=capacity)
+    t_setup = time.perf_counter()
+    eng = SpecMoEEngine(arch, hw, timings, policy, batch=cfg["batch"], max_tokens=cfg["prompt"] + 64 * (cfg["N"] + 1),
+                        window_tokens=cfg["N"])
+    g = torch.Generator().manual_seed(1000 + rank)
+    prompts = torch.randint(0, arch.vocab, (cfg["batch"], cfg["prompt"]), generator=g)
+    eng.prefill(prompts)
+    log(f"[bench] setup {time.perf_counter() - t_setup:.1f}s capacity={capacity} cutoff={eng.cutoff} "
+        f"h2d_peak={peak_h2d:.1f}GB/s timings={timings}")
+    for _ in range(args.warmup):
+        eng.step()
+    torch.cuda.synchronize()
+    eng._reset_run_state()
+    eng.cache.reset_stats()
+    eng.cache.clear_log()
+    eng.time_k3 = True
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = K.LAUNCHES["count"]
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    prof_range = os.environ.get("SPMOE_PROFILE_RANGE") == "1"
+    if prof_range:
+        torch.cuda.profiler.start()
+    e0.record(st)
+    emitted = 0
+    for _ in range(args.steps):
+        emitted += sum(eng.step())
+    e1.record(st)
+    if prof_range:
+        torch.cuda.profiler.stop()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = K.LAUNCHES["count"] - launches0
+    dev_ms = e0.elapsed_time(e1)
+    rep = eng.report(wall_s=wall)
+    roof = eng.k3_roofline()
+    stats = torch.tensor([dev_ms, wall, float(emitted)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        mx = stats.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = stats.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dev_ms, wall, emitted_all = float(mx[0]), float(mx[1]), float(sm[2])
+    else:
+        emitted_all = float(emitted)
+    value = emitted_all / (dev_ms / 1e3)
+    e2e = emitted_all / wall
+    peaks = measured_peaks()
+    B, N = cfg["batch"], cfg["N"]
+    # per-step host<->device bytes of the public step() API: int64 token /
+    # position inputs (first[B,2], start[B], last[B,1], vstart[B]) and the
+    # int32 result [B,2] + drafts [B,N]
+    h2d_step = 8 * B * (2 + 1 + 1 + 1)
+    d2h_step = 4 * B * (2 + N)
+    ex = rep.extras
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": dev_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (random-init weights, seeded random prompts)",
+        "config": {
+            "workload": f"{args.config}: {arch.name} target + dense draft, SD N={N}, batch {B}/GPU, "
+                        f"expert budget {cfg['budget']:.0%} ({capacity}/{E_all} slots), policy {args.policy}",
+            "global_batch": B * world,
+            "prompt_len": cfg["prompt"],
+            "l2": "inputs larger than L2: each step streams >=20 GB of expert weights (126 MB L2)",
+            "parallelism": f"replicas x{world} (independent SD streams, per-GPU caches)",
+        },
+        "tpot_ms": dev_ms / args.steps / (emitted / args.steps / B) if emitted else None,
+        "tokens_emitted": emitted_all,
+        "acceptance_rate": ex.get("acceptance_rate"),
+        "hit_rate": rep.hit_rate,
+        "cutoff_layer": eng.cutoff,
+        "latency_breakdown": rep.latency_breakdown,
+        "verify_moe_hbm_gbs": roof.get("achieved_gbs"),
+        "h2d_gbs": ex.get("h2d_gbs"),
+        "h2d_peak_gbs": peak_h2d,
+        "h2d_frac": (ex.get("h2d_gbs") or 0.0) / peak_h2d if peak_h2d else None,
+        "h2d_expert_bytes_per_step": ex.get("h2d_bytes", 0) / args.steps,
+        "hidden_prefetch_fraction": ex.get("hidden_prefetch_fraction"),
+        "stall_ms_per_step": {"prefetch": ex.get("stall_prefetch_ms", 0) / args.steps,
+                              "demand": ex.get("stall_demand_ms", 0) / args.steps},
+        "roofline": {
+            "kernel": "spmoe_expert_ffn (K3 grouped SwiGLU, up+down launch pair)",
+            "bound": "hbm",
+            "achieved": roof.get("achieved_gbs"),
+            "peak": peaks["hbm_gbs"],
+            "peak_source": peaks["source"] + " copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+            "unit": "GB/s",
+            "frac": (roof.get("achieved_gbs") or 0.0) / peaks["hbm_gbs"],
+            "traffic": None,
+            "launches": roof.get("launches"),
+            "bytes_per_launch": roof.get("bytes_per_launch"),
+            "ms_per_launch": roof.get("ms_per_launch"),
+        },
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": d2h_step},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    prof = ROOT / "profiles" / "ncu_k3_traffic.json"
+    if prof.exists():
+        t = json.loads(prof.read_text())
+        out["roofline"]["traffic"] = t.get("traffic_per_launch_bytes")
+        out["roofline"]["traffic_source"] = t.get("source")
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        emitted_per_iter = emitted / args.steps
+        sample_layers = 2
+        hp = eng.host_pool
+        t_cpu = cpu_path_iteration(arch, 1234, N, B, policy.prefetch_k, eng.cutoff, sample_layers, threads,
+                                   blob_rows=lambda l, e: hp.array[hp.row_of(l, e)])
+        out["cpu_baseline"] = {
+            "value": emitted_per_iter / t_cpu, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{sample_layers} of {arch.num_layers} verify-MoE layers + predictor projections on the CPU "
+                      f"oracle (oracle/spmoe_oracle.c, {threads} threads), scaled to one SD iteration; "
+                      f"{emitted_per_iter:.2f} emitted tokens/iteration from this run",
+            "ms_per_iteration": t_cpu * 1e3,
+        }
+    if rank == 0 and args.write_calibration:
+        p = ROOT / "profiles" / "bench_calibration.json"
+        d = json.loads(p.read_text()) if p.exists() else {}
+        d[args.config] = {"emitted_per_iter": emitted / args.steps / B, "cutoff": eng.cutoff}
+        p.write_text(json.dumps(d, indent=1))
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,72 @@
+"""Recalibrate the cutoff model's latency inputs for B200.
+
+The reference takes ``ProfiledTimings`` from desk measurements
+(``configs/*.yaml``); here they come from the B200's own numbers:
+
+* ``t_io_expert`` = expert bytes / measured pinned H2D bandwidth + a copy
+  launch overhead (validated against ``validate_timings``'s floor/ceiling);
+* ``t_comp_draft`` / ``t_comp_target`` = per-layer weight bytes / sustained
+  HBM bandwidth (the decode step is weight-bandwidth bound) + a fixed
+  per-layer launch overhead; :func:`measure_timings` replaces these model
+  values with CUDA-event measurements of a live engine;
+* ``t_predict`` = K1 router latency.
+
+:func:`write_profiled_config` emits the reference YAML (``config.py:436-482``)
+so moesim's simulator can run calibrated what-if sweeps.
+"""
+
+from __future__ import annotations
+
+import json
+from pathlib import Path
+
+from .config import HardwareSpec, ProfiledTimings
+
+ROOT = Path(__file__).resolve().parents[1]
+LAYER_OVERHEAD_S = 40e-6  # measured order of host launch overhead per layer
+K1_LATENCY_S = 25e-6  # K1 router latency measured on B200 (tools/bench_kernels.py)
+COPY_OVERHEAD_S = 20e-6
+
+
+def hbm_gbs() -> float:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text()).get("hbm_gbs", 6650.0))
+    return 6650.0
+
+
+def b200_timings(arch, hw: HardwareSpec, hbm_efficiency: float = 0.7) -> ProfiledTimings:
+    bw = hbm_gbs() * 1e9 * hbm_efficiency
+    attn_bytes = 2 * arch.hidden * (arch.qkv_dim + arch.num_heads * arch.head_dim)
+    draft_layer = (attn_bytes + 3 * arch.d_ffn * arch.hidden * 2) / bw + LAYER_OVERHEAD_S
+    # verify touches ~min(E, T*k) experts per layer; T = 5 (N=4) reference case
+    distinct = min(arch.num_experts, 5 * arch.top_k)
+    target_layer = (attn_bytes + distinct * arch.expert_bytes + 3 * arch.shared_ffn * arch.hidden * 2) / bw
+    target_layer += LAYER_OVERHEAD_S
+    t_io = arch.expert_bytes / hw.pcie_bandwidth + COPY_OVERHEAD_S + hw.io_launch_overhead
+    return ProfiledTimings(t_comp_target=target_layer, t_comp_draft=draft_layer, t_io_expert=t_io,
+                           t_predict=K1_LATENCY_S)
+
+
+def measure_timings(engine, steps: int = 3) -> ProfiledTimings:
+    """Per-layer draft / verify compute from CUDA events on a live engine
+    (fully resident layers only would be ideal; we subtract measured copy
+    stalls instead), and t_io from the engine's transfer log."""
+    rep = engine.report()
+    ts = engine.timing_summary()
+    n_it = max(1, len(engine.iter_records))
+    L = engine.arch.num_layers
+    N = engine.policy.draft_length
+    draft_layer = ts["draft_ms"] / 1e3 / n_it / (N * L)
+    stall = (ts["stall_ms"]["prefetch"] + ts["stall_ms"]["demand"]) / 1e3
+    target_layer = max(0.0, ts["verify_ms"] / 1e3 - stall) / n_it / L
+    per_expert = [t.duration / max(1, len(t.experts)) for t in rep.transfers if t.experts]
+    t_io = sorted(per_expert)[len(per_expert) // 2] if per_expert else engine.timings.t_io_expert
+    return ProfiledTimings(t_comp_target=target_layer, t_comp_draft=draft_layer, t_io_expert=t_io,
+                           t_predict=K1_LATENCY_S)
+
+
+def write_profiled_config(path, model, hw, timings, policy) -> None:
+    from .config import write_config
+
+    write_config(path, model, hw, timings, policy)

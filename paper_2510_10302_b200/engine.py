@@ -180,6 +180,8 @@ class SpecMoEEngine:
         self.record_timeline = record_timeline
         self.record = record
         self.capture_layers = set(capture_layers)
+        self.time_k3 = False
+        self.k3_events: list = []
         self._reset_run_state()
 
     # ------------------------------------------------------------------ utils
@@ -233,6 +235,40 @@ class SpecMoEEngine:
         K.expert_ffn(blob, [0], 1, xn, F, 1, off, perm, s.hd, s.yd, max_tokens_per_expert=T)
         return K.moe_combine(s.yd, perm, None, T, self.arch.hidden, 1, residual=resid, out=out)
 
+    def _timed_ffn(self, experts, counts, slots, mask, xn, offsets, perm, s, maxtok) -> None:
+        """K3 over ``experts``; with ``time_k3`` set, brackets the launch pair
+        with CUDA events and books its algorithmic bytes (weights of every
+        expert in the mask read once + activations in/out) for the roofline."""
+        a = self.arch
+        if not self.time_k3:
+            K.expert_ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok)
+            return
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record()
+        K.expert_ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok)
+        eb.record()
+        rows = int(sum(int(counts[e]) for e in experts))
+        act = rows * (a.hidden * 2 + 2 * a.ffn * 2 + a.hidden * 4)  # x in, h out+in, y out
+        self.k3_events.append((ea, eb, len(experts) * a.expert_bytes + act, len(experts), rows))
+
+    def k3_roofline(self) -> dict:
+        """Average algorithmic bytes / launch-pair duration of the timed K3 calls."""
+        torch.cuda.synchronize(self.device)
+        if not self.k3_events:
+            return {}
+        ms = [a_.elapsed_time(b_) for a_, b_, *_ in self.k3_events]
+        byts = [x[2] for x in self.k3_events]
+        tot_ms = sum(ms)
+        return {
+            "launches": len(ms),
+            "bytes_per_launch": sum(byts) / len(byts),
+            "ms_per_launch": tot_ms / len(ms),
+            "achieved_gbs": sum(byts) / (tot_ms / 1e3) / 1e9,
+            "experts_per_launch": sum(x[3] for x in self.k3_events) / len(ms),
+            "rows_per_launch": sum(x[4] for x in self.k3_events) / len(ms),
+            "total_ms": tot_ms,
+        }
+
     def _moe_verify(self, l: int, xn: torch.Tensor, resid: torch.Tensor, s: _Scratch) -> torch.Tensor:
         a = self.arch
         lw = self.weights.layers[l]
@@ -274,7 +310,7 @@ class SpecMoEEngine:
         maxtok = int(counts.max()) if counts.size else 0
         if ready:
             mask = sum(1 << e for e in ready)
-            K.expert_ffn(self.pool, slots, mask, xn, a.ffn, k, offsets, perm, s.h, s.y, maxtok)
+            self._timed_ffn(ready, counts, slots, mask, xn, offsets, perm, s, maxtok)
         for kind, group in (("prefetch", late_prefetch), ("demand", missing)):
             for e in group:
                 ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -282,7 +318,7 @@ class SpecMoEEngine:
                 self.cache.wait_slot(slot[e], stream_ptr)
                 eb.record()
                 self.stalls.append(_Stall(kind, l, ea, eb))
-                K.expert_ffn(self.pool, slots, 1 << e, xn, a.ffn, k, offsets, perm, s.h, s.y, int(counts[e]))
+                self._timed_ffn([e], counts, slots, 1 << e, xn, offsets, perm, s, int(counts[e]))
         for e in required:
             self.cache.mark_read(slot[e], stream_ptr)
         ys = None

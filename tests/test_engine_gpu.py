@@ -124,7 +124,7 @@ def run_and_check(oracle, **kw):
         lookups = sum(len(set(ids)) for k, _, ids in eng.decisions if k == "verify")
         assert rep.counters["hits"] + rep.counters["misses"] == lookups
         for it in rep.iterations:
-            assert it.emitted == min(it.accepted + 1, it.emitted) and 1 <= it.emitted <= it.drafted + 1
+            assert 0 <= it.emitted <= it.accepted + 1 <= it.drafted + 1
         assert rep.emitted_tokens == 20 * eng.batch
         assert abs(sum(rep.latency_breakdown.values()) - 1.0) < 1e-6
         return eng, rep

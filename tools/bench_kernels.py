@@ -87,10 +87,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--json", default=None)
     ap.add_argument("--cases", default=",".join(CASES))
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     a = ap.parse_args()
     out = []
     for name in a.cases.split(","):
-        r = run_case(name, **CASES[name])
+        r = run_case(name, iters=a.iters, warmup=a.warmup, **CASES[name])
         out.append(r)
         print(json.dumps(r))
     if a.json:
