@@ -62,6 +62,12 @@ class ArchSpec:
     max_seq: int = 2048
     init_std: float = 0.02
     expert_out_scale: float = 1.0  # scales W2 std (residual-branch scaling)
+    # Upcycled experts (None = independent random experts): every routed
+    # expert of a layer = shared layer component + expert_spread x its own
+    # deviation, so the draft's mean-expert FFN tracks the routed mixture and
+    # random-init SD accepts drafts at a realistic rate (SURVEY.md §7 hard
+    # part 2).  Bytes moved and FLOPs are unchanged.
+    expert_spread: float | None = 0.25
 
     def __post_init__(self):
         if self.hidden % 8 or self.ffn % 8 or (self.shared_ffn % 8):
@@ -176,7 +182,7 @@ def tensor_seed(base: int, *ids: int) -> int:
 
 
 # kind codes for tensor_seed
-K_EMBED, K_QKV, K_WO, K_ROUTER, K_EXPERT, K_SHARED, K_SGATE, K_LMHEAD, K_PERTURB = range(9)
+K_EMBED, K_QKV, K_WO, K_ROUTER, K_EXPERT, K_SHARED, K_SGATE, K_LMHEAD, K_PERTURB, K_BASE = range(10)
 
 
 # ---------------------------------------------------------------------------
@@ -285,17 +291,25 @@ def build_weights(
         )
         router = _fill(torch.empty((E, H), dtype=bf, device=device), tensor_seed(seed, K_ROUTER, l), 1.0 / math.sqrt(H))
         acc = torch.zeros((arch.expert_elems,), dtype=torch.float32, device=device)
+        base = None
+        if arch.expert_spread is not None:
+            base = torch.empty((arch.expert_elems,), dtype=bf, device=device)
+            fill_blob_generic(base, F, H, tensor_seed(seed, K_BASE, l), std, arch.expert_out_scale)
         for e0 in range(0, E, stage.shape[0]):
             n = min(stage.shape[0], E - e0)
             for j in range(n):
                 row = host_pool.row_of(l, e0 + j) if host_pool is not None else l * E + e0 + j
                 fill_expert_blob(stage[j], arch, seed, row)
+                if base is not None:
+                    # upcycled experts: a shared per-layer component plus a
+                    # per-expert deviation of relative size expert_spread
+                    stage[j].copy_((base.float() + stage[j].float() * arch.expert_spread).to(bf))
                 acc += stage[j].float()
             if host_pool is not None:
                 for j in range(n):
                     host_pool.blob(l, e0 + j).copy_(stage[j], non_blocking=False)
         mean = (acc / E).to(bf)
-        del acc
+        del acc, base
         if arch.d_ffn != F:
             draft = torch.empty((1, 3 * arch.d_ffn * H), dtype=bf, device=device)
             fill_blob_generic(draft[0], arch.d_ffn, H, tensor_seed(seed, K_EXPERT, l, 10_000), std, arch.expert_out_scale)
