@@ -282,6 +282,17 @@ int spmoe_host_free(void* host);
 int spmoe_host_register(void* host, size_t bytes);
 int spmoe_host_unregister(void* host);
 
+/* --------------------------------------------------------------------- */
+/* Events usable across CUDA-graph replays: record_external inside stream */
+/* capture creates an external event-record node (cudaEventRecordExternal)*/
+/* so the prefetch worker can wait on a predictor kernel that runs inside */
+/* a replayed draft-step graph; outside capture it is cudaEventRecord.    */
+/* --------------------------------------------------------------------- */
+int spmoe_event_create(void** ev);
+int spmoe_event_destroy(void* ev);
+int spmoe_event_record_external(void* ev, void* stream);
+int spmoe_event_synchronize(void* ev);
+
 #ifdef __cplusplus
 }
 #endif

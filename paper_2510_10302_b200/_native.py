@@ -73,6 +73,10 @@ SIGNATURES: dict[str, tuple] = {
     "spmoe_host_free": (_i, [_p]),
     "spmoe_host_register": (_i, [_p, _sz]),
     "spmoe_host_unregister": (_i, [_p]),
+    "spmoe_event_create": (_i, [_p]),
+    "spmoe_event_destroy": (_i, [_p]),
+    "spmoe_event_record_external": (_i, [_p, _p]),
+    "spmoe_event_synchronize": (_i, [_p]),
 }
 
 _lib = None

@@ -197,12 +197,13 @@ __device__ __forceinline__ int gather_active(const FfnParams& p, int* s_active, 
   return s_n;
 }
 
-// acc[r][t] += dot(weight row r, activation row t) over nchunks 16-byte
-// chunks, lane-strided fixed order.
+// One warp row: acc[r][t] += dot(weight row r, activation row t) over nchunks
+// 16-byte chunks in the lane-strided fixed order; weights stream from HBM
+// straight into registers (UNR chunks per row in flight per lane), the
+// activation chunks come from the CTA's shared-memory stage.
 template <int TT, int NR, int UNR>
-__device__ __forceinline__ void stream_rows(const uint4* const (&wr)[NR],
-                                            const uint4* const (&ar)[TT], int nt, int nchunks,
-                                            int lane, float (&acc)[NR][TT]) {
+__device__ __forceinline__ void stream_rows(const uint4* const (&wr)[NR], const uint4* act, int act_stride,
+                                            int nt, int nchunks, int lane, float (&acc)[NR][TT]) {
   for (int base = 0; base < nchunks; base += 32 * UNR) {
     uint4 w[NR][UNR];
 #pragma unroll
@@ -223,7 +224,7 @@ __device__ __forceinline__ void stream_rows(const uint4* const (&wr)[NR],
         for (int t = 0; t < TT; ++t) {
           if (t < nt) {
             float af[8];
-            unpack8(ldg_act(ar[t] + c), af);
+            unpack8(act[t * act_stride + c], af);
 #pragma unroll
             for (int v = 0; v < 8; ++v)
 #pragma unroll
@@ -235,45 +236,77 @@ __device__ __forceinline__ void stream_rows(const uint4* const (&wr)[NR],
   }
 }
 
-template <int TT>
-__global__ void __launch_bounds__(kFfnThreads, 1) ffn_up_kernel(const FfnParams p) {
+// K3 phase kernel.  UP: rows f of W1 and W3 (NR=2, K=H) -> h = bf16(silu(g)*u);
+// DOWN: rows h of W2 (NR=1, K=F) -> y fp32.  The (active expert, 16-row
+// tile) space is split into one contiguous range per CTA (balanced to one
+// tile, at most a couple of expert switches per CTA); a switch restages the
+// expert's routed-token activations [TT][K] in shared memory.  Warp w owns
+// row w of every tile.
+template <bool UP, int TT>
+__global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const FfnParams p) {
+  extern __shared__ __align__(16) uint4 s_act[];
   __shared__ int s_active[kMaxFfnExperts];
   __shared__ int s_off[kMaxFfnExperts + 1];
+  constexpr int NR = UP ? 2 : 1;
+  constexpr int UNR = UP ? 8 : 16;
+  constexpr int kRowsPerTile = kFfnThreads / 32;
   const int n_active = gather_active(p, s_active, s_off);
-  const int lane = threadIdx.x & 31;
-  const int gwarp = blockIdx.x * (kFfnThreads / 32) + (threadIdx.x >> 5);
-  const int nwarps = gridDim.x * (kFfnThreads / 32);
-  const int64_t total = (int64_t)n_active * p.F;
-  const int nchunks = p.H >> 3;
-  for (int64_t u = gwarp; u < total; u += nwarps) {
-    const int a = (int)(u / p.F);
-    const int f = (int)(u - (int64_t)a * p.F);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int K = UP ? p.H : p.F;            // reduction length
+  const int R = UP ? p.F : p.H;            // rows per expert
+  const int nchunks = K >> 3;
+  const int tpe = (R + kRowsPerTile - 1) / kRowsPerTile;
+  const int64_t total = (int64_t)n_active * tpe;
+  const int64_t t_begin = total * blockIdx.x / gridDim.x;
+  const int64_t t_end = total * (blockIdx.x + 1) / gridDim.x;
+  int cur_e = -1, cur_t0 = -1;
+  for (int64_t tile = t_begin; tile < t_end; ++tile) {
+    const int a = (int)(tile / tpe);
+    const int row = (int)(tile - (int64_t)a * tpe) * kRowsPerTile + warp;
     const int e = s_active[a];
-    const uint16_t* blob = p.pool + (int64_t)p.slot[e] * p.slot_elems;
-    const uint4* const wr[2] = {reinterpret_cast<const uint4*>(blob + (int64_t)f * p.H),
-                                reinterpret_cast<const uint4*>(blob + ((int64_t)p.F + f) * p.H)};
     const int off = s_off[e];
     const int cnt = s_off[e + 1] - off;
+    const uint16_t* blob = p.pool + (int64_t)p.slot[e] * p.slot_elems;
     for (int t0 = 0; t0 < cnt; t0 += TT) {
       const int nt = min(TT, cnt - t0);
-      const uint4* ar[TT];
-#pragma unroll
-      for (int t = 0; t < TT; ++t) {
-        const int tok = p.perm[off + t0 + min(t, nt - 1)];
-        ar[t] = reinterpret_cast<const uint4*>(p.x + (int64_t)tok * p.H);
+      if (e != cur_e || t0 != cur_t0) {
+        __syncthreads();  // every warp is done with the previous stage
+        for (int q = threadIdx.x; q < nt * nchunks; q += kFfnThreads) {
+          const int t = q / nchunks, c = q - t * nchunks;
+          const uint16_t* src = UP ? p.x + (int64_t)p.perm[off + t0 + t] * p.H
+                                   : p.h + (int64_t)(off + t0 + t) * p.F;
+          s_act[t * nchunks + c] = __ldg(reinterpret_cast<const uint4*>(src) + c);
+        }
+        __syncthreads();
+        cur_e = e;
+        cur_t0 = t0;
       }
-      float acc[2][TT];
+      if (row >= R) continue;
+      const uint4* wr[NR];
+      if (UP) {
+        wr[0] = reinterpret_cast<const uint4*>(blob + (int64_t)row * p.H);
+        wr[NR - 1] = reinterpret_cast<const uint4*>(blob + ((int64_t)p.F + row) * p.H);
+      } else {
+        wr[0] = reinterpret_cast<const uint4*>(blob + 2 * (int64_t)p.F * p.H + (int64_t)row * p.F);
+      }
+      float acc[NR][TT];
 #pragma unroll
-      for (int t = 0; t < TT; ++t) { acc[0][t] = 0.0f; acc[1][t] = 0.0f; }
-      stream_rows<TT, 2, 8>(wr, ar, nt, nchunks, lane, acc);
+      for (int r = 0; r < NR; ++r)
+#pragma unroll
+        for (int t = 0; t < TT; ++t) acc[r][t] = 0.0f;
+      stream_rows<TT, NR, UNR>(wr, s_act, nchunks, nt, nchunks, lane, acc);
 #pragma unroll
       for (int t = 0; t < TT; ++t) {
         if (t < nt) {
-          const float g = warp_sum_fixed(acc[0][t]);
-          const float v = warp_sum_fixed(acc[1][t]);
-          if (lane == t) {
-            const float hv = __fmul_rn(det_silu(g), v);
-            p.h_out[(int64_t)(off + t0 + t) * p.F + f] = f32_to_bf16(hv);
+          const float s0 = warp_sum_fixed(acc[0][t]);
+          if (UP) {
+            const float s1 = warp_sum_fixed(acc[NR - 1][t]);
+            if (lane == t) {
+              const float hv = __fmul_rn(det_silu(s0), s1);
+              p.h_out[(int64_t)(off + t0 + t) * p.F + row] = f32_to_bf16(hv);
+            }
+          } else if (lane == t) {
+            p.y[(int64_t)(off + t0 + t) * p.H + row] = s0;
           }
         }
       }
@@ -281,58 +314,38 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_up_kernel(const FfnParams 
   }
 }
 
-template <int TT>
-__global__ void __launch_bounds__(kFfnThreads, 1) ffn_down_kernel(const FfnParams p) {
-  __shared__ int s_active[kMaxFfnExperts];
-  __shared__ int s_off[kMaxFfnExperts + 1];
-  const int n_active = gather_active(p, s_active, s_off);
-  const int lane = threadIdx.x & 31;
-  const int gwarp = blockIdx.x * (kFfnThreads / 32) + (threadIdx.x >> 5);
-  const int nwarps = gridDim.x * (kFfnThreads / 32);
-  // a warp owns the row pair (h, h+1) of W2 so every activation chunk it
-  // loads feeds two weight chunks (as W1/W3 do in the up phase); H is even
-  const int half = p.H >> 1;
-  const int64_t total = (int64_t)n_active * half;
-  const int nchunks = p.F >> 3;
-  for (int64_t u = gwarp; u < total; u += nwarps) {
-    const int a = (int)(u / half);
-    const int hrow = 2 * (int)(u - (int64_t)a * half);
-    const int e = s_active[a];
-    const uint16_t* blob = p.pool + (int64_t)p.slot[e] * p.slot_elems;
-    const uint16_t* w2 = blob + 2 * (int64_t)p.F * p.H + (int64_t)hrow * p.F;
-    const uint4* const wr[2] = {reinterpret_cast<const uint4*>(w2),
-                                reinterpret_cast<const uint4*>(w2 + p.F)};
-    const int off = s_off[e];
-    const int cnt = s_off[e + 1] - off;
-    for (int t0 = 0; t0 < cnt; t0 += TT) {
-      const int nt = min(TT, cnt - t0);
-      const uint4* ar[TT];
-#pragma unroll
-      for (int t = 0; t < TT; ++t)
-        ar[t] = reinterpret_cast<const uint4*>(p.h + (int64_t)(off + t0 + min(t, nt - 1)) * p.F);
-      float acc[2][TT];
-#pragma unroll
-      for (int t = 0; t < TT; ++t) { acc[0][t] = 0.0f; acc[1][t] = 0.0f; }
-      stream_rows<TT, 2, 8>(wr, ar, nt, nchunks, lane, acc);
-#pragma unroll
-      for (int t = 0; t < TT; ++t) {
-        if (t < nt) {
-          const float y0 = warp_sum_fixed(acc[0][t]);
-          const float y1 = warp_sum_fixed(acc[1][t]);
-          if (lane == t)
-            *reinterpret_cast<float2*>(p.y + (int64_t)(off + t0 + t) * p.H + hrow) = make_float2(y0, y1);
-        }
-      }
-    }
-  }
+constexpr int kActSmemCap = 200 * 1024;
+
+// Register tile: the smallest of 1/2/4/8 covering the hint that also fits
+// the activation stage (TT x K bf16) in shared memory.
+int pick_tile(int hint, int K) {
+  int tt = hint <= 0 ? 8 : hint <= 1 ? 1 : hint <= 2 ? 2 : hint <= 4 ? 4 : 8;
+  while (tt > 1 && (size_t)tt * K * 2 > (size_t)kActSmemCap) tt >>= 1;
+  return tt;
 }
 
-int pick_tile(int hint) {
-  if (hint <= 0) return 8;
-  if (hint <= 1) return 1;
-  if (hint <= 2) return 2;
-  if (hint <= 4) return 4;
-  return 8;
+template <bool UP, int TT>
+int launch_ffn(const FfnParams& p, cudaStream_t s) {
+  const int K = UP ? p.H : p.F;
+  const size_t smem = (size_t)TT * K * 2;
+  if (smem > (size_t)kActSmemCap) return (int)cudaErrorInvalidValue;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(ffn_kernel<UP, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kActSmemCap);
+    configured = true;
+  }
+  ffn_kernel<UP, TT><<<num_sms(), kFfnThreads, smem, s>>>(p);
+  return launch_status();
+}
+
+template <bool UP>
+int launch_ffn_tt(const FfnParams& p, int hint, cudaStream_t s) {
+  switch (pick_tile(hint, UP ? p.H : p.F)) {
+    case 1: return launch_ffn<UP, 1>(p, s);
+    case 2: return launch_ffn<UP, 2>(p, s);
+    case 4: return launch_ffn<UP, 4>(p, s);
+    default: return launch_ffn<UP, 8>(p, s);
+  }
 }
 
 bool fill_params(FfnParams& p, const uint16_t* pool, int64_t slot_elems,
@@ -520,13 +533,8 @@ int spmoe_expert_ffn_up(const uint16_t* pool, int64_t slot_elems, const int32_t*
   p.h_out = h_scratch;
   const int grid = num_sms();
   cudaStream_t s = (cudaStream_t)stream;
-  switch (pick_tile(max_tokens_per_expert)) {
-    case 1: ffn_up_kernel<1><<<grid, kFfnThreads, 0, s>>>(p); break;
-    case 2: ffn_up_kernel<2><<<grid, kFfnThreads, 0, s>>>(p); break;
-    case 4: ffn_up_kernel<4><<<grid, kFfnThreads, 0, s>>>(p); break;
-    default: ffn_up_kernel<8><<<grid, kFfnThreads, 0, s>>>(p); break;
-  }
-  return launch_status();
+  (void)grid;
+  return launch_ffn_tt<true>(p, max_tokens_per_expert, s);
 }
 
 int spmoe_expert_ffn_down(const uint16_t* pool, int64_t slot_elems,
@@ -544,13 +552,8 @@ int spmoe_expert_ffn_down(const uint16_t* pool, int64_t slot_elems,
   p.y = y;
   const int grid = num_sms();
   cudaStream_t s = (cudaStream_t)stream;
-  switch (pick_tile(max_tokens_per_expert)) {
-    case 1: ffn_down_kernel<1><<<grid, kFfnThreads, 0, s>>>(p); break;
-    case 2: ffn_down_kernel<2><<<grid, kFfnThreads, 0, s>>>(p); break;
-    case 4: ffn_down_kernel<4><<<grid, kFfnThreads, 0, s>>>(p); break;
-    default: ffn_down_kernel<8><<<grid, kFfnThreads, 0, s>>>(p); break;
-  }
-  return launch_status();
+  (void)grid;
+  return launch_ffn_tt<false>(p, max_tokens_per_expert, s);
 }
 
 int spmoe_expert_ffn(const uint16_t* pool, int64_t slot_elems, const int32_t* slot_of_expert,

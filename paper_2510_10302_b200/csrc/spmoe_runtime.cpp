@@ -589,3 +589,25 @@ int spmoe_host_register(void* host, size_t bytes) {
 int spmoe_host_unregister(void* host) { return (int)cudaHostUnregister(host); }
 
 }  // extern "C"
+
+extern "C" {
+
+int spmoe_event_create(void** ev) {
+  if (!ev) return (int)cudaErrorInvalidValue;
+  return (int)cudaEventCreateWithFlags((cudaEvent_t*)ev, cudaEventDisableTiming);
+}
+
+int spmoe_event_destroy(void* ev) { return (int)cudaEventDestroy((cudaEvent_t)ev); }
+
+int spmoe_event_record_external(void* ev, void* stream) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing((cudaStream_t)stream, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    return (int)cudaEventRecordWithFlags((cudaEvent_t)ev, (cudaStream_t)stream,
+                                         cudaEventRecordExternal);
+  return (int)cudaEventRecord((cudaEvent_t)ev, (cudaStream_t)stream);
+}
+
+int spmoe_event_synchronize(void* ev) { return (int)cudaEventSynchronize((cudaEvent_t)ev); }
+
+}  // extern "C"

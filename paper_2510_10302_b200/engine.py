@@ -34,13 +34,14 @@ times from CUDA events: ``expert_load`` is the time the compute stream sat in
 
 from __future__ import annotations
 
-import math
+import ctypes as C
 import time
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
+from . import _native
 from . import kernels as K
 from .cache import ExpertId, NativeExpertCache
 from .config import HardwareSpec, Policy, PolicySpec, ProfiledTimings, ValidationError, cache_capacity_slots
@@ -121,6 +122,7 @@ class SpecMoEEngine:
         record_timeline: bool = False,
         record: bool = False,
         capture_layers: tuple[int, ...] = (),
+        cuda_graphs: bool = True,
     ):
         if not torch.cuda.is_available():
             raise RuntimeError("SpecMoEEngine needs a CUDA device (there is no CPU fallback)")
@@ -171,7 +173,14 @@ class SpecMoEEngine:
         self.pred_idx = torch.empty((batch, pk), dtype=torch.int32, device=self.device)
         # mapped host buffer receiving verify routing (zero-copy hand-off)
         self.route_ring = DraftGuidedPredictor(entries=1, width=max(T_max * arch.top_k, 1))
-        self._route_ev = torch.cuda.Event()
+        self._lib = _native.load()
+        _ev = C.c_void_p()
+        _native.check("spmoe_event_create", self._lib.spmoe_event_create(C.byref(_ev)))
+        self._route_ev = _ev.value
+        self.use_graphs = cuda_graphs and not (
+            policy.policy is Policy.DRAFT_PREFETCH and not policy.worker_prefetch
+        )
+        self._graphs_ready = False
         self.history = HistoryCounter(arch.num_layers, arch.num_experts)
         self._history_bufs: list[np.ndarray] = []
         self.use_worker = policy.worker_prefetch and policy.policy in (Policy.DRAFT_PREFETCH, Policy.COARSE_HISTORY)
@@ -269,24 +278,34 @@ class SpecMoEEngine:
             "total_ms": tot_ms,
         }
 
-    def _moe_verify(self, l: int, xn: torch.Tensor, resid: torch.Tensor, s: _Scratch) -> torch.Tensor:
+    def _route(self, l: int, xn: torch.Tensor, s: _Scratch):
+        """K1 on the verify tokens; indices also land in the mapped route ring
+        (zero-copy hand-off to the host), then the route event is recorded
+        (as an external graph node when captured)."""
         a = self.arch
         lw = self.weights.layers[l]
-        T, H = xn.shape
-        k, E = a.top_k, a.num_experts
+        T = xn.shape[0]
         w, idx, _, sg = K.router_topk(
             xn,
             lw.router,
-            k,
+            a.top_k,
             a.renorm,
             host_idx_dev_ptr=self.route_ring.dev_ptr,
             shared_gate_w=lw.shared_gate,
             out=(s.w[:T], s.idx[:T]),
         )
-        self._route_ev.record()
+        self._lib.spmoe_event_record_external(self._route_ev, self.stream.cuda_stream)
+        return w, idx, sg
+
+    def _moe_verify(self, l: int, xn: torch.Tensor, resid: torch.Tensor, s: _Scratch, routed=None) -> torch.Tensor:
+        a = self.arch
+        lw = self.weights.layers[l]
+        T, H = xn.shape
+        k, E = a.top_k, a.num_experts
+        w, idx, sg = routed if routed is not None else self._route(l, xn, s)
         if self.policy.policy is Policy.GATING_NEXT_LAYER and l + 1 < a.num_layers:
             self._gating_predict(l + 1, xn)
-        self._route_ev.synchronize()
+        self._lib.spmoe_event_synchronize(self._route_ev)
         ids = self.route_ring.view[0, : T * k].copy()
         self.history.record_many(l, ids)
         if self.record:
@@ -346,7 +365,7 @@ class SpecMoEEngine:
         i, hptr, ev = self.predictor.predict(
             x_pos, self.weights.layers[layer].router, pk, True, self.scratch.pw[:B, :pk], self.scratch.pidx[:B, :pk]
         )
-        self.cache.push_task(layer, hptr, B * pk, ev.cuda_event)
+        self.cache.push_task(layer, hptr, B * pk, ev)
         self._pushed.append((layer, i))
         self._drain()
         for e in set(int(v) for v in self.predictor.view[i][: B * pk] if v >= 0):
@@ -358,30 +377,108 @@ class SpecMoEEngine:
     def _embed(self, tokens: torch.Tensor) -> torch.Tensor:
         return self.weights.embed[tokens]
 
-    def _draft_forward(self, tokens: torch.Tensor, start: torch.Tensor, kv_len_max: int, predict_step: int | None):
+    def _draft_forward(self, tokens: torch.Tensor, start: torch.Tensor, kv_len_max: int, predict_step: int | None,
+                       ring_base: int | None = None):
         """Draft pass over ``tokens`` [B, T]; returns last-token logits [B, V] f32.
         ``predict_step`` (iteration-local draft step index) enables Algorithm 1
-        at layers <= cutoff."""
+        at layers <= cutoff: eagerly (predict + push per layer) or, with
+        ``ring_base`` set (CUDA-graph capture), K1 into ring entry
+        ring_base + l plus an external event node; the host pushes the tasks
+        after launching the graph."""
         a, w = self.arch, self.weights
         B, T = tokens.shape
         x = self._embed(tokens)
         s = self.scratch if B * T <= self.scratch.T else self._prefill_scratch(B * T)
         spmoe = predict_step is not None and self.cutoff is not None
+        pk = self.policy.prefetch_k
         for l in range(a.num_layers):
             lw = w.layers[l]
             h = rms_norm(x, lw.attn_norm, a.rms_eps)
             x = x + attention(w, l, h, self.draft_kv, start, kv_len_max)
             hn = rms_norm(x, lw.ffn_norm, a.rms_eps)
             if spmoe and l <= self.cutoff:
-                self._predict_and_enqueue(l, hn[:, -1, :].contiguous(), predict_step)
+                if ring_base is None:
+                    self._predict_and_enqueue(l, hn[:, -1, :].contiguous(), predict_step)
+                else:
+                    self.predictor.predict_at(ring_base + l, hn[:, -1, :].contiguous(), lw.router, pk, True,
+                                              self.pred_w, self.pred_idx)
             x = self._dense_ffn(lw.draft_ffn, a.d_ffn, hn.reshape(B * T, -1), x.reshape(B * T, -1), s).view(B, T, -1)
         hn = rms_norm(x[:, -1, :], w.final_norm, a.rms_eps)
         return torch.matmul(hn, w.lm_head.t()).float()
 
+    # ------------------------------------------------------------ CUDA graphs
+    def _capture(self, fn) -> torch.cuda.CUDAGraph:
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            fn()  # warm-up outside capture (kernel selection, workspaces)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        # thread_local: the prefetch worker thread may call CUDA (event
+        # queries, copies on its own stream) while the main thread captures
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            fn()
+        return g
+
+    def _ensure_graphs(self) -> None:
+        """Capture, once per engine (after prefill): one graph per draft step
+        (embed, 32 layers with attention, predictor K1 + external event
+        nodes, dense FFN, lm_head, argmax) and one graph per verify layer for
+        the pre-MoE block (norm, attention, norm, router K1 + route event).
+        Static buffers: base positions, step-0 tokens, draft tokens, the
+        verify residual stream and MLP input."""
+        if self._graphs_ready or not self.use_graphs:
+            return
+        a, B, N = self.arch, self.batch, self.policy.draft_length
+        dev = self.device
+        L, H = a.num_layers, a.hidden
+        T = N + 1
+        self._g_base = torch.zeros((B,), dtype=torch.int64, device=dev)
+        self._g_tok0 = torch.zeros((B, 2), dtype=torch.int64, device=dev)
+        self._g_draft = torch.zeros((B, N), dtype=torch.int32, device=dev)
+        self._h_base = torch.zeros((B,), dtype=torch.int64).pin_memory()
+        self._h_tok0 = torch.zeros((B, 2), dtype=torch.int64).pin_memory()
+        self._vx = torch.zeros((B * T, H), dtype=torch.bfloat16, device=dev)
+        self._vxn = torch.zeros((B * T, H), dtype=torch.bfloat16, device=dev)
+        self._vstart = torch.zeros((B,), dtype=torch.int64, device=dev)
+        self._h_vstart = torch.zeros((B,), dtype=torch.int64).pin_memory()
+        # plausible positions for the warm-up/capture runs (overwritten later)
+        P0 = min(len(sq) for sq in self.seqs)
+        self._g_base.fill_(P0 - 2)
+        self._vstart.fill_(P0 - 1)
+        dkv, tkv = self.draft_kv.max_seq, self.target_kv.max_seq
+
+        def draft_fn(d):
+            def fn():
+                if d == 0:
+                    tok, start = self._g_tok0, self._g_base
+                else:
+                    tok, start = self._g_draft[:, d - 1 : d].long(), self._g_base + (d + 1)
+                logits = self._draft_forward(tok, start, dkv, d, ring_base=d * L)
+                self._g_draft[:, d].copy_(K.argmax_rows(logits))
+            return fn
+
+        self._vroute: list = [None] * L
+
+        def verify_fn(l):
+            def fn():
+                lw = self.weights.layers[l]
+                x = self._vx.view(B, T, H)
+                h = rms_norm(x, lw.attn_norm, a.rms_eps)
+                x.add_(attention(self.weights, l, h, self.target_kv, self._vstart, tkv))
+                self._vxn.copy_(rms_norm(x, lw.ffn_norm, a.rms_eps).view(B * T, H))
+                self._vroute[l] = self._route(l, self._vxn, self.scratch)
+            return fn
+
+        self._draft_graphs = [self._capture(draft_fn(d)) for d in range(N)]
+        self._verify_graphs = [self._capture(verify_fn(l)) for l in range(L)]
+        torch.cuda.synchronize(dev)
+        self._graphs_ready = True
+
     def _predict_and_enqueue(self, l: int, x_last: torch.Tensor, step: int) -> None:
         pk = self.policy.prefetch_k
         i, hptr, ev = self.predictor.predict(x_last, self.weights.layers[l].router, pk, True, self.pred_w, self.pred_idx)
-        self.cache.push_task(l, hptr, self.predictor.width, ev.cuda_event, step)
+        self.cache.push_task(l, hptr, self.predictor.width, ev, step)
         self._pushed.append((l, i))
         if not self.policy.worker_prefetch:
             # vanilla executor: block until the copies are issued, and make the
@@ -401,18 +498,8 @@ class SpecMoEEngine:
         a, w = self.arch, self.weights
         B, T = tokens.shape
         x = self._embed(tokens)
-        sp = self.stream.cuda_stream
         for l in range(a.num_layers):
-            if self._pending_gating:
-                waits = [sl for (ly, sl) in self._pending_gating if ly == l]
-                self._pending_gating = [(ly, sl) for (ly, sl) in self._pending_gating if ly != l]
-                for sl in waits:
-                    if not self.cache.slot_ready(sl):
-                        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                        ea.record()
-                        self.cache.wait_slot(sl, sp)
-                        eb.record()
-                        self.stalls.append(_Stall("prefetch", l, ea, eb))
+            self._gating_waits(l)
             lw = w.layers[l]
             h = rms_norm(x, lw.attn_norm, a.rms_eps)
             x = x + attention(w, l, h, self.target_kv, start, kv_len_max)
@@ -420,6 +507,59 @@ class SpecMoEEngine:
             x = self._moe_verify(l, hn.reshape(B * T, -1).contiguous(), x.reshape(B * T, -1).contiguous(), s).view(B, T, -1)
         hn = rms_norm(x, w.final_norm, a.rms_eps)
         return torch.matmul(hn, w.lm_head.t()).float()
+
+    def _step_graphed(self, P: list[int], N: int, ev1):
+        """Drafting + verification with the captured graphs; the per-layer
+        verify MoE (host cache logic, demand loads, K2-K4) stays eager."""
+        a, B = self.arch, self.batch
+        L, H, T = a.num_layers, a.hidden, N + 1
+        for b, sq in enumerate(self.seqs):
+            self._h_base[b] = P[b] - 2
+            self._h_tok0[b, 0] = sq[-2]
+            self._h_tok0[b, 1] = sq[-1]
+            self._h_vstart[b] = P[b] - 1
+        self._g_base.copy_(self._h_base, non_blocking=True)
+        self._g_tok0.copy_(self._h_tok0, non_blocking=True)
+        self._vstart.copy_(self._h_vstart, non_blocking=True)
+        spmoe = self.cutoff is not None and self.policy.policy is Policy.DRAFT_PREFETCH
+        width = self.predictor.width
+        for d in range(N):
+            self._draft_graphs[d].replay()
+            if spmoe:
+                # tasks are pushed after the graph is enqueued, so the worker
+                # waits on this replay's event nodes (Algorithm 1 l.8-9)
+                for l in range(self.cutoff + 1):
+                    i = d * L + l
+                    self.cache.push_task(l, self.predictor.host_ptr_of(i), width, self.predictor.events[i], d)
+                    self._pushed.append((l, i))
+        ev1.record(self.stream)
+        if self.use_worker:
+            self._drain()
+        draft_tok = self._g_draft
+        # verify: embed [last committed, drafts] into the static residual stream
+        vtok = torch.cat([self._g_tok0[:, 1:2], draft_tok.long()], dim=1)
+        self._vx.copy_(self._embed(vtok).view(B * T, H))
+        for l in range(L):
+            self._gating_waits(l)
+            self._verify_graphs[l].replay()
+            self._moe_verify(l, self._vxn, self._vx, self.scratch, routed=self._vroute[l])
+        hn = rms_norm(self._vx.view(B, T, H), self.weights.final_norm, a.rms_eps)
+        logits = torch.matmul(hn, self.weights.lm_head.t()).float()
+        return logits, draft_tok
+
+    def _gating_waits(self, l: int) -> None:
+        if not self._pending_gating:
+            return
+        sp = self.stream.cuda_stream
+        waits = [sl for (ly, sl) in self._pending_gating if ly == l]
+        self._pending_gating = [(ly, sl) for (ly, sl) in self._pending_gating if ly != l]
+        for sl in waits:
+            if not self.cache.slot_ready(sl):
+                ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ea.record()
+                self.cache.wait_slot(sl, sp)
+                eb.record()
+                self.stalls.append(_Stall("prefetch", l, ea, eb))
 
     def _prefill_scratch(self, T: int) -> _Scratch:
         if self.prefill_scratch is None or self.prefill_scratch.T < T:
@@ -445,6 +585,7 @@ class SpecMoEEngine:
         self._target_forward(ctx, start, P - 1, s)
         self.cache.drain()
         torch.cuda.synchronize(self.device)
+        self._ensure_graphs()
         self.cache.reset_stats()
         self.cache.clear_log()
         self.history = HistoryCounter(self.arch.num_layers, self.arch.num_experts)
@@ -474,28 +615,33 @@ class SpecMoEEngine:
         ev0.record(st)
         if pol.policy is Policy.COARSE_HISTORY:
             self._coarse_history_enqueue()
-        # ---- drafting
         P = [len(sq) for sq in self.seqs]
-        first = torch.tensor([[sq[-2], sq[-1]] for sq in self.seqs], dtype=torch.int64, device=dev)
-        start = torch.tensor([p - 2 for p in P], dtype=torch.int64, device=dev)
-        drafts = []
-        inp = first
-        for d in range(N):
-            logits = self._draft_forward(inp, start, max(P) + d, d)
-            tok = K.argmax_rows(logits)
-            drafts.append(tok)
-            start = (start + inp.shape[1]) if d == 0 else start + 1
-            inp = tok.long().view(B, 1)
-        draft_tok = torch.stack(drafts, dim=1).contiguous()  # [B, N] int32
-        ev1.record(st)
-        # ---- verification
-        if self.use_worker:
-            self._drain()
-        last = torch.tensor([[sq[-1]] for sq in self.seqs], dtype=torch.int64, device=dev)
-        vtok = torch.cat([last, draft_tok.long()], dim=1)  # [B, N+1]
-        vstart = torch.tensor([p - 1 for p in P], dtype=torch.int64, device=dev)
-        s = self.scratch if B * (N + 1) <= self.scratch.T else self._prefill_scratch(B * (N + 1))
-        logits = self._target_forward(vtok, vstart, max(P) + N, s)
+        graphs = self.use_graphs and N == pol.draft_length
+        if graphs:
+            self._ensure_graphs()
+            logits, draft_tok = self._step_graphed(P, N, ev1)
+        else:
+            # ---- drafting (eager)
+            first = torch.tensor([[sq[-2], sq[-1]] for sq in self.seqs], dtype=torch.int64, device=dev)
+            start = torch.tensor([p - 2 for p in P], dtype=torch.int64, device=dev)
+            drafts = []
+            inp = first
+            for d in range(N):
+                logits = self._draft_forward(inp, start, max(P) + d, d)
+                tok = K.argmax_rows(logits)
+                drafts.append(tok)
+                start = (start + inp.shape[1]) if d == 0 else start + 1
+                inp = tok.long().view(B, 1)
+            draft_tok = torch.stack(drafts, dim=1).contiguous()  # [B, N] int32
+            ev1.record(st)
+            # ---- verification (eager)
+            if self.use_worker:
+                self._drain()
+            last = torch.tensor([[sq[-1]] for sq in self.seqs], dtype=torch.int64, device=dev)
+            vtok = torch.cat([last, draft_tok.long()], dim=1)  # [B, N+1]
+            vstart = torch.tensor([p - 1 for p in P], dtype=torch.int64, device=dev)
+            s = self.scratch if B * (N + 1) <= self.scratch.T else self._prefill_scratch(B * (N + 1))
+            logits = self._target_forward(vtok, vstart, max(P) + N, s)
         _, res = K.greedy_accept(logits.contiguous(), draft_tok)
         if self.record:
             self.captures.append({"accept_logits": logits.clone(), "draft": draft_tok.clone(), "res": res.clone()})

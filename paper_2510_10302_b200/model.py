@@ -68,6 +68,16 @@ class ArchSpec:
     # random-init SD accepts drafts at a realistic rate (SURVEY.md §7 hard
     # part 2).  Bytes moved and FLOPs are unchanged.
     expert_spread: float | None = 0.25
+    # init scales: token embedding std, and GPT-2-style residual-branch
+    # scaling of the output projections (W_o, W2): std * residual_scale,
+    # None -> 1/sqrt(2 * num_layers).  Keeps the 32-layer random network out
+    # of the chaotic regime so a slightly different draft still agrees.
+    embed_std: float = 0.02
+    residual_scale: float | None = None
+
+    @property
+    def res_scale(self) -> float:
+        return self.residual_scale if self.residual_scale is not None else 1.0 / math.sqrt(2 * self.num_layers)
 
     def __post_init__(self):
         if self.hidden % 8 or self.ffn % 8 or (self.shared_ffn % 8):
@@ -278,7 +288,7 @@ def build_weights(
     H, E, F = arch.hidden, arch.num_experts, arch.ffn
     bf = torch.bfloat16
     std = arch.init_std
-    embed = _fill(torch.empty((arch.vocab, H), dtype=bf, device=device), tensor_seed(seed, K_EMBED), std)
+    embed = _fill(torch.empty((arch.vocab, H), dtype=bf, device=device), tensor_seed(seed, K_EMBED), arch.embed_std)
     lm_head = _fill(torch.empty((arch.vocab, H), dtype=bf, device=device), tensor_seed(seed, K_LMHEAD), std)
     layers = []
     stage = torch.empty((min(chunk_experts, E), arch.expert_elems), dtype=bf, device=device)
@@ -287,14 +297,14 @@ def build_weights(
         wo = _fill(
             torch.empty((H, arch.num_heads * arch.head_dim), dtype=bf, device=device),
             tensor_seed(seed, K_WO, l),
-            std,
+            std * arch.res_scale,
         )
         router = _fill(torch.empty((E, H), dtype=bf, device=device), tensor_seed(seed, K_ROUTER, l), 1.0 / math.sqrt(H))
         acc = torch.zeros((arch.expert_elems,), dtype=torch.float32, device=device)
         base = None
         if arch.expert_spread is not None:
             base = torch.empty((arch.expert_elems,), dtype=bf, device=device)
-            fill_blob_generic(base, F, H, tensor_seed(seed, K_BASE, l), std, arch.expert_out_scale)
+            fill_blob_generic(base, F, H, tensor_seed(seed, K_BASE, l), std, arch.expert_out_scale * arch.res_scale)
         for e0 in range(0, E, stage.shape[0]):
             n = min(stage.shape[0], E - e0)
             for j in range(n):
@@ -312,7 +322,7 @@ def build_weights(
         del acc, base
         if arch.d_ffn != F:
             draft = torch.empty((1, 3 * arch.d_ffn * H), dtype=bf, device=device)
-            fill_blob_generic(draft[0], arch.d_ffn, H, tensor_seed(seed, K_EXPERT, l, 10_000), std, arch.expert_out_scale)
+            fill_blob_generic(draft[0], arch.d_ffn, H, tensor_seed(seed, K_EXPERT, l, 10_000), std, arch.expert_out_scale * arch.res_scale)
         else:
             draft = mean.view(1, -1).clone()
         if draft_perturb > 0.0:
@@ -323,7 +333,7 @@ def build_weights(
         sgate = None
         if arch.shared_ffn:
             shared = torch.empty((1, 3 * arch.shared_ffn * H), dtype=bf, device=device)
-            fill_blob_generic(shared[0], arch.shared_ffn, H, tensor_seed(seed, K_SHARED, l), std, arch.expert_out_scale)
+            fill_blob_generic(shared[0], arch.shared_ffn, H, tensor_seed(seed, K_SHARED, l), std, arch.expert_out_scale * arch.res_scale)
             if arch.shared_gate:
                 sgate = _fill(torch.empty((H,), dtype=bf, device=device), tensor_seed(seed, K_SGATE, l), 1.0 / math.sqrt(H))
         layers.append(
@@ -364,7 +374,7 @@ def fill_expert_blob(blob: torch.Tensor, arch: ArchSpec, seed: int, row: int) ->
     """Routed expert content is a function of its host-pool row (row =
     layer*E + expert unless the pool aliases)."""
     fill_blob_generic(
-        blob, arch.ffn, arch.hidden, tensor_seed(seed, K_EXPERT, row), arch.init_std, arch.expert_out_scale
+        blob, arch.ffn, arch.hidden, tensor_seed(seed, K_EXPERT, row), arch.init_std, arch.expert_out_scale * arch.res_scale
     )
 
 

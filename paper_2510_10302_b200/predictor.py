@@ -94,33 +94,55 @@ class DraftGuidedPredictor:
         buf = (C.c_int32 * (entries * width)).from_address(self.host_ptr)
         self.view = np.ctypeslib.as_array(buf).reshape(entries, width)
         self.view[:] = -1
-        self.events = [torch.cuda.Event() for _ in range(entries)]
+        # raw CUDA events (recorded as external event nodes when a draft step
+        # is captured in a CUDA graph, so the worker can wait on them)
+        self.events = []
+        for _ in range(entries):
+            ev = C.c_void_p()
+            _native.check("spmoe_event_create", lib.spmoe_event_create(C.byref(ev)))
+            self.events.append(ev.value)
         self.next = 0
 
     def reset(self) -> None:
         self.next = 0
 
-    def entry(self):
+    def entry(self) -> int:
         if self.next >= self.entries:
             raise RuntimeError("predictor ring exhausted (drain before reuse)")
-        i = self.next
         self.next += 1
-        return i, self.host_ptr + 4 * i * self.width, self.dev_ptr + 4 * i * self.width, self.events[i]
+        return self.next - 1
 
-    def predict(self, x_last, router_w, k: int, renorm: bool, weights_out, idx_out):
-        """Run K1 on ``x_last`` [B, H] against the target router; returns the
-        ring entry (index, host_ptr, event) after recording the event."""
+    def host_ptr_of(self, i: int) -> int:
+        return self.host_ptr + 4 * i * self.width
+
+    def predict_at(self, i: int, x_last, router_w, k: int, renorm: bool, weights_out, idx_out) -> None:
+        """K1 on ``x_last`` [B, H] against the target router writing ring
+        entry ``i``, then record entry i's event on the current stream."""
+        import torch
+
+        from . import _native
         from .kernels import router_topk
 
-        i, hptr, dptr, ev = self.entry()
+        dptr = self.dev_ptr + 4 * i * self.width
         router_topk(x_last, router_w, k, renorm, host_idx_dev_ptr=dptr, out=(weights_out, idx_out))
-        ev.record()
-        return i, hptr, ev
+        _native.check(
+            "spmoe_event_record_external",
+            self._lib.spmoe_event_record_external(self.events[i], torch.cuda.current_stream().cuda_stream),
+        )
+
+    def predict(self, x_last, router_w, k: int, renorm: bool, weights_out, idx_out):
+        """Eager form: next free entry; returns (index, host_ptr, event)."""
+        i = self.entry()
+        self.predict_at(i, x_last, router_w, k, renorm, weights_out, idx_out)
+        return i, self.host_ptr_of(i), self.events[i]
 
     def close(self) -> None:
         import ctypes as C
 
         if getattr(self, "host_ptr", None):
             self.view = None
+            for ev in self.events:
+                self._lib.spmoe_event_destroy(ev)
+            self.events = []
             self._lib.spmoe_host_free(C.c_void_p(self.host_ptr))
             self.host_ptr = None

@@ -21,6 +21,12 @@ def bits(t: torch.Tensor) -> np.ndarray:
     return t.contiguous().cpu().numpy()
 
 
+def _native_lib():
+    from paper_2510_10302_b200 import _native
+
+    return _native.load()
+
+
 def to_dev_bf16(a_u16: np.ndarray) -> torch.Tensor:
     return torch.from_numpy(a_u16.view(np.int16).copy()).view(torch.bfloat16).cuda()
 
@@ -118,7 +124,7 @@ def test_router_host_mapped_handoff(oracle):
         w = rand_bf16((64, 4096), 6, std=1 / 64)
         i, hptr, ev = ring.predict(x.cuda(), w.cuda(), 3, False, torch.empty((1, 3), device="cuda"),
                                    torch.empty((1, 3), dtype=torch.int32, device="cuda"))
-        ev.synchronize()
+        _native_lib().spmoe_event_synchronize(ev)
         _, io, _, _ = oracle.router_topk(bits(x), bits(w), 3, False)
         assert list(ring.view[i]) == list(io[0])
     finally:
