@@ -128,6 +128,21 @@ int spmoe_expert_ffn_down(const uint16_t* pool, int64_t slot_elems,
                           const uint16_t* h_scratch, float* y, int max_tokens_per_expert,
                           void* stream);
 
+/*
+ * tcgen05/TMEM/TMA variant of spmoe_expert_ffn (same inputs, same h / y
+ * outputs): weight rows as the UMMA M=128 operand, routed tokens as N
+ * (<= 64 per tile), TMA over a 3-D tensor map of the slot pool, fp32
+ * accumulators in TMEM.  Needs H % 128 == 0 and F % 128 == 0.  Workspaces:
+ * x_perm [T*k, H] bf16 (routed rows gathered by perm_token), y_split
+ * [split_k, T*k, H] f32 (down-phase split-K partials, reduced in fixed
+ * order; unused when split_k == 1).  Results equal the CUDA-core path
+ * within fp32 rounding of the tensor core's accumulation order.
+ */
+int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, const int32_t* slot_of_expert,
+                        uint64_t expert_mask, const uint16_t* x, int T, int H, int F, int E, int k,
+                        const int32_t* expert_offsets, const int32_t* perm_token, uint16_t* x_perm,
+                        uint16_t* h_scratch, float* y, float* y_split, int split_k, void* stream);
+
 /* --------------------------------------------------------------------- */
 /* K4  moe_combine                                                        */
 /*   Eq. 1 weighted sum Output = sum_i G(x)_i E_i(x)  */

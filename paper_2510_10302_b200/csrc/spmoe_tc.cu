@@ -1,0 +1,475 @@
+// spmoe_tc.cu — tcgen05/TMEM/TMA path of K3 (grouped SwiGLU over the HBM
+// slot pool) for sm_100a.
+//
+// Swap-AB: the expert weight rows are the MMA's M dimension (tiles of 128
+// rows), the routed tokens of one expert are N (padded to a multiple of 16,
+// at most 64 per tile), K is the reduction (H for the up phase, F for the
+// down phase).  Weight tiles [128 x 64] and activation tiles [64 x 64] are
+// fetched by TMA (128B swizzle) from 3-D tensor maps over the slot pool
+// (slot = outer coordinate, so no per-expert descriptor rebuilds) into a
+// multi-stage shared-memory ring; one elected thread issues tcgen05.mma
+// (kind::f16, bf16 x bf16 -> fp32) into a double-buffered TMEM accumulator;
+// four epilogue warps drain TMEM with tcgen05.ld and apply SiLU*up (up
+// phase) or write fp32 partial sums (down phase, split-K, reduced in a fixed
+// order afterwards).
+//
+// Numerics: fp32 accumulation in the tensor core's order, so results match
+// the CPU oracle within fp32 rounding (tolerance documented in
+// tests/test_tc_gpu.py) rather than bit for bit; the CUDA-core path of
+// spmoe_kernels.cu is the bit-exact one.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/spmoe.h"
+#include "spmoe_common.cuh"
+
+using namespace spmoe;
+
+namespace tc {
+
+constexpr int BM = 128;  // weight rows per tile (UMMA M)
+constexpr int BK = 64;   // K elements per stage (128 bytes: one swizzle atom row)
+constexpr int BN = 64;   // max tokens per tile (activation box rows)
+constexpr int kThreads = 192;  // warp 0 TMA, warp 1 MMA + TMEM alloc, warps 2-5 epilogue
+constexpr int kMaxExperts = 64;
+constexpr int kTmemCols = 256;
+
+struct Params {
+  uint64_t mask;
+  const int32_t* offsets;
+  uint16_t* h_out;  // up: [rows, F] bf16
+  float* y_part;    // down: [split][rows, H] fp32
+  int E, H, F, rows, split;
+  int slot[kMaxExperts];
+};
+
+// ------------------------------------------------------------------ PTX
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// K-major operand, 128-byte swizzle, 8-row atoms of 1024 bytes (SBO), LBO
+// unused (1), descriptor version 1 (sm100), layout type 2 = SWIZZLE_128B.
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  return ((addr & 0x3FFFFull) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128.
+__device__ __forceinline__ uint32_t instr_desc(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                     uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 32 lanes x 16 columns of 32-bit from TMEM (one row per thread).
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32"
+      " {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ------------------------------------------------------------ tile list
+// Tiles enumerate (active expert, token chunk of <= BN, 128-row block,
+// K split); every role walks the same static sequence.
+struct TileList {
+  int n_active;
+  int active[kMaxExperts];
+  int start[kMaxExperts + 1];  // prefix of tiles per active expert
+};
+
+__device__ __forceinline__ void build_tiles(const Params& p, int mtiles, int split, TileList* tl) {
+  if (threadIdx.x == 0) {
+    int n = 0, acc = 0;
+    for (int e = 0; e < p.E; ++e) {
+      const int cnt = p.offsets[e + 1] - p.offsets[e];
+      if (((p.mask >> e) & 1ull) && cnt > 0) {
+        tl->active[n] = e;
+        tl->start[n] = acc;
+        acc += ((cnt + BN - 1) / BN) * mtiles * split;
+        ++n;
+      }
+    }
+    tl->start[n] = acc;
+    tl->n_active = n;
+  }
+}
+
+struct Tile {
+  int e, n0, ntok, m0, kb0, kb1, ks;
+};
+
+__device__ __forceinline__ Tile decode(const Params& p, const TileList& tl, int tile, int mtiles, int split,
+                                       int kblocks) {
+  int a = 0;
+  while (tile >= tl.start[a + 1]) ++a;
+  int r = tile - tl.start[a];
+  Tile t;
+  t.e = tl.active[a];
+  t.ks = r % split;
+  r /= split;
+  t.m0 = (r % mtiles) * BM;
+  r /= mtiles;
+  t.n0 = r * BN;
+  const int cnt = p.offsets[t.e + 1] - p.offsets[t.e];
+  t.ntok = min(BN, cnt - t.n0);
+  t.kb0 = kblocks * t.ks / split;
+  t.kb1 = kblocks * (t.ks + 1) / split;
+  return t;
+}
+
+template <bool UP, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+ffn_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_act,
+              const Params p) {
+  constexpr int A_BYTES = BM * BK * 2;          // 16 KB weight tile
+  constexpr int B_BYTES = BN * BK * 2;          // 8 KB activation tile
+  constexpr int NA = UP ? 2 : 1;                // W1 + W3 tiles in the up phase
+  constexpr int STAGE_BYTES = NA * A_BYTES + B_BYTES;
+  constexpr int ACC_COLS = UP ? 2 * BN : BN;    // g | u, or y
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the 128B-swizzle atoms
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ TileList tl;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = UP ? p.H : p.F;
+  const int R = UP ? p.F : p.H;
+  const int kblocks = K / BK;
+  const int mtiles = R / BM;
+  const int split = UP ? 1 : p.split;
+
+  build_tiles(p, mtiles, split, &tl);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+  const int ntiles = tl.start[tl.n_active];
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const Tile t = decode(p, tl, tile, mtiles, split, kblocks);
+        const int slot = p.slot[t.e];
+        const int arow = p.offsets[t.e] + t.n0;
+        for (int kb = t.kb0; kb < t.kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* st = smem + stage * STAGE_BYTES;
+          mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
+          tma_load_3d(st, &map_w, &full_bar[stage], kb * BK, t.m0, slot);
+          if (UP) tma_load_3d(st + A_BYTES, &map_w, &full_bar[stage], kb * BK, p.F + t.m0, slot);
+          tma_load_2d(st + NA * A_BYTES, &map_act, &full_bar[stage], kb * BK, arow);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (single thread)
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const Tile t = decode(p, tl, tile, mtiles, split, kblocks);
+        const int n = ((t.ntok + 15) / 16) * 16;
+        const uint32_t idesc = instr_desc(n);
+        mbar_wait(&tempty_bar[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * ACC_COLS;
+        for (int kb = t.kb0; kb < t.kb1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          uint8_t* st = smem + stage * STAGE_BYTES;
+          const uint64_t a0 = smem_desc_sw128(st);
+          const uint64_t a1 = smem_desc_sw128(st + A_BYTES);
+          const uint64_t b0 = smem_desc_sw128(st + NA * A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint32_t accum = (kb > t.kb0 || k > 0) ? 1u : 0u;
+            // +32 bytes per K=16 step inside the swizzle atom (desc units of 16 B)
+            umma(d, a0 + 2 * k, b0 + 2 * k, idesc, accum);
+            if (UP) umma(d + BN, a1 + 2 * k, b0 + 2 * k, idesc, accum);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull_bar[acc]);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2..5, TMEM lane quarter = warp % 4
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const Tile t = decode(p, tl, tile, mtiles, split, kblocks);
+      mbar_wait(&tfull_bar[acc], aphase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + acc * ACC_COLS;
+      const int row = t.m0 + 32 * q + lane;
+      const int64_t prow = p.offsets[t.e] + t.n0;
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        if (c0 < t.ntok) {  // warp-uniform
+          float g[16], u[16];
+          tmem_ld16(taddr + c0, g);
+          if (UP) tmem_ld16(taddr + BN + c0, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            if (c0 + c < t.ntok) {
+              if (UP) {
+                p.h_out[(prow + c0 + c) * p.F + row] = f32_to_bf16(__fmul_rn(det_silu(g[c]), u[c]));
+              } else {
+                p.y_part[((int64_t)t.ks * p.rows + prow + c0 + c) * p.H + row] = g[c];
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+  }
+}
+
+// y[r, :] = sum_s y_part[s][r, :] in split order (deterministic), only for
+// rows of experts in this launch's mask (other rows keep their values).
+__global__ void reduce_split_kernel(const float* __restrict__ part, int split, int rows, int H,
+                                    const int32_t* __restrict__ offsets, int E, uint64_t mask,
+                                    float* __restrict__ y) {
+  const int64_t n = (int64_t)rows * H;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / H);
+    int e = 0;
+    while (e < E - 1 && r >= offsets[e + 1]) ++e;
+    if (!((mask >> e) & 1ull)) continue;
+    float s = part[i];
+    for (int k = 1; k < split; ++k) s = __fadd_rn(s, part[(int64_t)k * n + i]);
+    y[i] = s;
+  }
+}
+
+// x_perm[r] = x[perm[r]] (activation rows grouped by expert for TMA).
+__global__ void gather_rows_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ perm,
+                                   const int32_t* __restrict__ offsets, int E, int H, uint16_t* __restrict__ out) {
+  const int rows = offsets[E];
+  const int nch = H >> 3;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)rows * nch;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / nch), c = (int)(i - (int64_t)r * nch);
+    reinterpret_cast<uint4*>(out + (int64_t)r * H)[c] =
+        reinterpret_cast<const uint4*>(x + (int64_t)perm[r] * H)[c];
+  }
+}
+
+// -------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)ptr;
+  }
+  return fn;
+}
+
+// bf16 tensor map, 128B swizzle, box = {64, box_rows, 1}; dims/strides in
+// elements / bytes, innermost first.
+bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+              uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t d[3], s[2];
+  cuuint32_t box[3] = {(cuuint32_t)BK, box_rows, 1}, es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) d[i] = dims[i];
+  for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)rank, const_cast<void*>(base), d, s, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <bool UP, int STAGES>
+int launch(const CUtensorMap& mw, const CUtensorMap& ma, const Params& p, int nsms, cudaStream_t s) {
+  constexpr int NA = UP ? 2 : 1;
+  constexpr int STAGE_BYTES = NA * BM * BK * 2 + BN * BK * 2;
+  const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(ffn_tc_kernel<UP, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  ffn_tc_kernel<UP, STAGES><<<nsms, kThreads, smem, s>>>(mw, ma, p);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace tc
+
+extern "C" int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, const int32_t* slot_of_expert,
+                                   uint64_t expert_mask, const uint16_t* x, int T, int H, int F, int E, int k,
+                                   const int32_t* expert_offsets, const int32_t* perm_token, uint16_t* x_perm,
+                                   uint16_t* h_scratch, float* y, float* y_split, int split_k, void* stream) {
+  using namespace tc;
+  if (!pool || !slot_of_expert || !expert_offsets || T < 0 || E < 1 || E > kMaxExperts || k < 1)
+    return (int)cudaErrorInvalidValue;
+  if (H % BM || F % BM || H % BK || F % BK || split_k < 1) return (int)cudaErrorInvalidValue;
+  if (T == 0 || expert_mask == 0) return 0;
+  if (!x || !perm_token || !x_perm || !h_scratch || !y || (split_k > 1 && !y_split))
+    return (int)cudaErrorInvalidValue;
+  cudaStream_t s = (cudaStream_t)stream;
+  int dev = 0, nsms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsms, cudaDevAttrMultiProcessorCount, dev);
+  const int rows = T * k;
+  Params p{};
+  p.mask = expert_mask;
+  p.offsets = expert_offsets;
+  p.h_out = h_scratch;
+  p.y_part = split_k > 1 ? y_split : y;
+  p.E = E;
+  p.H = H;
+  p.F = F;
+  p.rows = rows;
+  p.split = split_k;
+  int max_slot = 0;
+  for (int e = 0; e < E; ++e) {
+    p.slot[e] = ((expert_mask >> e) & 1ull) ? slot_of_expert[e] : 0;
+    if (p.slot[e] > max_slot) max_slot = p.slot[e];
+  }
+  gather_rows_kernel<<<nsms, 256, 0, s>>>(x, perm_token, expert_offsets, E, H, x_perm);
+  int st = (int)cudaGetLastError();
+  if (st) return st;
+  CUtensorMap mw_up, ma_up, mw_dn, ma_dn;
+  const uint64_t sb = (uint64_t)slot_elems * 2;
+  {
+    const uint64_t d[3] = {(uint64_t)H, (uint64_t)2 * F, (uint64_t)max_slot + 1};
+    const uint64_t str[2] = {(uint64_t)H * 2, sb};
+    if (!make_map(&mw_up, pool, 3, d, str, BM)) return (int)cudaErrorInvalidValue;
+    const uint64_t da[2] = {(uint64_t)H, (uint64_t)rows};
+    const uint64_t sa[1] = {(uint64_t)H * 2};
+    if (!make_map(&ma_up, x_perm, 2, da, sa, BN)) return (int)cudaErrorInvalidValue;
+  }
+  {
+    const uint64_t d[3] = {(uint64_t)F, (uint64_t)H, (uint64_t)max_slot + 1};
+    const uint64_t str[2] = {(uint64_t)F * 2, sb};
+    if (!make_map(&mw_dn, pool + (int64_t)2 * F * H, 3, d, str, BM)) return (int)cudaErrorInvalidValue;
+    const uint64_t da[2] = {(uint64_t)F, (uint64_t)rows};
+    const uint64_t sa[1] = {(uint64_t)F * 2};
+    if (!make_map(&ma_dn, h_scratch, 2, da, sa, BN)) return (int)cudaErrorInvalidValue;
+  }
+  st = launch<true, 5>(mw_up, ma_up, p, nsms, s);
+  if (st) return st;
+  st = launch<false, 8>(mw_dn, ma_dn, p, nsms, s);
+  if (st) return st;
+  if (split_k > 1) {
+    reduce_split_kernel<<<nsms * 4, 256, 0, s>>>(y_split, split_k, rows, H, expert_offsets, E, expert_mask, y);
+    st = (int)cudaGetLastError();
+  }
+  return st;
+}

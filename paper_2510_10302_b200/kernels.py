@@ -209,6 +209,61 @@ def expert_ffn(
         )
 
 
+def tc_split(ffn_dim: int) -> int:
+    """Down-phase split-K used by the tcgen05 path (K blocks of 64)."""
+    kb = ffn_dim // 64
+    for s in (8, 4, 2):
+        if kb >= 4 * s:
+            return s
+    return 1
+
+
+def expert_ffn_tc(
+    pool: torch.Tensor,
+    slot_of_expert: Sequence[int],
+    expert_mask: int,
+    x: torch.Tensor,
+    ffn_dim: int,
+    top_k: int,
+    offsets: torch.Tensor,
+    perm: torch.Tensor,
+    x_perm: torch.Tensor,
+    h_scratch: torch.Tensor,
+    y: torch.Tensor,
+    y_split: torch.Tensor | None,
+    split_k: int | None = None,
+    stream=None,
+) -> None:
+    """tcgen05/TMEM/TMA grouped SwiGLU (same outputs as :func:`expert_ffn`)."""
+    _need(pool, BF16, "pool", 2)
+    _need(x, BF16, "x", 2)
+    T, H = x.shape
+    E = len(slot_of_expert)
+    split = tc_split(ffn_dim) if split_k is None else split_k
+    LAUNCHES["count"] += 3 + (1 if split > 1 else 0)
+    _native.call(
+        "spmoe_expert_ffn_tc",
+        pool.data_ptr(),
+        pool.shape[1],
+        _slot_array(slot_of_expert, E),
+        expert_mask,
+        x.data_ptr(),
+        T,
+        H,
+        ffn_dim,
+        E,
+        top_k,
+        offsets.data_ptr(),
+        perm.data_ptr(),
+        x_perm.data_ptr(),
+        h_scratch.data_ptr(),
+        y.data_ptr(),
+        _ptr(y_split),
+        split,
+        _stream(stream),
+    )
+
+
 # ---------------------------------------------------------------------------
 # K4
 # ---------------------------------------------------------------------------

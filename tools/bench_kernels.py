@@ -53,13 +53,20 @@ def run_case(name, H, F, E, k, T, iters=20, warmup=5):
     mask = (1 << E) - 1
     st = torch.cuda.current_stream()
 
+    xp = torch.empty((T * k, H), dtype=torch.bfloat16, device=dev)
+    split = K.tc_split(F)
+    ys = torch.empty((split, T * k, H), dtype=torch.float32, device=dev)
+
     def once(i, phase="both"):
+        if phase == "tc":
+            K.expert_ffn_tc(pools[i % R], slots, mask, x, F, k, off, perm, xp, h, y, ys, split)
+            return
         K.expert_ffn(pools[i % R], slots, mask, x, F, k, off, perm, h, y, maxtok, phase=phase)
 
     for i in range(warmup):
         once(i)
     res = {}
-    for phase in ("both", "up", "down"):
+    for phase in ("both", "up", "down", "tc"):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
         torch.cuda.synchronize()
         for i in range(iters):
@@ -68,7 +75,7 @@ def run_case(name, H, F, E, k, T, iters=20, warmup=5):
             evs[i][1].record(st)
         torch.cuda.synchronize()
         ms = float(np.median([a.elapsed_time(b) for a, b in evs]))
-        wbytes = {"both": 3, "up": 2, "down": 1}[phase] * F * H * 2 * U
+        wbytes = {"both": 3, "up": 2, "down": 1, "tc": 3}[phase] * F * H * 2 * U
         act = T * k * (H * 2 + F * 2 * 2 + H * 4)
         res[phase] = {"ms": ms, "GBps": (wbytes + act) / (ms / 1e3) / 1e9, "weight_bytes": wbytes}
     # router latency
