@@ -89,6 +89,15 @@ class _Scratch:
         self.y = torch.empty((T * k, H), dtype=f32, device=device)
         self.hd = torch.empty((T, max(arch.d_ffn, arch.shared_ffn)), dtype=bf, device=device)
         self.yd = torch.empty((T, H), dtype=f32, device=device)
+        # tcgen05 path workspaces: gathered routed rows, split-K partials
+        kmax = max(k, 1)
+        self.xp = torch.empty((T * kmax, H), dtype=bf, device=device)
+        fmax = max(arch.ffn, arch.d_ffn, arch.shared_ffn)
+        from .kernels import tc_split
+
+        smax = max(tc_split(f) for f in (arch.ffn, arch.d_ffn, arch.shared_ffn or arch.ffn))
+        self.ysplit = torch.empty((smax * T * kmax * H,), dtype=f32, device=device)
+        del fmax
         self.pw = torch.empty((T, 64), dtype=f32, device=device)
         self.pidx = torch.empty((T, 64), dtype=i32, device=device)
         self._dense: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
@@ -123,7 +132,11 @@ class SpecMoEEngine:
         record: bool = False,
         capture_layers: tuple[int, ...] = (),
         cuda_graphs: bool = True,
+        ffn_impl: str = "auto",
     ):
+        if ffn_impl not in ("auto", "tcgen05", "cuda_core"):
+            raise ValueError("ffn_impl must be auto | tcgen05 | cuda_core")
+        self.ffn_impl = ffn_impl
         if not torch.cuda.is_available():
             raise RuntimeError("SpecMoEEngine needs a CUDA device (there is no CPU fallback)")
         self.arch = arch
@@ -238,10 +251,26 @@ class SpecMoEEngine:
                 self.decisions.append(("task", layer, ids))
         self._pushed = []
 
+    def _use_tc(self, F: int, maxtok: int) -> bool:
+        """tcgen05 path unless pinned to the CUDA-core (bit-exact) path; the
+        CUDA-core kernel wins only when every expert sees a single token."""
+        if self.ffn_impl == "cuda_core" or self.arch.hidden % 128 or F % 128:
+            return False
+        return self.ffn_impl == "tcgen05" or maxtok > 1
+
+    def _ffn(self, pool, slots, mask, xn, F, k, offsets, perm, h, y, maxtok, s: _Scratch) -> None:
+        if self._use_tc(F, maxtok):
+            rows = xn.shape[0] * k
+            split = K.tc_split(F)
+            K.expert_ffn_tc(pool, slots, mask, xn, F, k, offsets, perm, s.xp[:rows], h, y,
+                            s.ysplit[: split * rows].view(split, rows, -1), split)
+        else:
+            K.expert_ffn(pool, slots, mask, xn, F, k, offsets, perm, h, y, maxtok)
+
     def _dense_ffn(self, blob: torch.Tensor, F: int, xn: torch.Tensor, resid: torch.Tensor, s: _Scratch, out=None):
         T = xn.shape[0]
         off, perm = s.dense(T)
-        K.expert_ffn(blob, [0], 1, xn, F, 1, off, perm, s.hd, s.yd, max_tokens_per_expert=T)
+        self._ffn(blob, [0], 1, xn, F, 1, off, perm, s.hd, s.yd, T, s)
         return K.moe_combine(s.yd, perm, None, T, self.arch.hidden, 1, residual=resid, out=out)
 
     def _timed_ffn(self, experts, counts, slots, mask, xn, offsets, perm, s, maxtok) -> None:
@@ -250,11 +279,11 @@ class SpecMoEEngine:
         expert in the mask read once + activations in/out) for the roofline."""
         a = self.arch
         if not self.time_k3:
-            K.expert_ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok)
+            self._ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok, s)
             return
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ea.record()
-        K.expert_ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok)
+        self._ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok, s)
         eb.record()
         rows = int(sum(int(counts[e]) for e in experts))
         act = rows * (a.hidden * 2 + 2 * a.ffn * 2 + a.hidden * 4)  # x in, h out+in, y out
@@ -343,7 +372,7 @@ class SpecMoEEngine:
         ys = None
         if lw.shared is not None:
             off, pm = s.dense(T)
-            K.expert_ffn(lw.shared, [0], 1, xn, a.shared_ffn, 1, off, pm, s.hd, s.yd, T)
+            self._ffn(lw.shared, [0], 1, xn, a.shared_ffn, 1, off, pm, s.hd, s.yd, T, s)
             ys = s.yd
         if l in self.capture_layers:
             cap = {"layer": l, "xn": xn.clone(), "resid": resid.clone(), "idx": idx.clone(), "w": w.clone(),

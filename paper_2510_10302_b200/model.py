@@ -292,6 +292,8 @@ def build_weights(
     lm_head = _fill(torch.empty((arch.vocab, H), dtype=bf, device=device), tensor_seed(seed, K_LMHEAD), std)
     layers = []
     stage = torch.empty((min(chunk_experts, E), arch.expert_elems), dtype=bf, device=device)
+    base_cache: dict[int, torch.Tensor] = {}
+    written: set[int] = set()
     for l in range(arch.num_layers):
         wqkv = _fill(torch.empty((arch.qkv_dim, H), dtype=bf, device=device), tensor_seed(seed, K_QKV, l), std)
         wo = _fill(
@@ -301,25 +303,33 @@ def build_weights(
         )
         router = _fill(torch.empty((E, H), dtype=bf, device=device), tensor_seed(seed, K_ROUTER, l), 1.0 / math.sqrt(H))
         acc = torch.zeros((arch.expert_elems,), dtype=torch.float32, device=device)
-        base = None
-        if arch.expert_spread is not None:
-            base = torch.empty((arch.expert_elems,), dtype=bf, device=device)
-            fill_blob_generic(base, F, H, tensor_seed(seed, K_BASE, l), std, arch.expert_out_scale * arch.res_scale)
         for e0 in range(0, E, stage.shape[0]):
             n = min(stage.shape[0], E - e0)
+            rows = []
             for j in range(n):
                 row = host_pool.row_of(l, e0 + j) if host_pool is not None else l * E + e0 + j
+                rows.append(row)
+                # expert content is a pure function of its host-pool row, so an
+                # aliased row means the same weights for every layer using it
                 fill_expert_blob(stage[j], arch, seed, row)
-                if base is not None:
-                    # upcycled experts: a shared per-layer component plus a
+                if arch.expert_spread is not None:
+                    # upcycled experts: the home layer's shared component plus a
                     # per-expert deviation of relative size expert_spread
+                    base = base_cache.get(row // E)
+                    if base is None:
+                        base = torch.empty((arch.expert_elems,), dtype=bf, device=device)
+                        fill_blob_generic(base, F, H, tensor_seed(seed, K_BASE, row // E), std,
+                                          arch.expert_out_scale * arch.res_scale)
+                        base_cache = {row // E: base}
                     stage[j].copy_((base.float() + stage[j].float() * arch.expert_spread).to(bf))
                 acc += stage[j].float()
             if host_pool is not None:
-                for j in range(n):
-                    host_pool.blob(l, e0 + j).copy_(stage[j], non_blocking=False)
+                for j, row in enumerate(rows):
+                    if row not in written:
+                        host_pool.tensor[row].copy_(stage[j], non_blocking=False)
+                        written.add(row)
         mean = (acc / E).to(bf)
-        del acc, base
+        del acc
         if arch.d_ffn != F:
             draft = torch.empty((1, 3 * arch.d_ffn * H), dtype=bf, device=device)
             fill_blob_generic(draft[0], arch.d_ffn, H, tensor_seed(seed, K_EXPERT, l, 10_000), std, arch.expert_out_scale * arch.res_scale)
