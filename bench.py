@@ -241,6 +241,7 @@ def main():
     ap.add_argument("--policy", default="draft_prefetch")
     ap.add_argument("--cutoff", type=int, default=None, help="explicit cutoff layer (default: solver)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ffn-impl", default="auto", choices=["auto", "tcgen05", "cuda_core"])
     ap.add_argument("--write-calibration", action="store_true")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
@@ -284,8 +285,12 @@ def main():
                         draft_length=cfg["N"], acceptance_rate=1.0, seed=1234, cutoff_layer=args.cutoff,
                         cache_capacity_experts=capacity)
     t_setup = time.perf_counter()
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    # replicas on one box share ONE pinned host expert pool through /dev/shm
+    share = f"{arch.name}_s1234_{os.environ.get('MASTER_PORT', '0')}" if local_world > 1 else None
     eng = SpecMoEEngine(arch, hw, timings, policy, batch=cfg["batch"], max_tokens=cfg["prompt"] + 64 * (cfg["N"] + 1),
-                        window_tokens=cfg["N"])
+                        window_tokens=cfg["N"], host_share=share, host_leader=(local == 0),
+                        ffn_impl=args.ffn_impl)
     g = torch.Generator().manual_seed(1000 + rank)
     prompts = torch.randint(0, arch.vocab, (cfg["batch"], cfg["prompt"]), generator=g)
     eng.prefill(prompts)

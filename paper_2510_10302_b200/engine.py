@@ -125,6 +125,9 @@ class SpecMoEEngine:
         seed: int | None = None,
         device=None,
         host_distinct: int | None = None,
+        host_share: str | None = None,
+        host_leader: bool = True,
+        model_state: tuple | None = None,
         draft_perturb: float = 0.0,
         window_tokens: int = 1,
         max_tokens: int = 1024,
@@ -153,8 +156,15 @@ class SpecMoEEngine:
             )
         self.capacity = min(self.capacity, arch.num_layers * arch.num_experts)
         torch.cuda.set_device(self.device)
-        self.host_pool = HostExpertPool(arch, host_distinct)
-        self.weights = build_weights(arch, self.seed, self.device, self.host_pool, draft_perturb=draft_perturb)
+        if model_state is not None:
+            # reuse another engine's pinned host pool and device weights
+            # (sweeps over policy / batch / budget on one model)
+            self.host_pool, self.weights = model_state
+            self._owns_model = False
+        else:
+            self.host_pool = HostExpertPool(arch, host_distinct, share=host_share, leader=host_leader)
+            self.weights = build_weights(arch, self.seed, self.device, self.host_pool, draft_perturb=draft_perturb)
+            self._owns_model = True
         self.pool = torch.empty((self.capacity, arch.expert_elems), dtype=torch.bfloat16, device=self.device)
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self.cache = NativeExpertCache(
@@ -238,7 +248,14 @@ class SpecMoEEngine:
         finally:
             self.predictor.close()
             self.route_ring.close()
-            self.host_pool.close()
+            self._lib.spmoe_event_destroy(self._route_ev)
+            if self._owns_model:
+                self.host_pool.close()
+
+    @property
+    def model_state(self) -> tuple:
+        """(host pool, device weights) to share with another engine."""
+        return self.host_pool, self.weights
 
     # ------------------------------------------------------------- MoE layers
     def _drain(self) -> None:

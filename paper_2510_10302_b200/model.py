@@ -67,12 +67,12 @@ class ArchSpec:
     # deviation, so the draft's mean-expert FFN tracks the routed mixture and
     # random-init SD accepts drafts at a realistic rate (SURVEY.md §7 hard
     # part 2).  Bytes moved and FLOPs are unchanged.
-    expert_spread: float | None = 0.25
+    expert_spread: float | None = 0.04
     # init scales: token embedding std, and GPT-2-style residual-branch
     # scaling of the output projections (W_o, W2): std * residual_scale,
     # None -> 1/sqrt(2 * num_layers).  Keeps the 32-layer random network out
     # of the chaotic regime so a slightly different draft still agrees.
-    embed_std: float = 0.02
+    embed_std: float = 1.0
     residual_scale: float | None = None
 
     @property
@@ -207,7 +207,11 @@ class HostExpertPool:
     mapped) through the native library.
     """
 
-    def __init__(self, arch: ArchSpec, distinct: int | None = None):
+    def __init__(self, arch: ArchSpec, distinct: int | None = None, share: str | None = None,
+                 leader: bool = True):
+        """``share`` = name of a /dev/shm pool shared by the per-GPU processes
+        of one box (replica mode): the local leader creates and fills it
+        (``writable``), followers attach once the leader publishes it."""
         from . import _native
 
         self.arch = arch
@@ -217,16 +221,30 @@ class HostExpertPool:
         self.slot_bytes = arch.expert_bytes
         self.nbytes = self.rows * self.slot_bytes
         self._lib = _native.load()
-        host = C.c_void_p()
-        dev = C.c_void_p()
-        _native.check(
-            "spmoe_host_alloc_mapped",
-            self._lib.spmoe_host_alloc_mapped(self.nbytes, C.byref(host), C.byref(dev)),
-        )
-        self.ptr = host.value
-        buf = (C.c_uint16 * (self.rows * arch.expert_elems)).from_address(self.ptr)
-        self.array = np.ctypeslib.as_array(buf).reshape(self.rows, arch.expert_elems)
+        self._shared = None
+        self.writable = leader
+        if share:
+            from .replicas import SharedHostPool
+
+            self._shared = SharedHostPool(share, self.rows, arch.expert_elems, leader=leader, publish=False)
+            self.ptr = self._shared.ptr
+            self.array = self._shared.array
+        else:
+            host = C.c_void_p()
+            dev = C.c_void_p()
+            _native.check(
+                "spmoe_host_alloc_mapped",
+                self._lib.spmoe_host_alloc_mapped(self.nbytes, C.byref(host), C.byref(dev)),
+            )
+            self.ptr = host.value
+            buf = (C.c_uint16 * (self.rows * arch.expert_elems)).from_address(self.ptr)
+            self.array = np.ctypeslib.as_array(buf).reshape(self.rows, arch.expert_elems)
         self.tensor = torch.from_numpy(self.array.view(np.int16)).view(torch.bfloat16)
+
+    def publish(self) -> None:
+        """Leader: mark a shared pool complete (followers unblock)."""
+        if self._shared is not None and self.writable:
+            self._shared.publish()
 
     def row_of(self, layer: int, expert: int) -> int:
         return self.index[layer * self.arch.num_experts + expert]
@@ -238,7 +256,10 @@ class HostExpertPool:
         if getattr(self, "ptr", None):
             self.tensor = None
             self.array = None
-            self._lib.spmoe_host_free(C.c_void_p(self.ptr))
+            if self._shared is not None:
+                self._shared.close(unlink=self.writable)
+            else:
+                self._lib.spmoe_host_free(C.c_void_p(self.ptr))
             self.ptr = None
 
 
@@ -323,7 +344,7 @@ def build_weights(
                         base_cache = {row // E: base}
                     stage[j].copy_((base.float() + stage[j].float() * arch.expert_spread).to(bf))
                 acc += stage[j].float()
-            if host_pool is not None:
+            if host_pool is not None and host_pool.writable:
                 for j, row in enumerate(rows):
                     if row not in written:
                         host_pool.tensor[row].copy_(stage[j], non_blocking=False)
@@ -359,6 +380,9 @@ def build_weights(
             )
         )
     del stage
+    if host_pool is not None:
+        torch.cuda.synchronize(device)
+        host_pool.publish()
     cos, sin = rope_tables(arch, device)
     return ModelWeights(
         arch=arch,

@@ -57,7 +57,7 @@ class SharedHostPool:
     """
 
     def __init__(self, name: str, rows: int, row_elems: int, leader: bool, fill=None, timeout_s: float = 1800.0,
-                 register: bool = True, root: str = "/dev/shm"):
+                 register: bool = True, root: str = "/dev/shm", publish: bool = True):
         self.path = Path(root) / f"spmoe_{name}.pool"
         self.ready = Path(root) / f"spmoe_{name}.ready"
         self.nbytes = rows * row_elems * 2
@@ -81,17 +81,23 @@ class SharedHostPool:
         self.array = np.frombuffer(self._mm, dtype=np.uint16).reshape(rows, row_elems)
         self.ptr = self.array.ctypes.data
         self._registered = False
+        self.leader = leader
         if leader:
             if fill is not None:
                 fill(self.array)
-            self._mm.flush()
-            self.ready.write_text(str(os.getpid()))
+            if publish:
+                self.publish()
         if register:
             from . import _native
 
             lib = _native.load()
             _native.check("spmoe_host_register", lib.spmoe_host_register(self.ptr, self.nbytes))
             self._registered = True
+
+    def publish(self) -> None:
+        """Leader: the pool content is complete; unblock the followers."""
+        self._mm.flush()
+        self.ready.write_text(str(os.getpid()))
 
     def close(self, unlink: bool = False) -> None:
         if self._registered:
