@@ -133,15 +133,20 @@ int spmoe_expert_ffn_down(const uint16_t* pool, int64_t slot_elems,
  * outputs): weight rows as the UMMA M=128 operand, routed tokens as N
  * (<= 64 per tile), TMA over a 3-D tensor map of the slot pool, fp32
  * accumulators in TMEM.  Needs H % 128 == 0 and F % 128 == 0.  Workspaces:
- * x_perm [T*k, H] bf16 (routed rows gathered by perm_token), y_split
- * [split_k, T*k, H] f32 (down-phase split-K partials, reduced in fixed
- * order; unused when split_k == 1).  Results equal the CUDA-core path
- * within fp32 rounding of the tensor core's accumulation order.
+ * x_perm [T*k, H] bf16 (routed rows gathered by perm_token) and workspace
+ * f32 of max(2*split_up*T*k*F, split_dn*T*k*H) elements holding split-K
+ * partials (up: gate then up sums, reduced with SiLU; down: y partials),
+ * always reduced in split order, so results are deterministic; unused
+ * when both splits are 1.  split_up <= H/64, split_dn <= F/64: the host
+ * picks them so that (tiles x split) fills the SMs (kernels.tc_plan).
+ * Results equal the CUDA-core path within fp32 rounding of the tensor
+ * core's accumulation order.
  */
 int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, const int32_t* slot_of_expert,
                         uint64_t expert_mask, const uint16_t* x, int T, int H, int F, int E, int k,
                         const int32_t* expert_offsets, const int32_t* perm_token, uint16_t* x_perm,
-                        uint16_t* h_scratch, float* y, float* y_split, int split_k, void* stream);
+                        uint16_t* h_scratch, float* y, float* workspace, int split_up, int split_dn,
+                        void* stream);
 
 /* --------------------------------------------------------------------- */
 /* K4  moe_combine                                                        */

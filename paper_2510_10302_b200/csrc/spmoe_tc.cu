@@ -38,8 +38,9 @@ constexpr int kTmemCols = 256;
 struct Params {
   uint64_t mask;
   const int32_t* offsets;
-  uint16_t* h_out;  // up: [rows, F] bf16
-  float* y_part;    // down: [split][rows, H] fp32
+  uint16_t* h_out;  // up, split 1: [rows, F] bf16
+  float* g_part;    // up, split > 1: [split][rows, F] fp32 (gate), then up
+  float* y_part;    // down: [split][rows, H] fp32 (split 1: y itself)
   int E, H, F, rows, split;
   int slot[kMaxExperts];
 };
@@ -208,7 +209,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__
   const int R = UP ? p.F : p.H;
   const int kblocks = K / BK;
   const int mtiles = R / BM;
-  const int split = UP ? 1 : p.split;
+  const int split = p.split;
 
   build_tiles(p, mtiles, split, &tl);
   if (threadIdx.x == 0) {
@@ -311,7 +312,13 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__
           for (int c = 0; c < 16; ++c) {
             if (c0 + c < t.ntok) {
               if (UP) {
-                p.h_out[(prow + c0 + c) * p.F + row] = f32_to_bf16(__fmul_rn(det_silu(g[c]), u[c]));
+                if (split == 1) {
+                  p.h_out[(prow + c0 + c) * p.F + row] = f32_to_bf16(__fmul_rn(det_silu(g[c]), u[c]));
+                } else {
+                  const int64_t i = ((int64_t)t.ks * p.rows + prow + c0 + c) * p.F + row;
+                  p.g_part[i] = g[c];
+                  p.g_part[(int64_t)split * p.rows * p.F + i] = u[c];
+                }
               } else {
                 p.y_part[((int64_t)t.ks * p.rows + prow + c0 + c) * p.H + row] = g[c];
               }
@@ -346,6 +353,26 @@ __global__ void reduce_split_kernel(const float* __restrict__ part, int split, i
     float s = part[i];
     for (int k = 1; k < split; ++k) s = __fadd_rn(s, part[(int64_t)k * n + i]);
     y[i] = s;
+  }
+}
+
+// h[r, f] = bf16(silu(sum_s g) * sum_s u), split order, masked rows only.
+__global__ void reduce_swiglu_kernel(const float* __restrict__ part, int split, int rows, int F,
+                                     const int32_t* __restrict__ offsets, int E, uint64_t mask,
+                                     uint16_t* __restrict__ h) {
+  const int64_t n = (int64_t)rows * F;
+  const float* up = part + (int64_t)split * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / F);
+    int e = 0;
+    while (e < E - 1 && r >= offsets[e + 1]) ++e;
+    if (!((mask >> e) & 1ull)) continue;
+    float g = part[i], u = up[i];
+    for (int k = 1; k < split; ++k) {
+      g = __fadd_rn(g, part[(int64_t)k * n + i]);
+      u = __fadd_rn(u, up[(int64_t)k * n + i]);
+    }
+    h[i] = f32_to_bf16(__fmul_rn(det_silu(g), u));
   }
 }
 
@@ -414,13 +441,15 @@ int launch(const CUtensorMap& mw, const CUtensorMap& ma, const Params& p, int ns
 extern "C" int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, const int32_t* slot_of_expert,
                                    uint64_t expert_mask, const uint16_t* x, int T, int H, int F, int E, int k,
                                    const int32_t* expert_offsets, const int32_t* perm_token, uint16_t* x_perm,
-                                   uint16_t* h_scratch, float* y, float* y_split, int split_k, void* stream) {
+                                   uint16_t* h_scratch, float* y, float* workspace, int split_up, int split_dn,
+                                   void* stream) {
   using namespace tc;
   if (!pool || !slot_of_expert || !expert_offsets || T < 0 || E < 1 || E > kMaxExperts || k < 1)
     return (int)cudaErrorInvalidValue;
-  if (H % BM || F % BM || H % BK || F % BK || split_k < 1) return (int)cudaErrorInvalidValue;
+  if (H % BM || F % BM || H % BK || F % BK || split_up < 1 || split_dn < 1) return (int)cudaErrorInvalidValue;
+  if (split_up > H / BK || split_dn > F / BK) return (int)cudaErrorInvalidValue;
   if (T == 0 || expert_mask == 0) return 0;
-  if (!x || !perm_token || !x_perm || !h_scratch || !y || (split_k > 1 && !y_split))
+  if (!x || !perm_token || !x_perm || !h_scratch || !y || ((split_up > 1 || split_dn > 1) && !workspace))
     return (int)cudaErrorInvalidValue;
   cudaStream_t s = (cudaStream_t)stream;
   int dev = 0, nsms = 148;
@@ -431,12 +460,11 @@ extern "C" int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, con
   p.mask = expert_mask;
   p.offsets = expert_offsets;
   p.h_out = h_scratch;
-  p.y_part = split_k > 1 ? y_split : y;
+  p.g_part = workspace;
   p.E = E;
   p.H = H;
   p.F = F;
   p.rows = rows;
-  p.split = split_k;
   int max_slot = 0;
   for (int e = 0; e < E; ++e) {
     p.slot[e] = ((expert_mask >> e) & 1ull) ? slot_of_expert[e] : 0;
@@ -463,12 +491,21 @@ extern "C" int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, con
     const uint64_t sa[1] = {(uint64_t)F * 2};
     if (!make_map(&ma_dn, h_scratch, 2, da, sa, BN)) return (int)cudaErrorInvalidValue;
   }
+  p.split = split_up;
   st = launch<true, 5>(mw_up, ma_up, p, nsms, s);
   if (st) return st;
+  if (split_up > 1) {
+    reduce_swiglu_kernel<<<nsms * 4, 256, 0, s>>>(workspace, split_up, rows, F, expert_offsets, E, expert_mask,
+                                                   h_scratch);
+    st = (int)cudaGetLastError();
+    if (st) return st;
+  }
+  p.split = split_dn;
+  p.y_part = split_dn > 1 ? workspace : y;
   st = launch<false, 8>(mw_dn, ma_dn, p, nsms, s);
   if (st) return st;
-  if (split_k > 1) {
-    reduce_split_kernel<<<nsms * 4, 256, 0, s>>>(y_split, split_k, rows, H, expert_offsets, E, expert_mask, y);
+  if (split_dn > 1) {
+    reduce_split_kernel<<<nsms * 4, 256, 0, s>>>(workspace, split_dn, rows, H, expert_offsets, E, expert_mask, y);
     st = (int)cudaGetLastError();
   }
   return st;

@@ -92,12 +92,12 @@ class _Scratch:
         # tcgen05 path workspaces: gathered routed rows, split-K partials
         kmax = max(k, 1)
         self.xp = torch.empty((T * kmax, H), dtype=bf, device=device)
-        fmax = max(arch.ffn, arch.d_ffn, arch.shared_ffn)
-        from .kernels import tc_split
+        from .kernels import tc_split, tc_workspace_floats
 
-        smax = max(tc_split(f) for f in (arch.ffn, arch.d_ffn, arch.shared_ffn or arch.ffn))
-        self.ysplit = torch.empty((smax * T * kmax * H,), dtype=f32, device=device)
-        del fmax
+        need = 1
+        for f in (arch.ffn, arch.d_ffn, arch.shared_ffn or arch.ffn):
+            need = max(need, tc_workspace_floats(T * kmax, H, f, tc_split(H), tc_split(f)))
+        self.ysplit = torch.empty((need,), dtype=f32, device=device)
         self.pw = torch.empty((T, 64), dtype=f32, device=device)
         self.pidx = torch.empty((T, 64), dtype=i32, device=device)
         self._dense: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
@@ -140,6 +140,7 @@ class SpecMoEEngine:
         if ffn_impl not in ("auto", "tcgen05", "cuda_core"):
             raise ValueError("ffn_impl must be auto | tcgen05 | cuda_core")
         self.ffn_impl = ffn_impl
+        self.num_sms = torch.cuda.get_device_properties(device if device is not None else 0).multi_processor_count
         if not torch.cuda.is_available():
             raise RuntimeError("SpecMoEEngine needs a CUDA device (there is no CPU fallback)")
         self.arch = arch
@@ -275,12 +276,13 @@ class SpecMoEEngine:
             return False
         return self.ffn_impl == "tcgen05" or maxtok > 1
 
-    def _ffn(self, pool, slots, mask, xn, F, k, offsets, perm, h, y, maxtok, s: _Scratch) -> None:
+    def _ffn(self, pool, slots, mask, xn, F, k, offsets, perm, h, y, maxtok, s: _Scratch, counts=None) -> None:
+        """K3 for the experts in ``mask``; ``counts`` = routed tokens of each
+        of those experts (host-known), used to plan the tcgen05 split-K."""
         if self._use_tc(F, maxtok):
             rows = xn.shape[0] * k
-            split = K.tc_split(F)
-            K.expert_ffn_tc(pool, slots, mask, xn, F, k, offsets, perm, s.xp[:rows], h, y,
-                            s.ysplit[: split * rows].view(split, rows, -1), split)
+            su, sd = K.tc_plan(counts if counts is not None else [maxtok], self.arch.hidden, F, self.num_sms)
+            K.expert_ffn_tc(pool, slots, mask, xn, F, k, offsets, perm, s.xp[:rows], h, y, s.ysplit, su, sd)
         else:
             K.expert_ffn(pool, slots, mask, xn, F, k, offsets, perm, h, y, maxtok)
 
@@ -295,12 +297,13 @@ class SpecMoEEngine:
         with CUDA events and books its algorithmic bytes (weights of every
         expert in the mask read once + activations in/out) for the roofline."""
         a = self.arch
+        cnt = [int(counts[e]) for e in experts]
         if not self.time_k3:
-            self._ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok, s)
+            self._ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok, s, cnt)
             return
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ea.record()
-        self._ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok, s)
+        self._ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok, s, cnt)
         eb.record()
         rows = int(sum(int(counts[e]) for e in experts))
         act = rows * (a.hidden * 2 + 2 * a.ffn * 2 + a.hidden * 4)  # x in, h out+in, y out

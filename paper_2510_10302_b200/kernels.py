@@ -210,12 +210,41 @@ def expert_ffn(
 
 
 def tc_split(ffn_dim: int) -> int:
-    """Down-phase split-K used by the tcgen05 path (K blocks of 64)."""
+    """Upper bound of the split-K factor for a reduction of ``ffn_dim``
+    (sizes the workspace): at most 16, at least 4 K-blocks of 64 per split."""
     kb = ffn_dim // 64
-    for s in (8, 4, 2):
-        if kb >= 4 * s:
-            return s
-    return 1
+    return max(1, min(16, kb // 4))
+
+
+def _best_split(tiles: int, kblocks: int, sms: int) -> int:
+    """Smallest split whose (tiles x split) fills the SMs to >= 95 %, else the
+    best fill found (fixed-order partial reduction keeps it deterministic)."""
+    best_s, best_eff = 1, 0.0
+    for s in range(1, min(16, max(1, kblocks // 4)) + 1):
+        n = tiles * s
+        eff = n / (sms * -(-n // sms))
+        if eff > best_eff + 1e-9:
+            best_s, best_eff = s, eff
+        if eff >= 0.95:
+            break
+    return best_s
+
+
+def tc_plan(token_counts, hidden: int, ffn_dim: int, sms: int = 148) -> tuple[int, int]:
+    """(split_up, split_dn) for the tcgen05 K3 launch of experts with the
+    given routed-token counts: the number of (expert, 64-token chunk, 128-row)
+    tiles of each phase times the split should be a near multiple of the SM
+    count."""
+    chunks = sum((int(c) + 63) // 64 for c in token_counts if c > 0)
+    if chunks == 0:
+        return 1, 1
+    up = _best_split(chunks * (ffn_dim // 128), hidden // 64, sms)
+    dn = _best_split(chunks * (hidden // 128), ffn_dim // 64, sms)
+    return up, dn
+
+
+def tc_workspace_floats(rows: int, hidden: int, ffn_dim: int, split_up: int, split_dn: int) -> int:
+    return max(2 * split_up * rows * ffn_dim if split_up > 1 else 0, split_dn * rows * hidden if split_dn > 1 else 0)
 
 
 def expert_ffn_tc(
@@ -230,17 +259,23 @@ def expert_ffn_tc(
     x_perm: torch.Tensor,
     h_scratch: torch.Tensor,
     y: torch.Tensor,
-    y_split: torch.Tensor | None,
-    split_k: int | None = None,
+    workspace: torch.Tensor | None,
+    split_up: int = 1,
+    split_dn: int = 1,
     stream=None,
 ) -> None:
-    """tcgen05/TMEM/TMA grouped SwiGLU (same outputs as :func:`expert_ffn`)."""
+    """tcgen05/TMEM/TMA grouped SwiGLU (same outputs as :func:`expert_ffn`);
+    ``workspace`` f32 of :func:`tc_workspace_floats` elements holds the
+    split-K partials (see :func:`tc_plan`)."""
     _need(pool, BF16, "pool", 2)
     _need(x, BF16, "x", 2)
     T, H = x.shape
     E = len(slot_of_expert)
-    split = tc_split(ffn_dim) if split_k is None else split_k
-    LAUNCHES["count"] += 3 + (1 if split > 1 else 0)
+    if split_up > 1 or split_dn > 1:
+        need = tc_workspace_floats(T * top_k, H, ffn_dim, split_up, split_dn)
+        if workspace is None or workspace.numel() < need:
+            raise ValueError(f"tcgen05 workspace needs {need} floats")
+    LAUNCHES["count"] += 3 + (split_up > 1) + (split_dn > 1)
     _native.call(
         "spmoe_expert_ffn_tc",
         pool.data_ptr(),
@@ -258,8 +293,9 @@ def expert_ffn_tc(
         x_perm.data_ptr(),
         h_scratch.data_ptr(),
         y.data_ptr(),
-        _ptr(y_split),
-        split,
+        _ptr(workspace),
+        split_up,
+        split_dn,
         _stream(stream),
     )
 

@@ -39,10 +39,13 @@ def run_tc(oracle, T, H, F, E, k, seed, masks=None, split=None):
     xp = torch.empty((n, H), dtype=torch.bfloat16, device="cuda")
     h = torch.zeros((n, F), dtype=torch.bfloat16, device="cuda")
     y = torch.zeros((n, H), dtype=torch.float32, device="cuda")
-    s = K.tc_split(F) if split is None else split
-    ys = torch.empty((s, n, H), dtype=torch.float32, device="cuda")
+    if split is None:
+        su, sd = K.tc_plan(np.bincount(idx.ravel(), minlength=E), H, F)
+    else:
+        su, sd = split
+    ws = torch.empty((max(1, K.tc_workspace_floats(n, H, F, su, sd)),), dtype=torch.float32, device="cuda")
     for m in masks or [(1 << E) - 1]:
-        K.expert_ffn_tc(pool, slots, m, xd, F, k, off, perm, xp, h, y, ys, s)
+        K.expert_ffn_tc(pool, slots, m, xd, F, k, off, perm, xp, h, y, ws, su, sd)
     torch.cuda.synchronize()
     pool_h = bits(pool)
     o2, p2, _ = oracle.moe_permute(idx, E)
@@ -77,7 +80,17 @@ def test_tc_masks_cached_first(oracle):
 
 
 def test_tc_split_invariance(oracle):
-    """Down-phase split-K (fixed-order reduction) stays within tolerance for
-    every split."""
-    for s in (1, 2, 4):
+    """Split-K in either phase (fixed-order partial reduction, SiLU applied
+    after the up-phase reduction) stays within tolerance for every split."""
+    for s in ((1, 1), (2, 1), (1, 2), (4, 4), (2, 16)):
         check(*run_tc(oracle, 9, 256, 1024, 8, 2, seed=11, split=s))
+
+
+def test_tc_plan_fills_sms():
+    from paper_2510_10302_b200.kernels import tc_plan
+
+    # one Mixtral expert, one token: 112 up tiles / 32 down tiles alone leave SMs idle
+    su, sd = tc_plan([1], 4096, 14336)
+    assert (112 * su) / (148 * -(-112 * su // 148)) >= 0.9
+    assert (32 * sd) / (148 * -(-32 * sd // 148)) >= 0.9
+    assert tc_plan([], 4096, 14336) == (1, 1)

@@ -54,12 +54,12 @@ def run_case(name, H, F, E, k, T, iters=20, warmup=5):
     st = torch.cuda.current_stream()
 
     xp = torch.empty((T * k, H), dtype=torch.bfloat16, device=dev)
-    split = K.tc_split(F)
-    ys = torch.empty((split, T * k, H), dtype=torch.float32, device=dev)
+    su, sd = K.tc_plan(np.bincount(ids, minlength=E), H, F)
+    ws = torch.empty((max(1, K.tc_workspace_floats(T * k, H, F, su, sd)),), dtype=torch.float32, device=dev)
 
     def once(i, phase="both"):
         if phase == "tc":
-            K.expert_ffn_tc(pools[i % R], slots, mask, x, F, k, off, perm, xp, h, y, ys, split)
+            K.expert_ffn_tc(pools[i % R], slots, mask, x, F, k, off, perm, xp, h, y, ws, su, sd)
             return
         K.expert_ffn(pools[i % R], slots, mask, x, F, k, off, perm, h, y, maxtok, phase=phase)
 
