@@ -299,6 +299,13 @@ def main():
     for _ in range(args.warmup):
         eng.step()
     torch.cuda.synchronize()
+    # cutoff model recalibrated from this GPU's measured draft/verify layer
+    # times and host-link copy time
+    cutoff_analytic = eng.cutoff
+    measured = eng.recalibrate()
+    eng.step()
+    torch.cuda.synchronize()
+    log(f"[bench] measured timings {measured} -> cutoff {cutoff_analytic} -> {eng.cutoff}")
     eng._reset_run_state()
     eng.cache.reset_stats()
     eng.cache.clear_log()
@@ -376,6 +383,13 @@ def main():
         "acceptance_rate": ex.get("acceptance_rate"),
         "hit_rate": rep.hit_rate,
         "cutoff_layer": eng.cutoff,
+        "cutoff_calibration": {
+            "analytic_cutoff": cutoff_analytic,
+            "measured_timings_ms": {"t_comp_draft": measured.t_comp_draft * 1e3,
+                                    "t_comp_target": measured.t_comp_target * 1e3,
+                                    "t_io_expert": measured.t_io_expert * 1e3},
+            "window_tokens": cfg["N"],
+        },
         "latency_breakdown": rep.latency_breakdown,
         "verify_moe_hbm_gbs": roof.get("achieved_gbs"),
         "h2d_gbs": ex.get("h2d_gbs"),

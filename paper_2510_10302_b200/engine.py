@@ -100,6 +100,7 @@ class _Scratch:
         self.ysplit = torch.empty((need,), dtype=f32, device=device)
         self.pw = torch.empty((T, 64), dtype=f32, device=device)
         self.pidx = torch.empty((T, 64), dtype=i32, device=device)
+        self.logits = torch.empty((T, arch.num_experts), dtype=f32, device=device)
         self._dense: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
         self.device = device
 
@@ -133,6 +134,7 @@ class SpecMoEEngine:
         max_tokens: int = 1024,
         record_timeline: bool = False,
         record: bool = False,
+        record_routing: bool = False,
         capture_layers: tuple[int, ...] = (),
         cuda_graphs: bool = True,
         ffn_impl: str = "auto",
@@ -179,6 +181,7 @@ class SpecMoEEngine:
             copy_stream_ptr=self.copy_stream.cuda_stream,
             batched_io=policy.batched_io,
         )
+        self.window_tokens = window_tokens
         self.cutoff = (
             effective_cutoff(self.model, hw, timings, policy, window_tokens)
             if policy.policy is Policy.DRAFT_PREFETCH
@@ -212,6 +215,9 @@ class SpecMoEEngine:
             self.cache.start_worker()
         self.record_timeline = record_timeline
         self.record = record
+        self.record_routing = record_routing
+        self.trace_scores: list[list[np.ndarray]] = [[] for _ in range(batch)]
+        self._iter_logits: list[torch.Tensor] = []
         self.capture_layers = set(capture_layers)
         self.time_k3 = False
         self.k3_events: list = []
@@ -252,6 +258,25 @@ class SpecMoEEngine:
             self._lib.spmoe_event_destroy(self._route_ev)
             if self._owns_model:
                 self.host_pool.close()
+
+    def recalibrate(self, timings: ProfiledTimings | None = None) -> ProfiledTimings:
+        """Replace the latency-model inputs with measurements of this engine
+        (:func:`calibrate.measure_timings`), re-solve the cutoff layer and,
+        if it moved, re-capture the draft-step graphs (they contain the
+        predictor launches of layers <= cutoff)."""
+        from .calibrate import measure_timings
+
+        t = timings if timings is not None else measure_timings(self)
+        self.timings = t
+        if self.policy.policy is Policy.DRAFT_PREFETCH:
+            new = effective_cutoff(self.model, self.hw, t, self.policy, self.window_tokens)
+            if new != self.cutoff:
+                self.cutoff = new
+                if self._graphs_ready:
+                    torch.cuda.synchronize(self.device)
+                    self._graphs_ready = False
+                    self._ensure_graphs()
+        return t
 
     @property
     def model_state(self) -> tuple:
@@ -342,6 +367,7 @@ class SpecMoEEngine:
             host_idx_dev_ptr=self.route_ring.dev_ptr,
             shared_gate_w=lw.shared_gate,
             out=(s.w[:T], s.idx[:T]),
+            logits_out=s.logits[:T] if self.record_routing else None,
         )
         self._lib.spmoe_event_record_external(self._route_ev, self.stream.cuda_stream)
         return w, idx, sg
@@ -359,6 +385,8 @@ class SpecMoEEngine:
         self.history.record_many(l, ids)
         if self.record:
             self.decisions.append(("verify", l, [int(v) for v in ids]))
+        if self.record_routing:
+            self._iter_logits.append(s.logits[:T].clone())
         required = sorted(set(int(e) for e in ids))
         stream_ptr = self.stream.cuda_stream
         hits, missing = [], []
@@ -708,6 +736,17 @@ class SpecMoEEngine:
             self.emitted_total += len(new)
             self.accepted_total += acc
         self.drafted_total += N * B
+        if self.record_routing and self._iter_logits:
+            # committed positions of this verify: rows 0..accepted of each
+            # sequence (the last committed token and the accepted drafts)
+            from .tracefile import softmax_rows
+
+            lg = torch.stack(self._iter_logits[-a.num_layers:]).cpu().numpy()  # [L, B*(N+1), E]
+            lg = lg.reshape(a.num_layers, B, N + 1, -1)
+            for b in range(B):
+                for t in range(min(res_h[b][0] + 1, emitted[b])):
+                    self.trace_scores[b].append(softmax_rows(lg[:, b, t, :]))
+            self._iter_logits = []
         self.iter_events.append((ev0, ev1, ev2))
         self.iter_records.append(
             IterationRecord(
@@ -748,6 +787,18 @@ class SpecMoEEngine:
         for s_ in self.stalls:
             stall[s_.kind] += s_.a.elapsed_time(s_.b)
         return {"draft_ms": draft, "verify_ms": verify, "stall_ms": stall, "iters": iters}
+
+    def export_trace(self, path, seq: int = 0) -> int:
+        """Write the real gating scores of sequence ``seq``'s committed tokens
+        as a reference trace-v1 file (needs ``record_routing=True``);
+        returns the token count."""
+        from .tracefile import write_trace
+
+        rows = self.trace_scores[seq]
+        if not rows:
+            raise ValueError("no routing recorded (construct the engine with record_routing=True)")
+        write_trace(path, np.stack(rows), self.arch.name, self.arch.top_k, 0, self.policy.seed)
+        return len(rows)
 
     def transfers(self) -> list[TransferRecord]:
         out = []

@@ -55,6 +55,7 @@ def router_topk(
     host_idx_dev_ptr: int | None = None,
     shared_gate_w: torch.Tensor | None = None,
     out: tuple[torch.Tensor, torch.Tensor] | None = None,
+    logits_out: torch.Tensor | None = None,
     stream=None,
 ):
     """Fused router projection + top-k + softmax weights.
@@ -73,7 +74,8 @@ def router_topk(
         idx = torch.empty((T, k), dtype=I32, device=x.device)
     else:
         weights, idx = out
-    logits = torch.empty((T, E), dtype=F32, device=x.device) if want_logits else None
+    logits = logits_out if logits_out is not None else (
+        torch.empty((T, E), dtype=F32, device=x.device) if want_logits else None)
     sg = None
     if shared_gate_w is not None:
         _need(shared_gate_w, BF16, "shared_gate_w")

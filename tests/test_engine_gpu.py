@@ -227,3 +227,27 @@ def test_engine_tiny_tcgen05_path(oracle):
     layer's max |value|, i.e. one bf16 ulp at the top of the range)."""
     eng, rep = run_and_check(oracle, tol=2.0 ** -7, ffn_impl="tcgen05", batch=2)
     eng.close()
+
+
+def test_engine_trace_export_and_measured_timings(tmp_path):
+    """§8(f) rows: real gating scores exported as trace-v1 (one row block
+    per committed token), ProfiledTimings measured on the live engine."""
+    from paper_2510_10302_b200.calibrate import measure_timings
+    from paper_2510_10302_b200.tracefile import read_trace
+
+    eng = make_engine(record=False, capture=(), record_routing=True)
+    try:
+        eng.prefill(prompts(1))
+        remaining = [12]
+        while remaining[0] > 0:
+            remaining = [remaining[0] - eng.step(remaining)[0]]
+        rep = eng.report()
+        n = eng.export_trace(tmp_path / "trace.txt")
+        fields, scores = read_trace(tmp_path / "trace.txt")
+        assert n == rep.emitted_tokens == scores.shape[0]
+        assert scores.shape[1:] == (eng.arch.num_layers, eng.arch.num_experts)
+        assert np.allclose(scores.sum(-1), 1.0)
+        t = measure_timings(eng)
+        assert t.t_comp_draft > 0 and t.t_comp_target > 0 and t.t_io_expert > 0
+    finally:
+        eng.close()
