@@ -274,6 +274,15 @@ int spmoe_rt_slot_ready(spmoe_rt* rt, int slot);
 int spmoe_rt_worker_start(spmoe_rt* rt);
 int spmoe_rt_push_task(spmoe_rt* rt, int layer, const int32_t* host_idx, int k,
                        void* ready_event, int issue_token);
+/* Same, with a graph-safe hand-off: the worker waits until the int32
+ * counter *flag (mapped pinned memory, bumped on the device by
+ * spmoe_signal_bump after the predictor kernel) reaches `expected`, then
+ * reads host_idx.  Used for predictor kernels replayed inside CUDA graphs. */
+int spmoe_rt_push_task_flag(spmoe_rt* rt, int layer, const int32_t* host_idx, int k,
+                            const int32_t* flag, int32_t expected, int issue_token);
+/* Device-side increment of a host-visible counter in mapped memory
+ * (stream-ordered; system-scope fenced). */
+int spmoe_signal_bump(int32_t* flag, void* stream);
 /* Block until every pushed task has been popped and its copies issued. */
 int spmoe_rt_drain(spmoe_rt* rt);
 /* Drop queued-but-unpopped tasks (end of inference); returns count. */

@@ -95,7 +95,19 @@ router_topk_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ 
       idx[(size_t)t * k + i] = sel[i];
       if (host_idx != nullptr) host_idx[(size_t)t * k + i] = sel[i];
     }
+    // make the zero-copy indices visible to the host before any later
+    // signal (spmoe_signal_bump) can be observed
+    if (host_idx != nullptr) __threadfence_system();
   }
+}
+
+// Host-visible completion counter in mapped pinned memory: stream-ordered
+// after the kernels whose results the host waits for; graph-capturable (the
+// increment happens on the device at replay time).
+__global__ void signal_bump_kernel(volatile int32_t* flag) {
+  __threadfence_system();
+  *flag = *flag + 1;
+  __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -600,6 +612,12 @@ int spmoe_greedy_accept(const float* logits, int64_t ld, const int32_t* draft, i
   if (st) return st;
   accept_prefix_kernel<<<(B + 127) / 128, 128, 0, (cudaStream_t)stream>>>(argmax_out, draft, B,
                                                                           N, result);
+  return launch_status();
+}
+
+int spmoe_signal_bump(int32_t* flag, void* stream) {
+  if (!flag) return (int)cudaErrorInvalidValue;
+  signal_bump_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flag);
   return launch_status();
 }
 

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
 #include <cstring>
 #include <deque>
@@ -32,6 +33,12 @@ struct Task {
   int k;
   cudaEvent_t ready;
   int issue_token;
+  const volatile int32_t* flag;  // device-bumped completion counter (or null)
+  int32_t expected;
+};
+
+struct WindowEntry {
+  std::vector<int> ids, victims;
 };
 
 struct Transfer {
@@ -78,6 +85,9 @@ struct spmoe_rt {
   int64_t pushed_ = 0, processed_ = 0;
   bool stop_ = false, running_ = false;
   std::thread worker_;
+
+  // tasks consumed since the last drain (for evictions_of_queued_targets)
+  std::vector<WindowEntry> window_;
 
   // transfer log
   std::vector<Transfer> log_;
@@ -211,41 +221,54 @@ struct spmoe_rt {
 
   // -------------------------------------------------------------- worker
   void run_task(const Task& t) {
-    if (t.ready) cudaEventSynchronize(t.ready);
+    if (t.flag) {
+      // graph-safe hand-off: the predictor's completion counter in mapped
+      // memory reaches `expected` once this replay's indices are visible
+      int spins = 0;
+      while (*t.flag < t.expected) {
+        if (++spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(2));
+      }
+    } else if (t.ready) {
+      cudaEventSynchronize(t.ready);
+    }
     std::lock_guard<std::mutex> g(mu_);
     // pop-time residency filter (enqueue_critical prefetch.py:131-135 and the
     // worker re-check prefetch.py:186-189 collapse into one probe here,
-    // because the predicted ids live on the device until the event fires)
+    // because the predicted ids live on the device until the kernel is done)
+    WindowEntry we;
     std::vector<int> load;
     for (int i = 0; i < t.k; ++i) {
       const int e = ((volatile const int32_t*)t.host_idx)[i];
       if (e < 0 || e >= E) continue;
       const int key = t.layer * E + e;
+      we.ids.push_back(key);
       if (!resident(key) && std::find(load.begin(), load.end(), key) == load.end())
         load.push_back(key);
     }
-    if (load.empty()) return;  // nothing to move: no task materialises
-    std::vector<int> victims;
-    if (!insert_batch(load, 0, victims)) return;
-    // victims that are still queued targets of later tasks (simcore.py:275-278)
-    {
-      std::lock_guard<std::mutex> q(qmu_);
-      for (int v : victims) {
-        for (const Task& qt : queue_) {
-          bool hit = false;
-          if (qt.layer == v / E) {
-            // ids of queued tasks may not have landed yet; only count the
-            // ones whose event already completed
-            if (qt.ready == nullptr || cudaEventQuery(qt.ready) == cudaSuccess)
-              for (int i = 0; i < qt.k; ++i)
-                if (((volatile const int32_t*)qt.host_idx)[i] == v % E) hit = true;
-          }
-          if (hit) { ++evictions_of_queued; break; }
-        }
+    if (!load.empty()) {
+      std::vector<int> victims;
+      if (insert_batch(load, 0, victims)) {
+        we.victims = victims;
+        issue_copies(load, t.layer, 0);
+        ++tasks_completed;
       }
     }
-    issue_copies(load, t.layer, 0);
-    ++tasks_completed;
+    window_.push_back(std::move(we));
+  }
+
+  // Victims of a task that are predicted targets of a LATER task of the same
+  // drafting window (simcore.py:275-278), evaluated once every task of the
+  // window has been consumed, so the count is deterministic.
+  void close_window() {
+    std::lock_guard<std::mutex> g(mu_);
+    for (size_t i = 0; i < window_.size(); ++i)
+      for (int v : window_[i].victims) {
+        bool hit = false;
+        for (size_t j = i + 1; j < window_.size() && !hit; ++j)
+          hit = std::find(window_[j].ids.begin(), window_[j].ids.end(), v) != window_[j].ids.end();
+        if (hit) ++evictions_of_queued;
+      }
+    window_.clear();
   }
 
   void worker_loop() {
@@ -469,7 +492,20 @@ int spmoe_rt_push_task(spmoe_rt* rt, int layer, const int32_t* host_idx, int k, 
   if (!rt || !host_idx || k < 1 || layer < 0 || layer >= rt->L) return (int)cudaErrorInvalidValue;
   {
     std::lock_guard<std::mutex> q(rt->qmu_);
-    rt->queue_.push_back(Task{layer, host_idx, k, (cudaEvent_t)ready_event, issue_token});
+    rt->queue_.push_back(Task{layer, host_idx, k, (cudaEvent_t)ready_event, issue_token, nullptr, 0});
+    ++rt->pushed_;
+  }
+  rt->qcv_.notify_one();
+  return 0;
+}
+
+int spmoe_rt_push_task_flag(spmoe_rt* rt, int layer, const int32_t* host_idx, int k,
+                            const int32_t* flag, int32_t expected, int issue_token) {
+  if (!rt || !host_idx || !flag || k < 1 || layer < 0 || layer >= rt->L) return (int)cudaErrorInvalidValue;
+  {
+    std::lock_guard<std::mutex> q(rt->qmu_);
+    rt->queue_.push_back(
+        Task{layer, host_idx, k, nullptr, issue_token, (const volatile int32_t*)flag, expected});
     ++rt->pushed_;
   }
   rt->qcv_.notify_one();
@@ -478,20 +514,23 @@ int spmoe_rt_push_task(spmoe_rt* rt, int layer, const int32_t* host_idx, int k, 
 
 int spmoe_rt_drain(spmoe_rt* rt) {
   if (!rt) return (int)cudaErrorInvalidValue;
-  std::unique_lock<std::mutex> q(rt->qmu_);
-  if (!rt->running_) {
-    // no thread: run the queue inline (deterministic single-thread mode)
-    while (!rt->queue_.empty()) {
-      Task t = rt->queue_.front();
-      rt->queue_.pop_front();
-      q.unlock();
-      rt->run_task(t);
-      q.lock();
-      ++rt->processed_;
+  {
+    std::unique_lock<std::mutex> q(rt->qmu_);
+    if (!rt->running_) {
+      // no thread: run the queue inline (deterministic single-thread mode)
+      while (!rt->queue_.empty()) {
+        Task t = rt->queue_.front();
+        rt->queue_.pop_front();
+        q.unlock();
+        rt->run_task(t);
+        q.lock();
+        ++rt->processed_;
+      }
+    } else {
+      rt->done_cv_.wait(q, [&] { return rt->processed_ == rt->pushed_; });
     }
-    return 0;
   }
-  rt->done_cv_.wait(q, [&] { return rt->processed_ == rt->pushed_; });
+  rt->close_window();
   return 0;
 }
 

@@ -218,17 +218,15 @@ def tc_split(ffn_dim: int) -> int:
     return max(1, min(16, kb // 4))
 
 
-def _best_split(tiles: int, kblocks: int, sms: int) -> int:
-    """Smallest split whose (tiles x split) fills the SMs to >= 95 %, else the
-    best fill found (fixed-order partial reduction keeps it deterministic)."""
-    best_s, best_eff = 1, 0.0
+def _best_split(tiles: int, kblocks: int, sms: int, penalty_kb: float = 3.0) -> int:
+    """Split minimising the modelled critical path: each SM streams
+    ceil(tiles*s/sms) tile slices of kblocks/s K-blocks, and any split > 1
+    pays a fixed-order partial reduction (~penalty_kb K-blocks of time)."""
+    best_s, best_t = 1, None
     for s in range(1, min(16, max(1, kblocks // 4)) + 1):
-        n = tiles * s
-        eff = n / (sms * -(-n // sms))
-        if eff > best_eff + 1e-9:
-            best_s, best_eff = s, eff
-        if eff >= 0.95:
-            break
+        t = -(-tiles * s // sms) * (kblocks / s) + (penalty_kb if s > 1 else 0.0)
+        if best_t is None or t < best_t - 1e-9:
+            best_s, best_t = s, t
     return best_s
 
 

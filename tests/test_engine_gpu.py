@@ -169,18 +169,55 @@ def test_engine_tiny_batch4(oracle):
     eng.close()
 
 
-def test_engine_deterministic(oracle):
+@pytest.mark.parametrize("ffn_impl", ["cuda_core", "auto"])
+def test_engine_deterministic(oracle, ffn_impl):
+    """Same seeds -> same tokens, same transfers, same cache counters (the
+    worker thread's timing must not leak into any decision)."""
     outs = []
     for _ in range(2):
-        eng = make_engine(record=False, capture=())
+        eng = make_engine(record=False, capture=(), ffn_impl=ffn_impl)
         try:
             eng.prefill(prompts(1))
             for _ in range(4):
                 eng.step()
-            outs.append((list(eng.seqs[0]), eng.cache.counters()))
+            log = [(r["kind"], r["layer"], r["experts"]) for r in eng.cache.transfer_log()]
+            outs.append((list(eng.seqs[0]), eng.cache.counters(), log))
         finally:
             eng.close()
-    assert outs[0] == outs[1]
+    assert outs[0][0] == outs[1][0], "tokens differ"
+    assert outs[0][2] == outs[1][2], "transfer sequence differs"
+    assert outs[0][1] == outs[1][1], "cache counters differ"
+
+
+def test_flag_handoff_push_task():
+    """push_task_flag: the worker waits for a device-bumped counter in mapped
+    memory before reading the predicted ids (graph-safe hand-off)."""
+    import ctypes as C
+
+    from paper_2510_10302_b200 import _native
+    from paper_2510_10302_b200.cache import NativeExpertCache
+
+    lib = _native.load()
+    host, dev = C.c_void_p(), C.c_void_p()
+    _native.check("alloc", lib.spmoe_host_alloc_mapped(64, C.byref(host), C.byref(dev)))
+    arr = (C.c_int32 * 16).from_address(host.value)
+    arr[0], arr[1], arr[8] = 3, 5, 0  # ids at [0:2], counter at [8]
+    pool = torch.empty((4, 64), dtype=torch.bfloat16, device="cuda")
+    hostpool = torch.zeros((16, 64), dtype=torch.bfloat16).pin_memory()
+    cs = torch.cuda.Stream()
+    cache = NativeExpertCache(4, 2, 8, dev_pool_ptr=pool.data_ptr(), host_pool_ptr=hostpool.data_ptr(),
+                              slot_bytes=128, copy_stream_ptr=cs.cuda_stream)
+    try:
+        cache.start_worker()
+        _native.check("push", lib.spmoe_rt_push_task_flag(cache._h, 1, host.value, 2, host.value + 32, 1, 0))
+        torch.cuda._sleep(20_000_000)  # the bump lands well after the push
+        _native.check("bump", lib.spmoe_signal_bump(dev.value + 32, torch.cuda.current_stream().cuda_stream))
+        cache.drain()
+        assert arr[8] == 1
+        assert cache.lookup((1, 3), False) and cache.lookup((1, 5), False)
+    finally:
+        cache.close()
+        lib.spmoe_host_free(host)
 
 
 def test_engine_shared_expert_arch(oracle):
