@@ -97,7 +97,9 @@ class ArchSpec:
 
     @property
     def d_ffn(self) -> int:
-        return self.draft_ffn or self.ffn
+        """Draft dense FFN width: explicit, else the derived proxy (mean routed
+        expert, plus the shared expert(s) concatenated along F)."""
+        return self.draft_ffn or (self.ffn + self.shared_ffn)
 
     @property
     def qkv_dim(self) -> int:
@@ -351,15 +353,6 @@ def build_weights(
                         written.add(row)
         mean = (acc / E).to(bf)
         del acc
-        if arch.d_ffn != F:
-            draft = torch.empty((1, 3 * arch.d_ffn * H), dtype=bf, device=device)
-            fill_blob_generic(draft[0], arch.d_ffn, H, tensor_seed(seed, K_EXPERT, l, 10_000), std, arch.expert_out_scale * arch.res_scale)
-        else:
-            draft = mean.view(1, -1).clone()
-        if draft_perturb > 0.0:
-            noise = torch.empty_like(draft)
-            _fill(noise, tensor_seed(seed, K_PERTURB, l), std * draft_perturb)
-            draft = (draft.float() + noise.float()).to(bf)
         shared = None
         sgate = None
         if arch.shared_ffn:
@@ -367,6 +360,15 @@ def build_weights(
             fill_blob_generic(shared[0], arch.shared_ffn, H, tensor_seed(seed, K_SHARED, l), std, arch.expert_out_scale * arch.res_scale)
             if arch.shared_gate:
                 sgate = _fill(torch.empty((H,), dtype=bf, device=device), tensor_seed(seed, K_SGATE, l), 1.0 / math.sqrt(H))
+        if arch.draft_ffn:
+            draft = torch.empty((1, 3 * arch.d_ffn * H), dtype=bf, device=device)
+            fill_blob_generic(draft[0], arch.d_ffn, H, tensor_seed(seed, K_EXPERT, l, 10_000), std, arch.expert_out_scale * arch.res_scale)
+        else:
+            draft = _draft_proxy(arch, mean, shared, router)
+        if draft_perturb > 0.0:
+            noise = torch.empty_like(draft)
+            _fill(noise, tensor_seed(seed, K_PERTURB, l), std * draft_perturb)
+            draft = (draft.float() + noise.float()).to(bf)
         layers.append(
             LayerWeights(
                 attn_norm=torch.ones((H,), dtype=bf, device=device),
@@ -393,6 +395,38 @@ def build_weights(
         rope_cos=cos,
         rope_sin=sin,
     )
+
+
+def _draft_proxy(arch: ArchSpec, mean: torch.Tensor, shared: torch.Tensor | None, router: torch.Tensor) -> torch.Tensor:
+    """Dense draft FFN approximating the layer's MoE: the mean routed expert
+    with W2 scaled by the expected routed gate mass (1 with top-k renorm,
+    E[sum of the top-k softmax] otherwise, estimated on the router with unit
+    RMS inputs), concatenated along F with the shared expert (W2 scaled by
+    the expected sigmoid gate, 0.5, for Qwen)."""
+    H, F = arch.hidden, arch.ffn
+    if arch.renorm:
+        mass = 1.0
+    else:
+        g = torch.Generator(device=router.device).manual_seed(0)
+        xs = torch.randn((512, H), generator=g, device=router.device, dtype=torch.float32)
+        p = torch.softmax(xs @ router.float().t(), dim=-1)
+        mass = float(p.topk(arch.top_k, dim=-1).values.sum(-1).mean())
+    w1 = mean[: F * H].view(F, H)
+    w3 = mean[F * H : 2 * F * H].view(F, H)
+    w2 = (mean[2 * F * H :].view(H, F).float() * mass).to(mean.dtype)
+    if shared is None:
+        return torch.cat([w1.reshape(-1), w3.reshape(-1), w2.reshape(-1)]).view(1, -1)
+    Fs = arch.shared_ffn
+    s = shared[0]
+    s1 = s[: Fs * H].view(Fs, H)
+    s3 = s[Fs * H : 2 * Fs * H].view(Fs, H)
+    s2 = s[2 * Fs * H :].view(H, Fs)
+    if arch.shared_gate:
+        s2 = (s2.float() * 0.5).to(s.dtype)
+    d1 = torch.cat([w1, s1], dim=0)
+    d3 = torch.cat([w3, s3], dim=0)
+    d2 = torch.cat([w2, s2], dim=1)
+    return torch.cat([d1.reshape(-1), d3.reshape(-1), d2.reshape(-1)]).view(1, -1)
 
 
 def fill_blob_generic(blob: torch.Tensor, F: int, H: int, seed: int, std: float, out_scale: float) -> None:
