@@ -218,29 +218,25 @@ def tc_split(ffn_dim: int) -> int:
     return max(1, min(16, kb // 4))
 
 
-def _best_split(tiles: int, kblocks: int, sms: int, penalty_kb: float = 3.0) -> int:
-    """Split minimising the modelled critical path: each SM streams
-    ceil(tiles*s/sms) tile slices of kblocks/s K-blocks, and any split > 1
-    pays a fixed-order partial reduction (~penalty_kb K-blocks of time)."""
-    best_s, best_t = 1, None
-    for s in range(1, min(16, max(1, kblocks // 4)) + 1):
-        t = -(-tiles * s // sms) * (kblocks / s) + (penalty_kb if s > 1 else 0.0)
-        if best_t is None or t < best_t - 1e-9:
-            best_s, best_t = s, t
-    return best_s
-
-
 def tc_plan(token_counts, hidden: int, ffn_dim: int, sms: int = 148) -> tuple[int, int]:
     """(split_up, split_dn) for the tcgen05 K3 launch of experts with the
-    given routed-token counts: the number of (expert, 64-token chunk, 128-row)
-    tiles of each phase times the split should be a near multiple of the SM
-    count."""
+    given routed-token counts.
+
+    Rule measured on B200 (tools/tc_split_sweep.py, profiles/r1_tc_split_sweep.jsonl):
+    splitting never pays when the phase already has >= ~0.85 x SMs tiles
+    (the fixed-order partial reduction costs more than the tail it removes),
+    and the up phase always has enough (F/128 = 112 tiles per Mixtral
+    expert).  The down phase of one or two experts (32 tiles each) does not:
+    split K so that tiles x split reaches ~0.85 x SMs (1 expert: 3.3 -> 4.3
+    TB/s, 2 experts: 4.6 -> 5.1 TB/s)."""
     chunks = sum((int(c) + 63) // 64 for c in token_counts if c > 0)
     if chunks == 0:
         return 1, 1
-    up = _best_split(chunks * (ffn_dim // 128), hidden // 64, sms)
-    dn = _best_split(chunks * (hidden // 128), ffn_dim // 64, sms)
-    return up, dn
+    tiles_dn = chunks * (hidden // 128)
+    want = 0.85 * sms
+    sd = 1 if tiles_dn >= want else -(-int(want) // tiles_dn)
+    sd = max(1, min(sd, 16, (ffn_dim // 64) // 4))
+    return 1, sd
 
 
 def tc_workspace_floats(rows: int, hidden: int, ffn_dim: int, split_up: int, split_dn: int) -> int:

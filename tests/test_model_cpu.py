@@ -65,3 +65,16 @@ def test_oracle_fill_matches_seed_helper(oracle):
     assert np.array_equal(a, b)
     f = oracle.bf16_bits_to_f32(a)
     assert abs(f.std() - 0.02) < 2e-3
+
+
+def test_tc_plan_rule():
+    from paper_2510_10302_b200.kernels import tc_plan, tc_workspace_floats
+
+    assert tc_plan([], 4096, 14336) == (1, 1)
+    assert tc_plan([1], 4096, 14336) == (1, 4)  # 32 down tiles -> 128
+    assert tc_plan([1, 1], 4096, 14336) == (1, 2)
+    assert tc_plan([3, 2, 2, 2, 1], 4096, 14336) == (1, 1)
+    assert tc_plan([1] * 25, 2048, 1408) == (1, 1)
+    su, sd = tc_plan([1], 2048, 1408)
+    assert su == 1 and 1 < sd <= 1408 // 64 // 4
+    assert tc_workspace_floats(10, 4096, 14336, 1, 4) == 4 * 10 * 4096

@@ -86,11 +86,6 @@ def test_tc_split_invariance(oracle):
         check(*run_tc(oracle, 9, 256, 1024, 8, 2, seed=11, split=s))
 
 
-def test_tc_plan_fills_sms():
-    from paper_2510_10302_b200.kernels import tc_plan
-
-    # one Mixtral expert, one token: 112 up tiles / 32 down tiles alone leave SMs idle
-    su, sd = tc_plan([1], 4096, 14336)
-    assert (112 * su) / (148 * -(-112 * su // 148)) >= 0.9
-    assert (32 * sd) / (148 * -(-32 * sd // 148)) >= 0.9
-    assert tc_plan([], 4096, 14336) == (1, 1)
+def test_tc_planned_split_single_expert(oracle):
+    """The planner's down-phase split for a lone late expert stays in tolerance."""
+    check(*run_tc(oracle, 2, 256, 1024, 1, 1, seed=13))
