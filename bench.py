@@ -127,60 +127,70 @@ def h2d_peak_gbs(torch, nbytes=1 << 30, reps=5) -> float:
 # CPU restatement (oracle port) of the same path: the reference arm and the
 # cpu_baseline leg.  Executes oracle/ only here, as the timed CPU baseline.
 # ---------------------------------------------------------------------------
-def cpu_path_iteration(arch, seed, N, B, prefetch_k, cutoff, sample_layers, threads, blob_rows=None):
-    """Time one SD iteration of the verify-time expert path on the host cores:
-    for ``sample_layers`` target layers, K1 router + K2 permute + K3 SwiGLU
-    experts + K4 combine at T = B*(N+1) tokens, plus the drafting-stage
-    predictor projections (K1, k = prefetch_k) of those layers for N draft
-    steps, scaled to all layers; plus K6 acceptance.  Returns seconds."""
-    import numpy as np
+class CpuPath:
+    """The verify-time expert path of one SD iteration restated on the host
+    cores (oracle/spmoe_oracle.c, all threads): for ``sample_layers`` target
+    layers, K1 router + K2 permute + K3 SwiGLU experts + K4 combine at
+    T = B*(N+1) tokens, plus the drafting-stage predictor projections (K1,
+    k = prefetch_k) of the layers <= cutoff for N draft steps; scaled to all
+    layers; plus K6 acceptance.  Expert blobs are built once (setup), from
+    the GPU run's host pool when given, else regenerated with the same
+    counter-hash streams."""
 
-    from oracle import tensor_oracle as O
-    from paper_2510_10302_b200.model import K_EXPERT, K_ROUTER, _splitmix64, tensor_seed
+    def __init__(self, arch, seed, N, B, prefetch_k, cutoff, sample_layers, threads, blob_rows=None):
+        import numpy as np
 
-    O.set_threads(threads)
-    H, F, E, k = arch.hidden, arch.ffn, arch.num_experts, arch.top_k
-    T = B * (N + 1)
-    rng = np.random.default_rng(seed)
-    x = O.f32_to_bf16_bits(rng.standard_normal((T, H)).astype(np.float32))
-    resid = O.f32_to_bf16_bits(rng.standard_normal((T, H)).astype(np.float32) * 0.1)
-    layers = list(range(sample_layers))
-    # expert blobs for the sampled layers (same counter-hash bits the GPU uses)
-    blobs = {}
-    n13 = F * H
-    for l in layers:
-        rw = O.fill_normal_bf16(E * H, tensor_seed(seed, K_ROUTER, l), 0, 1.0 / np.sqrt(H)).reshape(E, H)
-        eb = []
-        for e in range(E):
-            if blob_rows is not None:
-                eb.append(blob_rows(l, e))
-                continue
-            s0 = tensor_seed(seed, K_EXPERT, l * E + e)
-            b = np.empty(3 * n13, np.uint16)
-            b[:n13] = O.fill_normal_bf16(n13, _splitmix64(s0 ^ 1), 0, arch.init_std)
-            b[n13:2 * n13] = O.fill_normal_bf16(n13, _splitmix64(s0 ^ 3), 0, arch.init_std)
-            b[2 * n13:] = O.fill_normal_bf16(n13, _splitmix64(s0 ^ 2), 0, arch.init_std * arch.expert_out_scale)
-            eb.append(b)
-        blobs[l] = (rw, eb)
-    logits = rng.standard_normal((B, N + 1, 4096)).astype(np.float32)
-    draft = rng.integers(0, 4096, (B, N)).astype(np.int32)
-    xd = x[:B]
-    t0 = time.perf_counter()
-    for l in layers:
-        rw, eb = blobs[l]
-        w, idx, _, _ = O.router_topk(x, rw, k, arch.renorm)
-        off, perm, inv = O.moe_permute(idx, E)
-        used = set(int(v) for v in idx.ravel())
-        _, y = O.expert_ffn([eb[e] if e in used else None for e in range(E)], x, F, off, perm)
-        O.moe_combine(y, inv, w, T, H, k, residual=resid)
-        if cutoff is not None and l <= cutoff:
-            for _ in range(N):
-                O.router_topk(xd, rw, prefetch_k, True)
-    t_layers = time.perf_counter() - t0
-    t1 = time.perf_counter()
-    O.greedy_accept(logits, draft)
-    t_acc = (time.perf_counter() - t1) * arch.vocab / 4096
-    return t_layers * arch.num_layers / len(layers) + t_acc
+        from oracle import tensor_oracle as O
+        from paper_2510_10302_b200.model import K_EXPERT, K_ROUTER, _splitmix64, tensor_seed
+
+        self.O, self.arch, self.N, self.B = O, arch, N, B
+        self.prefetch_k, self.cutoff = prefetch_k, cutoff
+        O.set_threads(threads)
+        H, F, E = arch.hidden, arch.ffn, arch.num_experts
+        self.T = B * (N + 1)
+        rng = np.random.default_rng(seed)
+        self.x = O.f32_to_bf16_bits(rng.standard_normal((self.T, H)).astype(np.float32))
+        self.resid = O.f32_to_bf16_bits(rng.standard_normal((self.T, H)).astype(np.float32) * 0.1)
+        self.layers = list(range(sample_layers))
+        self.blobs = {}
+        n13 = F * H
+        for l in self.layers:
+            rw = O.fill_normal_bf16(E * H, tensor_seed(seed, K_ROUTER, l), 0, 1.0 / np.sqrt(H)).reshape(E, H)
+            eb = []
+            for e in range(E):
+                if blob_rows is not None:
+                    eb.append(blob_rows(l, e))
+                    continue
+                s0 = tensor_seed(seed, K_EXPERT, l * E + e)
+                b = np.empty(3 * n13, np.uint16)
+                b[:n13] = O.fill_normal_bf16(n13, _splitmix64(s0 ^ 1), 0, arch.init_std)
+                b[n13:2 * n13] = O.fill_normal_bf16(n13, _splitmix64(s0 ^ 3), 0, arch.init_std)
+                b[2 * n13:] = O.fill_normal_bf16(n13, _splitmix64(s0 ^ 2), 0, arch.init_std * arch.res_scale)
+                eb.append(b)
+            self.blobs[l] = (rw, eb)
+        self.logits = rng.standard_normal((B, N + 1, 4096)).astype(np.float32)
+        self.draft = rng.integers(0, 4096, (B, N)).astype(np.int32)
+
+    def iteration_seconds(self) -> float:
+        O, a = self.O, self.arch
+        E, k = a.num_experts, a.top_k
+        xd = self.x[: self.B]
+        t0 = time.perf_counter()
+        for l in self.layers:
+            rw, eb = self.blobs[l]
+            w, idx, _, _ = O.router_topk(self.x, rw, k, a.renorm)
+            off, perm, inv = O.moe_permute(idx, E)
+            used = set(int(v) for v in idx.ravel())
+            _, y = O.expert_ffn([eb[e] if e in used else None for e in range(E)], self.x, a.ffn, off, perm)
+            O.moe_combine(y, inv, w, self.T, a.hidden, k, residual=self.resid)
+            if self.cutoff is not None and l <= self.cutoff:
+                for _ in range(self.N):
+                    O.router_topk(xd, rw, self.prefetch_k, True)
+        t_layers = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        O.greedy_accept(self.logits, self.draft)
+        t_acc = (time.perf_counter() - t1) * a.vocab / 4096
+        return t_layers * a.num_layers / len(self.layers) + t_acc
 
 
 def calibration(cfg_name: str) -> dict:
@@ -205,9 +215,11 @@ def run_reference(args, cfg, rank, world):
     cal = calibration(args.config)
     emitted = cal.get("emitted_per_iter", cfg["N"] + 1) * cfg["batch"]
     sample_layers = 2 if arch.hidden >= 4096 else 4
+    pk = 1 if arch.num_experts <= 16 else arch.top_k
+    path = CpuPath(arch, 1234, cfg["N"], cfg["batch"], pk, cal.get("cutoff"), sample_layers, threads)
     times = []
     for i in range(args.warmup + args.steps):
-        t = cpu_path_iteration(arch, 1234, cfg["N"], cfg["batch"], 1, cal.get("cutoff"), sample_layers, threads)
+        t = path.iteration_seconds()
         if i >= args.warmup:
             times.append(t)
     it_s = float(np.mean(times))
@@ -389,6 +401,7 @@ def main():
                                     "t_comp_target": measured.t_comp_target * 1e3,
                                     "t_io_expert": measured.t_io_expert * 1e3},
             "window_tokens": cfg["N"],
+            "k_eff_measured": getattr(eng, "k_eff", None),
         },
         "latency_breakdown": rep.latency_breakdown,
         "verify_moe_hbm_gbs": roof.get("achieved_gbs"),
@@ -426,8 +439,10 @@ def main():
         emitted_per_iter = emitted / args.steps
         sample_layers = 2
         hp = eng.host_pool
-        t_cpu = cpu_path_iteration(arch, 1234, N, B, policy.prefetch_k, eng.cutoff, sample_layers, threads,
-                                   blob_rows=lambda l, e: hp.array[hp.row_of(l, e)])
+        path = CpuPath(arch, 1234, N, B, policy.prefetch_k, eng.cutoff, sample_layers, threads,
+                       blob_rows=lambda l, e: hp.array[hp.row_of(l, e)])
+        path.iteration_seconds()  # warm caches / page in
+        t_cpu = min(path.iteration_seconds() for _ in range(2))
         out["cpu_baseline"] = {
             "value": emitted_per_iter / t_cpu, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{sample_layers} of {arch.num_layers} verify-MoE layers + predictor projections on the CPU "

@@ -51,14 +51,17 @@ from .predictor import DraftGuidedPredictor, HistoryCounter, top_k_indices
 from .report import ComputeSlot, IterationRecord, SimReport, TransferKind, TransferRecord
 
 
-def effective_cutoff(model, hw, timings, policy, window_tokens: int = 1) -> int | None:
+def effective_cutoff(model, hw, timings, policy, window_tokens: int = 1, k_eff: int | None = None) -> int | None:
     """Cutoff honoured by the engine: explicit override, else the solver's
     answer (None = infeasible -> no drafting-stage prefetch), clamped to both
-    depths (``simcore.py:182-197``)."""
+    depths (``simcore.py:182-197``).  ``k_eff`` replaces prefetch_k as the
+    per-layer expert count (measured distinct prefetches per layer over an
+    N-token window, see :meth:`SpecMoEEngine.recalibrate`)."""
     if policy.cutoff_layer is not None:
         layer = policy.cutoff_layer
     else:
-        res = solve_cutoff(cutoff_input_from_specs(model, hw, timings, policy.prefetch_k, window_tokens=window_tokens))
+        k = max(policy.prefetch_k, k_eff or 0)
+        res = solve_cutoff(cutoff_input_from_specs(model, hw, timings, k, window_tokens=window_tokens))
         if not res.feasible:
             return None
         layer = res.layer
@@ -269,7 +272,13 @@ class SpecMoEEngine:
         t = timings if timings is not None else measure_timings(self)
         self.timings = t
         if self.policy.policy is Policy.DRAFT_PREFETCH:
-            new = effective_cutoff(self.model, self.hw, t, self.policy, self.window_tokens)
+            # distinct experts actually prefetched per prefetched layer per
+            # iteration (each of the N draft tokens predicts its own top-k)
+            n_it = max(1, len(self.iter_records))
+            pre = sum(len(r.experts) for r in self.transfers() if r.kind is TransferKind.PREFETCH)
+            layers = (self.cutoff + 1) if self.cutoff is not None else 0
+            self.k_eff = max(self.policy.prefetch_k, round(pre / (n_it * layers))) if layers else None
+            new = effective_cutoff(self.model, self.hw, t, self.policy, self.window_tokens, self.k_eff)
             if new != self.cutoff:
                 self.cutoff = new
                 if self._graphs_ready:
