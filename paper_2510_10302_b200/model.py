@@ -67,7 +67,7 @@ class ArchSpec:
     # deviation, so the draft's mean-expert FFN tracks the routed mixture and
     # random-init SD accepts drafts at a realistic rate (SURVEY.md §7 hard
     # part 2).  Bytes moved and FLOPs are unchanged.
-    expert_spread: float | None = 0.04
+    expert_spread: float | None = 0.02
     # init scales: token embedding std, and GPT-2-style residual-branch
     # scaling of the output projections (W_o, W2): std * residual_scale,
     # None -> 1/sqrt(2 * num_layers).  Keeps the 32-layer random network out
