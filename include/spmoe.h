@@ -296,6 +296,10 @@ int spmoe_rt_worker_stop(spmoe_rt* rt);
 int spmoe_rt_transfer_log(spmoe_rt* rt, int32_t* rec4, double* t2, int cap);
 /* Experts of record i (expert ids, up to cap). */
 int spmoe_rt_transfer_experts(spmoe_rt* rt, int i, int32_t* experts, int cap);
+/* Milliseconds from the runtime epoch (a timing event recorded on the copy
+ * stream at creation) to `event` (a timing cudaEvent_t on any stream), so
+ * compute slots and transfers share one clock.  -1 if not measurable. */
+double spmoe_rt_since_epoch_ms(spmoe_rt* rt, void* event);
 /* Drop the transfer log (waits for logged copies to finish). */
 void spmoe_rt_clear_log(spmoe_rt* rt);
 

@@ -72,6 +72,7 @@ SIGNATURES: dict[str, tuple] = {
     "spmoe_rt_transfer_log": (_i, [_p, _p, _p, _i]),
     "spmoe_rt_transfer_experts": (_i, [_p, _i, _p, _i]),
     "spmoe_rt_clear_log": (None, [_p]),
+    "spmoe_rt_since_epoch_ms": (C.c_double, [_p, _p]),
     "spmoe_host_alloc_mapped": (_i, [_sz, _p, _p]),
     "spmoe_host_free": (_i, [_p]),
     "spmoe_host_register": (_i, [_p, _sz]),

@@ -345,3 +345,7 @@ class NativeExpertCache:
 
     def clear_log(self) -> None:
         self._lib.spmoe_rt_clear_log(self._h)
+
+    def since_epoch_ms(self, event) -> float:
+        """ms from the runtime epoch to a recorded torch.cuda.Event (timing)."""
+        return float(self._lib.spmoe_rt_since_epoch_ms(self._h, event.cuda_event))

@@ -650,3 +650,10 @@ int spmoe_event_record_external(void* ev, void* stream) {
 int spmoe_event_synchronize(void* ev) { return (int)cudaEventSynchronize((cudaEvent_t)ev); }
 
 }  // extern "C"
+
+extern "C" double spmoe_rt_since_epoch_ms(spmoe_rt* rt, void* event) {
+  if (!rt || !event) return -1.0;
+  float ms = -1.0f;
+  if (cudaEventElapsedTime(&ms, rt->epoch_, (cudaEvent_t)event) != cudaSuccess) return -1.0;
+  return ms;
+}

@@ -145,9 +145,9 @@ class SpecMoEEngine:
         if ffn_impl not in ("auto", "tcgen05", "cuda_core"):
             raise ValueError("ffn_impl must be auto | tcgen05 | cuda_core")
         self.ffn_impl = ffn_impl
-        self.num_sms = torch.cuda.get_device_properties(device if device is not None else 0).multi_processor_count
         if not torch.cuda.is_available():
             raise RuntimeError("SpecMoEEngine needs a CUDA device (there is no CPU fallback)")
+        self.num_sms = torch.cuda.get_device_properties(device if device is not None else 0).multi_processor_count
         self.arch = arch
         self.model = model_spec_for(arch)
         self.hw, self.timings, self.policy = hw, timings, policy
@@ -231,6 +231,7 @@ class SpecMoEEngine:
         self.stalls: list[_Stall] = []
         self.iter_records: list[IterationRecord] = []
         self.slots: list[ComputeSlot] = []
+        self._slot_events: list = []
         self.iter_events: list[tuple[torch.cuda.Event, torch.cuda.Event, torch.cuda.Event]] = []
         self.draft_ms = 0.0
         self.verify_ms = 0.0
@@ -610,7 +611,9 @@ class SpecMoEEngine:
         spmoe = self.cutoff is not None and self.policy.policy is Policy.DRAFT_PREFETCH
         width = self.predictor.width
         for d in range(N):
+            self._slot_begin()
             self._draft_graphs[d].replay()
+            self._slot_end("draft", P[0] - 1 + d, -1)
             if spmoe:
                 # tasks are pushed after the graph is enqueued, so the worker
                 # waits on this replay's event nodes (Algorithm 1 l.8-9)
@@ -626,12 +629,27 @@ class SpecMoEEngine:
         vtok = torch.cat([self._g_tok0[:, 1:2], draft_tok.long()], dim=1)
         self._vx.copy_(self._embed(vtok).view(B * T, H))
         for l in range(L):
+            self._slot_begin()
             self._gating_waits(l)
             self._verify_graphs[l].replay()
             self._moe_verify(l, self._vxn, self._vx, self.scratch, routed=self._vroute[l])
+            self._slot_end("verify", P[0] - 1, l)
         hn = rms_norm(self._vx.view(B, T, H), self.weights.final_norm, a.rms_eps)
         logits = torch.matmul(hn, self.weights.lm_head.t()).float()
         return logits, draft_tok
+
+    def _slot_begin(self) -> None:
+        if self.record_timeline:
+            self._slot_ev = torch.cuda.Event(enable_timing=True)
+            self._slot_ev.record(self.stream)
+
+    def _slot_end(self, kind: str, token: int, layer: int) -> None:
+        """ComputeSlot timeline (simcore.py:69-76): one slot per draft step
+        (layer -1 = the whole captured step) and per verify layer."""
+        if self.record_timeline:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(self.stream)
+            self._slot_events.append((kind, len(self.iter_records), token, layer, self._slot_ev, e))
 
     def _gating_waits(self, l: int) -> None:
         if not self._pending_gating:
@@ -849,6 +867,11 @@ class SpecMoEEngine:
             IterationRecord(r.index, it[0] / 1e3, it[1] / 1e3, it[2] / 1e3, r.position, r.drafted, r.accepted, r.emitted)
             for r, it in zip(self.iter_records, ts["iters"])
         ]
+        # compute slots on the same clock as the transfer log (runtime epoch)
+        slots = [
+            ComputeSlot(kind, it, tok, layer, self.cache.since_epoch_ms(ea) / 1e3, self.cache.since_epoch_ms(eb) / 1e3)
+            for kind, it, tok, layer, ea, eb in self._slot_events
+        ]
         n_emit = self.emitted_total
         extras = {
             "batch": self.batch,
@@ -882,7 +905,7 @@ class SpecMoEEngine:
             cache_capacity=self.capacity,
             iterations=iters,
             transfers=transfers,
-            compute_slots=self.slots,
+            compute_slots=slots,
             counters=counters,
             extras=extras,
         )

@@ -288,3 +288,30 @@ def test_engine_trace_export_and_measured_timings(tmp_path):
         assert t.t_comp_draft > 0 and t.t_comp_target > 0 and t.t_io_expert > 0
     finally:
         eng.close()
+
+
+def test_engine_timeline_csvs(tmp_path):
+    """§8(f) row 3: SimReport CSV, transfers.csv and compute_slots.csv in the
+    reference schema (report.py:22-23) from a real run, on one clock."""
+    from paper_2510_10302_b200.report import (
+        SLOTS_HEADER, TRANSFERS_HEADER, SimReport, write_compute_slots_csv, write_report_csv, write_transfer_log_csv)
+
+    eng = make_engine(record=False, capture=(), record_timeline=True)
+    try:
+        eng.prefill(prompts(1))
+        for _ in range(3):
+            eng.step()
+        rep = eng.report()
+        L = eng.arch.num_layers
+        assert sum(1 for s in rep.compute_slots if s.kind == "verify") == 3 * L
+        assert sum(1 for s in rep.compute_slots if s.kind == "draft") == 3 * eng.policy.draft_length
+        assert all(s.end >= s.start >= 0 for s in rep.compute_slots)
+        write_compute_slots_csv(rep, tmp_path / "slots.csv")
+        write_transfer_log_csv(rep, tmp_path / "transfers.csv")
+        write_report_csv([rep], tmp_path / "report.csv")
+        assert (tmp_path / "slots.csv").read_text().splitlines()[0] == SLOTS_HEADER
+        assert (tmp_path / "transfers.csv").read_text().splitlines()[0] == TRANSFERS_HEADER
+        rows = (tmp_path / "report.csv").read_text().splitlines()
+        assert rows[0] == SimReport.csv_header() and len(rows) == 2
+    finally:
+        eng.close()
