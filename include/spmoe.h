@@ -148,6 +148,19 @@ int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, const int32_t*
                         uint16_t* h_scratch, float* y, float* workspace, int split_up, int split_dn,
                         void* stream);
 
+/*
+ * Single-launch variant: up phase, grid-wide barrier, down phase in one
+ * persistent cooperative kernel (one CTA per SM); the TMA producer streams
+ * the first W2 stages before the barrier.  grid_sync: caller-owned device
+ * uint32 (reset by the call).  Up phase unsplit; workspace holds the
+ * split_dn down partials (split_dn * T*k * H floats) when split_dn > 1.
+ */
+int spmoe_expert_ffn_tc_fused(const uint16_t* pool, int64_t slot_elems, const int32_t* slot_of_expert,
+                              uint64_t expert_mask, const uint16_t* x, int T, int H, int F, int E, int k,
+                              const int32_t* expert_offsets, const int32_t* perm_token, uint16_t* x_perm,
+                              uint16_t* h_scratch, float* y, float* workspace, int split_dn,
+                              uint32_t* grid_sync, void* stream);
+
 /* --------------------------------------------------------------------- */
 /* K4  moe_combine                                                        */
 /*   Eq. 1 weighted sum Output = sum_i G(x)_i E_i(x)  */

@@ -339,6 +339,216 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__
   }
 }
 
+// ------------------------------------------------------------------ fused
+// One persistent cooperative launch for both phases of one K3 call: every
+// CTA walks its up tiles, its epilogue signals a grid-wide counter once its
+// last h store is visible, and the down phase starts; the TMA producer
+// issues the W2 (A operand) loads of its first STAGES down stages before
+// waiting for the counter (weights do not depend on h), so the barrier and
+// the W2 ramp overlap the up phase's tail.
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+ffn_tc_fused_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_constant__ CUtensorMap map_x,
+                    const __grid_constant__ CUtensorMap map_wd, const __grid_constant__ CUtensorMap map_h,
+                    const Params p, uint32_t* grid_sync) {
+  constexpr int A_BYTES = BM * BK * 2;
+  constexpr int B_BYTES = BN * BK * 2;
+  constexpr int STAGE_BYTES = 2 * A_BYTES + B_BYTES;  // sized for the up phase
+  constexpr int UP_TX = 2 * A_BYTES + B_BYTES;
+  constexpr int DN_TX = A_BYTES + B_BYTES;
+  constexpr int ACC_COLS = 2 * BN;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ TileList tl_up, tl_dn;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb_up = p.H / BK, kb_dn = p.F / BK;
+  const int mt_up = p.F / BM, mt_dn = p.H / BM;
+  const int split = p.split;
+
+  build_tiles(p, mt_up, 1, &tl_up);
+  build_tiles(p, mt_dn, split, &tl_dn);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+  const int n_up = tl_up.start[tl_up.n_active];
+  const int n_dn = tl_dn.start[tl_dn.n_active];
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < n_up; tile += gridDim.x) {
+        const Tile t = decode(p, tl_up, tile, mt_up, 1, kb_up);
+        const int slot = p.slot[t.e];
+        const int arow = p.offsets[t.e] + t.n0;
+        for (int kb = t.kb0; kb < t.kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* st = smem + stage * STAGE_BYTES;
+          mbar_expect_tx(&full_bar[stage], UP_TX);
+          tma_load_3d(st, &map_wu, &full_bar[stage], kb * BK, t.m0, slot);
+          tma_load_3d(st + A_BYTES, &map_wu, &full_bar[stage], kb * BK, p.F + t.m0, slot);
+          tma_load_2d(st + 2 * A_BYTES, &map_x, &full_bar[stage], kb * BK, arow);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+      // down phase: W2 loads run ahead of the grid barrier for up to STAGES
+      // stages; their h loads are issued once every up tile is stored
+      int pend_stage[STAGES], pend_kb[STAGES], pend_row[STAGES];
+      int npend = 0;
+      bool synced = false;
+      for (int tile = blockIdx.x; tile < n_dn; tile += gridDim.x) {
+        const Tile t = decode(p, tl_dn, tile, mt_dn, split, kb_dn);
+        const int slot = p.slot[t.e];
+        const int arow = p.offsets[t.e] + t.n0;
+        for (int kb = t.kb0; kb < t.kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* st = smem + stage * STAGE_BYTES;
+          mbar_expect_tx(&full_bar[stage], DN_TX);
+          tma_load_3d(st, &map_wd, &full_bar[stage], kb * BK, t.m0, slot);
+          if (synced) {
+            tma_load_2d(st + A_BYTES, &map_h, &full_bar[stage], kb * BK, arow);
+          } else {
+            pend_stage[npend] = stage;
+            pend_kb[npend] = kb;
+            pend_row[npend] = arow;
+            if (++npend == STAGES) {
+              while (ld_acquire_u32(grid_sync) < gridDim.x) __nanosleep(64);
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+              for (int i = 0; i < npend; ++i)
+                tma_load_2d(smem + pend_stage[i] * STAGE_BYTES + A_BYTES, &map_h, &full_bar[pend_stage[i]],
+                            pend_kb[i] * BK, pend_row[i]);
+              npend = 0;
+              synced = true;
+            }
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+      if (!synced && npend > 0) {
+        while (ld_acquire_u32(grid_sync) < gridDim.x) __nanosleep(64);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        for (int i = 0; i < npend; ++i)
+          tma_load_2d(smem + pend_stage[i] * STAGE_BYTES + A_BYTES, &map_h, &full_bar[pend_stage[i]],
+                      pend_kb[i] * BK, pend_row[i]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (int ph = 0; ph < 2; ++ph) {
+        const bool up = ph == 0;
+        const int ntile = up ? n_up : n_dn;
+        for (int tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+          const Tile t = up ? decode(p, tl_up, tile, mt_up, 1, kb_up) : decode(p, tl_dn, tile, mt_dn, split, kb_dn);
+          const uint32_t idesc = instr_desc(((t.ntok + 15) / 16) * 16);
+          mbar_wait(&tempty_bar[acc], aphase ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem_base + acc * ACC_COLS;
+          for (int kb = t.kb0; kb < t.kb1; ++kb) {
+            mbar_wait(&full_bar[stage], phase);
+            tc_fence_after();
+            uint8_t* st = smem + stage * STAGE_BYTES;
+            const uint64_t a0 = smem_desc_sw128(st);
+            const uint64_t a1 = smem_desc_sw128(st + A_BYTES);
+            const uint64_t b0 = smem_desc_sw128(st + (up ? 2 * A_BYTES : A_BYTES));
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint32_t accum = (kb > t.kb0 || k > 0) ? 1u : 0u;
+              umma(d, a0 + 2 * k, b0 + 2 * k, idesc, accum);
+              if (up) umma(d + BN, a1 + 2 * k, b0 + 2 * k, idesc, accum);
+            }
+            umma_commit(&empty_bar[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          umma_commit(&tfull_bar[acc]);
+          if (++acc == 2) { acc = 0; aphase ^= 1; }
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int ph = 0; ph < 2; ++ph) {
+      const bool up = ph == 0;
+      const int ntile = up ? n_up : n_dn;
+      for (int tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+        const Tile t = up ? decode(p, tl_up, tile, mt_up, 1, kb_up) : decode(p, tl_dn, tile, mt_dn, split, kb_dn);
+        mbar_wait(&tfull_bar[acc], aphase);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + acc * ACC_COLS;
+        const int row = t.m0 + 32 * q + lane;
+        const int64_t prow = p.offsets[t.e] + t.n0;
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          if (c0 < t.ntok) {
+            float g[16], u[16];
+            tmem_ld16(taddr + c0, g);
+            if (up) tmem_ld16(taddr + BN + c0, u);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              if (c0 + c < t.ntok) {
+                if (up) {
+                  p.h_out[(prow + c0 + c) * p.F + row] = f32_to_bf16(__fmul_rn(det_silu(g[c]), u[c]));
+                } else {
+                  p.y_part[((int64_t)t.ks * p.rows + prow + c0 + c) * p.H + row] = g[c];
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty_bar[acc]);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+      }
+      if (up) {
+        // every h store of this CTA is done: publish to the grid (release +
+        // generic->async proxy fence for the TMA readers in other CTAs)
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 64) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          atomicAdd(grid_sync, 1u);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+  }
+}
+
 // y[r, :] = sum_s y_part[s][r, :] in split order (deterministic), only for
 // rows of experts in this launch's mask (other rows keep their values).
 __global__ void reduce_split_kernel(const float* __restrict__ part, int split, int rows, int H,
@@ -503,6 +713,77 @@ extern "C" int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, con
   p.split = split_dn;
   p.y_part = split_dn > 1 ? workspace : y;
   st = launch<false, 8>(mw_dn, ma_dn, p, nsms, s);
+  if (st) return st;
+  if (split_dn > 1) {
+    reduce_split_kernel<<<nsms * 4, 256, 0, s>>>(workspace, split_dn, rows, H, expert_offsets, E, expert_mask, y);
+    st = (int)cudaGetLastError();
+  }
+  return st;
+}
+
+extern "C" int spmoe_expert_ffn_tc_fused(const uint16_t* pool, int64_t slot_elems, const int32_t* slot_of_expert,
+                                         uint64_t expert_mask, const uint16_t* x, int T, int H, int F, int E,
+                                         int k, const int32_t* expert_offsets, const int32_t* perm_token,
+                                         uint16_t* x_perm, uint16_t* h_scratch, float* y, float* workspace,
+                                         int split_dn, uint32_t* grid_sync, void* stream) {
+  using namespace tc;
+  if (!pool || !slot_of_expert || !expert_offsets || !grid_sync || T < 0 || E < 1 || E > kMaxExperts || k < 1)
+    return (int)cudaErrorInvalidValue;
+  if (H % BM || F % BM || split_dn < 1 || split_dn > F / BK) return (int)cudaErrorInvalidValue;
+  if (T == 0 || expert_mask == 0) return 0;
+  if (!x || !perm_token || !x_perm || !h_scratch || !y || (split_dn > 1 && !workspace))
+    return (int)cudaErrorInvalidValue;
+  cudaStream_t s = (cudaStream_t)stream;
+  int dev = 0, nsms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsms, cudaDevAttrMultiProcessorCount, dev);
+  const int rows = T * k;
+  Params p{};
+  p.mask = expert_mask;
+  p.offsets = expert_offsets;
+  p.h_out = h_scratch;
+  p.y_part = split_dn > 1 ? workspace : y;
+  p.E = E;
+  p.H = H;
+  p.F = F;
+  p.rows = rows;
+  p.split = split_dn;
+  int max_slot = 0;
+  for (int e = 0; e < E; ++e) {
+    p.slot[e] = ((expert_mask >> e) & 1ull) ? slot_of_expert[e] : 0;
+    if (p.slot[e] > max_slot) max_slot = p.slot[e];
+  }
+  gather_rows_kernel<<<nsms, 256, 0, s>>>(x, perm_token, expert_offsets, E, H, x_perm);
+  int st = (int)cudaGetLastError();
+  if (st) return st;
+  st = (int)cudaMemsetAsync(grid_sync, 0, sizeof(uint32_t), s);
+  if (st) return st;
+  CUtensorMap mwu, mx, mwd, mh;
+  const uint64_t sb = (uint64_t)slot_elems * 2;
+  {
+    const uint64_t d[3] = {(uint64_t)H, (uint64_t)2 * F, (uint64_t)max_slot + 1};
+    const uint64_t str[2] = {(uint64_t)H * 2, sb};
+    if (!make_map(&mwu, pool, 3, d, str, BM)) return (int)cudaErrorInvalidValue;
+    const uint64_t da[2] = {(uint64_t)H, (uint64_t)rows};
+    const uint64_t sa[1] = {(uint64_t)H * 2};
+    if (!make_map(&mx, x_perm, 2, da, sa, BN)) return (int)cudaErrorInvalidValue;
+    const uint64_t d2[3] = {(uint64_t)F, (uint64_t)H, (uint64_t)max_slot + 1};
+    const uint64_t str2[2] = {(uint64_t)F * 2, sb};
+    if (!make_map(&mwd, pool + (int64_t)2 * F * H, 3, d2, str2, BM)) return (int)cudaErrorInvalidValue;
+    const uint64_t dh[2] = {(uint64_t)F, (uint64_t)rows};
+    const uint64_t sh[1] = {(uint64_t)F * 2};
+    if (!make_map(&mh, h_scratch, 2, dh, sh, BN)) return (int)cudaErrorInvalidValue;
+  }
+  constexpr int STAGES = 5;
+  const size_t smem = (size_t)STAGES * (2 * BM * BK * 2 + BN * BK * 2) + 1024;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(ffn_tc_fused_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  void* args[] = {(void*)&mwu, (void*)&mx, (void*)&mwd, (void*)&mh, (void*)&p, (void*)&grid_sync};
+  st = (int)cudaLaunchCooperativeKernel((const void*)ffn_tc_fused_kernel<STAGES>, dim3(nsms), dim3(kThreads), args,
+                                        smem, s);
   if (st) return st;
   if (split_dn > 1) {
     reduce_split_kernel<<<nsms * 4, 256, 0, s>>>(workspace, split_dn, rows, H, expert_offsets, E, expert_mask, y);

@@ -296,6 +296,58 @@ def expert_ffn_tc(
     )
 
 
+def expert_ffn_tc_fused(
+    pool: torch.Tensor,
+    slot_of_expert: Sequence[int],
+    expert_mask: int,
+    x: torch.Tensor,
+    ffn_dim: int,
+    top_k: int,
+    offsets: torch.Tensor,
+    perm: torch.Tensor,
+    x_perm: torch.Tensor,
+    h_scratch: torch.Tensor,
+    y: torch.Tensor,
+    workspace: torch.Tensor | None,
+    split_dn: int,
+    grid_sync: torch.Tensor,
+    stream=None,
+) -> None:
+    """Single cooperative launch of both tcgen05 phases (grid barrier between
+    them); ``grid_sync`` is a 1-element int32 device tensor."""
+    _need(pool, BF16, "pool", 2)
+    _need(x, BF16, "x", 2)
+    T, H = x.shape
+    E = len(slot_of_expert)
+    if split_dn > 1:
+        need = split_dn * T * top_k * H
+        if workspace is None or workspace.numel() < need:
+            raise ValueError(f"tcgen05 workspace needs {need} floats")
+    LAUNCHES["count"] += 2 + (split_dn > 1)
+    _native.call(
+        "spmoe_expert_ffn_tc_fused",
+        pool.data_ptr(),
+        pool.shape[1],
+        _slot_array(slot_of_expert, E),
+        expert_mask,
+        x.data_ptr(),
+        T,
+        H,
+        ffn_dim,
+        E,
+        top_k,
+        offsets.data_ptr(),
+        perm.data_ptr(),
+        x_perm.data_ptr(),
+        h_scratch.data_ptr(),
+        y.data_ptr(),
+        _ptr(workspace),
+        split_dn,
+        grid_sync.data_ptr(),
+        _stream(stream),
+    )
+
+
 # ---------------------------------------------------------------------------
 # K4
 # ---------------------------------------------------------------------------

@@ -27,6 +27,7 @@ CASES = {
     "deepseek_T5": dict(H=2048, F=1408, E=64, k=6, T=5),
     "qwen_T5": dict(H=2048, F=1408, E=60, k=4, T=5),
     "qwen_T72": dict(H=2048, F=1408, E=60, k=4, T=72),
+    "mixtral_1exp": dict(H=4096, F=14336, E=1, k=1, T=2),
 }
 
 
@@ -57,7 +58,12 @@ def run_case(name, H, F, E, k, T, iters=20, warmup=5):
     su, sd = K.tc_plan(np.bincount(ids, minlength=E), H, F)
     ws = torch.empty((max(1, K.tc_workspace_floats(T * k, H, F, su, sd)),), dtype=torch.float32, device=dev)
 
+    sync = torch.zeros((1,), dtype=torch.int32, device=dev)
+
     def once(i, phase="both"):
+        if phase == "tcf":
+            K.expert_ffn_tc_fused(pools[i % R], slots, mask, x, F, k, off, perm, xp, h, y, ws, sd, sync)
+            return
         if phase == "tc":
             K.expert_ffn_tc(pools[i % R], slots, mask, x, F, k, off, perm, xp, h, y, ws, su, sd)
             return
@@ -66,7 +72,7 @@ def run_case(name, H, F, E, k, T, iters=20, warmup=5):
     for i in range(warmup):
         once(i)
     res = {}
-    for phase in ("both", "up", "down", "tc"):
+    for phase in ("both", "up", "down", "tc", "tcf"):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
         torch.cuda.synchronize()
         for i in range(iters):
@@ -75,7 +81,7 @@ def run_case(name, H, F, E, k, T, iters=20, warmup=5):
             evs[i][1].record(st)
         torch.cuda.synchronize()
         ms = float(np.median([a.elapsed_time(b) for a, b in evs]))
-        wbytes = {"both": 3, "up": 2, "down": 1, "tc": 3}[phase] * F * H * 2 * U
+        wbytes = {"both": 3, "up": 2, "down": 1, "tc": 3, "tcf": 3}[phase] * F * H * 2 * U
         act = T * k * (H * 2 + F * 2 * 2 + H * 4)
         res[phase] = {"ms": ms, "GBps": (wbytes + act) / (ms / 1e3) / 1e9, "weight_bytes": wbytes}
     # router latency
