@@ -28,14 +28,14 @@ from paper_2510_10302_b200.model import get_arch  # noqa: E402
 
 
 def point(arch, hw, state, *, N=4, batch=1, budget=0.25, cutoff=None, policy="draft_prefetch", steps=6, warmup=2,
-          window=True):
+          window=True, ffn_impl="cuda_core"):
     E_all = arch.num_layers * arch.num_experts
     cap = max(arch.num_experts, int(round(budget * E_all)))
     pk = 1 if arch.num_experts <= 16 else arch.top_k
     pol = PolicySpec(policy=Policy(policy), prefetch_k=pk, draft_length=N, acceptance_rate=1.0, seed=1234,
                      cutoff_layer=cutoff, cache_capacity_experts=cap)
     eng = SpecMoEEngine(arch, hw, b200_timings(arch, hw), pol, batch=batch, max_tokens=64 + (steps + warmup + 2) * (N + 1),
-                        window_tokens=N if window else 1, model_state=state)
+                        window_tokens=N if window else 1, model_state=state, ffn_impl=ffn_impl)
     try:
         g = torch.Generator().manual_seed(1000)
         eng.prefill(torch.randint(0, arch.vocab, (batch, 64), generator=g))
@@ -56,6 +56,8 @@ def point(arch, hw, state, *, N=4, batch=1, budget=0.25, cutoff=None, policy="dr
             "hidden_prefetch_fraction": ex["hidden_prefetch_fraction"], "h2d_gbs": ex["h2d_gbs"],
             "breakdown": rep.latency_breakdown, "prefetch_insertions": rep.counters["prefetch_insertions"],
             "demand_insertions": rep.counters["demand_insertions"],
+            "ms_per_iteration": rep.total_time * 1e3 / max(1, len(rep.iterations)),
+            "ffn_impl": ffn_impl,
         }
     finally:
         eng.close()
@@ -66,6 +68,10 @@ def main():
     ap.add_argument("which", choices=["deepseek", "qwen", "mixtral"])
     ap.add_argument("--out", default="profiles/sweeps_r1.jsonl")
     ap.add_argument("--steps", type=int, default=6)
+    # the bit-exact CUDA-core K3 gives every policy point the same token
+    # stream (its per-expert results do not depend on how experts are grouped
+    # into launches); tcgen05 split choices do, which perturbs acceptance
+    ap.add_argument("--ffn-impl", default="cuda_core")
     a = ap.parse_args()
     name = {"deepseek": "deepseek_v2_lite", "qwen": "qwen15_moe_a27b", "mixtral": "mixtral_8x7b"}[a.which]
     arch = get_arch(name)
@@ -101,7 +107,7 @@ def main():
             pts.append(dict(cutoff=c))
     with open(a.out, "a") as f:
         for kw in pts:
-            r = point(arch, hw, state, steps=a.steps, **kw)
+            r = point(arch, hw, state, steps=a.steps, ffn_impl=a.ffn_impl, **kw)
             r["sweep"] = a.which
             r["point"] = kw
             print(json.dumps(r), flush=True)
