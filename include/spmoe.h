@@ -161,6 +161,12 @@ int spmoe_expert_ffn_tc_fused(const uint16_t* pool, int64_t slot_elems, const in
                               uint16_t* h_scratch, float* y, float* workspace, int split_dn,
                               uint32_t* grid_sync, void* stream);
 
+/* Profiling hook: CUDA events (cudaEvent_t, timing-enabled) recorded on the
+ * stream right before the first kernel and after the last kernel of the
+ * NEXT spmoe_expert_ffn / _tc / _tc_fused call made by this host thread, so
+ * the measured span excludes host-side launch preparation.  NULLs clear. */
+int spmoe_k3_timing(void* start, void* end);
+
 /* --------------------------------------------------------------------- */
 /* K4  moe_combine                                                        */
 /*   Eq. 1 weighted sum Output = sum_i G(x)_i E_i(x)  */

@@ -12,6 +12,21 @@
 
 namespace spmoe {
 
+// Optional CUDA events for the next K3 call on this host thread: recorded
+// right before its first kernel and after its last (spmoe_k3_timing), so a
+// measured duration excludes host-side launch preparation.
+struct K3Timing {
+  cudaEvent_t start = nullptr, end = nullptr;
+};
+K3Timing& k3_timing();
+inline void k3_timing_begin(cudaStream_t s) {
+  if (k3_timing().start) cudaEventRecord(k3_timing().start, s);
+}
+inline void k3_timing_end(cudaStream_t s) {
+  if (k3_timing().end) cudaEventRecord(k3_timing().end, s);
+  k3_timing() = K3Timing{};
+}
+
 // bf16 -> f32 for the low / high half of a packed 32-bit word (exact).
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }

@@ -497,6 +497,11 @@ __global__ void fill_normal_kernel(uint16_t* __restrict__ dst, int64_t n, uint64
 
 }  // namespace
 
+K3Timing& spmoe::k3_timing() {
+  static thread_local K3Timing t;
+  return t;
+}
+
 // ===========================================================================
 // C ABI
 // ===========================================================================
@@ -572,12 +577,23 @@ int spmoe_expert_ffn(const uint16_t* pool, int64_t slot_elems, const int32_t* sl
                      uint64_t expert_mask, const uint16_t* x, int T, int H, int F, int E, int k,
                      const int32_t* expert_offsets, const int32_t* perm_token,
                      uint16_t* h_scratch, float* y, int max_tokens_per_expert, void* stream) {
+  const K3Timing tm = k3_timing();
+  k3_timing() = K3Timing{};
+  if (tm.start) cudaEventRecord(tm.start, (cudaStream_t)stream);
   int st = spmoe_expert_ffn_up(pool, slot_elems, slot_of_expert, expert_mask, x, T, H, F, E, k,
                                expert_offsets, perm_token, h_scratch, max_tokens_per_expert,
                                stream);
   if (st) return st;
-  return spmoe_expert_ffn_down(pool, slot_elems, slot_of_expert, expert_mask, T, H, F, E, k,
-                               expert_offsets, h_scratch, y, max_tokens_per_expert, stream);
+  st = spmoe_expert_ffn_down(pool, slot_elems, slot_of_expert, expert_mask, T, H, F, E, k,
+                             expert_offsets, h_scratch, y, max_tokens_per_expert, stream);
+  if (tm.end) cudaEventRecord(tm.end, (cudaStream_t)stream);
+  return st;
+}
+
+int spmoe_k3_timing(void* start, void* end) {
+  k3_timing().start = (cudaEvent_t)start;
+  k3_timing().end = (cudaEvent_t)end;
+  return 0;
 }
 
 int spmoe_moe_combine(const float* y, const int32_t* inv_pos, const float* weights, int T, int H,

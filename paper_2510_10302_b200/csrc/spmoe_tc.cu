@@ -680,9 +680,7 @@ extern "C" int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, con
     p.slot[e] = ((expert_mask >> e) & 1ull) ? slot_of_expert[e] : 0;
     if (p.slot[e] > max_slot) max_slot = p.slot[e];
   }
-  gather_rows_kernel<<<nsms, 256, 0, s>>>(x, perm_token, expert_offsets, E, H, x_perm);
-  int st = (int)cudaGetLastError();
-  if (st) return st;
+  int st = 0;
   CUtensorMap mw_up, ma_up, mw_dn, ma_dn;
   const uint64_t sb = (uint64_t)slot_elems * 2;
   {
@@ -701,6 +699,8 @@ extern "C" int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, con
     const uint64_t sa[1] = {(uint64_t)F * 2};
     if (!make_map(&ma_dn, h_scratch, 2, da, sa, BN)) return (int)cudaErrorInvalidValue;
   }
+  k3_timing_begin(s);
+  gather_rows_kernel<<<nsms, 256, 0, s>>>(x, perm_token, expert_offsets, E, H, x_perm);
   p.split = split_up;
   st = launch<true, 5>(mw_up, ma_up, p, nsms, s);
   if (st) return st;
@@ -718,6 +718,7 @@ extern "C" int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, con
     reduce_split_kernel<<<nsms * 4, 256, 0, s>>>(workspace, split_dn, rows, H, expert_offsets, E, expert_mask, y);
     st = (int)cudaGetLastError();
   }
+  k3_timing_end(s);
   return st;
 }
 
@@ -753,11 +754,7 @@ extern "C" int spmoe_expert_ffn_tc_fused(const uint16_t* pool, int64_t slot_elem
     p.slot[e] = ((expert_mask >> e) & 1ull) ? slot_of_expert[e] : 0;
     if (p.slot[e] > max_slot) max_slot = p.slot[e];
   }
-  gather_rows_kernel<<<nsms, 256, 0, s>>>(x, perm_token, expert_offsets, E, H, x_perm);
-  int st = (int)cudaGetLastError();
-  if (st) return st;
-  st = (int)cudaMemsetAsync(grid_sync, 0, sizeof(uint32_t), s);
-  if (st) return st;
+  int st = 0;
   CUtensorMap mwu, mx, mwd, mh;
   const uint64_t sb = (uint64_t)slot_elems * 2;
   {
@@ -782,6 +779,10 @@ extern "C" int spmoe_expert_ffn_tc_fused(const uint16_t* pool, int64_t slot_elem
     configured = true;
   }
   void* args[] = {(void*)&mwu, (void*)&mx, (void*)&mwd, (void*)&mh, (void*)&p, (void*)&grid_sync};
+  k3_timing_begin(s);
+  gather_rows_kernel<<<nsms, 256, 0, s>>>(x, perm_token, expert_offsets, E, H, x_perm);
+  st = (int)cudaMemsetAsync(grid_sync, 0, sizeof(uint32_t), s);
+  if (st) return st;
   st = (int)cudaLaunchCooperativeKernel((const void*)ffn_tc_fused_kernel<STAGES>, dim3(nsms), dim3(kThreads), args,
                                         smem, s);
   if (st) return st;
@@ -789,5 +790,6 @@ extern "C" int spmoe_expert_ffn_tc_fused(const uint16_t* pool, int64_t slot_elem
     reduce_split_kernel<<<nsms * 4, 256, 0, s>>>(workspace, split_dn, rows, H, expert_offsets, E, expert_mask, y);
     st = (int)cudaGetLastError();
   }
+  k3_timing_end(s);
   return st;
 }

@@ -337,9 +337,12 @@ class SpecMoEEngine:
             self._ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok, s, cnt)
             return
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ea.record()
-        self._ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok, s, cnt)
+        ea.record()  # creates the events; the launcher re-records them
         eb.record()
+        # the C launcher records ea right before its first kernel and eb after
+        # its last, so host-side launch preparation is not counted
+        self._lib.spmoe_k3_timing(ea.cuda_event, eb.cuda_event)
+        self._ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok, s, cnt)
         rows = int(sum(int(counts[e]) for e in experts))
         act = rows * (a.hidden * 2 + 2 * a.ffn * 2 + a.hidden * 4)  # x in, h out+in, y out
         self.k3_events.append((ea, eb, len(experts) * a.expert_bytes + act, len(experts), rows))

@@ -170,7 +170,15 @@ def expert_ffn(
         raise ValueError("slot too small for the expert blob")
     slots = _slot_array(slot_of_expert, E)
     st = _stream(stream)
-    if phase in ("both", "up"):
+    if phase == "both":
+        LAUNCHES["count"] += 2
+        _native.call(
+            "spmoe_expert_ffn", pool.data_ptr(), slot_elems, slots, expert_mask, x.data_ptr(), T, H, ffn_dim, E,
+            top_k, offsets.data_ptr(), perm.data_ptr(), h_scratch.data_ptr(), y.data_ptr(),
+            max_tokens_per_expert, st,
+        )
+        return
+    if phase == "up":
         LAUNCHES["count"] += 1
         _native.call(
             "spmoe_expert_ffn_up",
@@ -190,7 +198,7 @@ def expert_ffn(
             max_tokens_per_expert,
             st,
         )
-    if phase in ("both", "down"):
+    if phase == "down":
         LAUNCHES["count"] += 1
         _native.call(
             "spmoe_expert_ffn_down",
