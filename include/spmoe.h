@@ -184,6 +184,17 @@ int spmoe_moe_combine(const float* y, const int32_t* inv_pos, const float* weigh
                       const uint16_t* residual, uint16_t* out, void* stream);
 
 /* --------------------------------------------------------------------- */
+/* gather_rows  (expert-parallel exchange, SURVEY §8 e)                   */
+/*   dst[j] = src[idx[j] / div] for j < n, rows of row_bytes (multiple of */
+/*   4).  Packs routed rows in K2's expert order before the dispatch     */
+/*   all-to-all (div = k, idx = perm_token) and restores receive order   */
+/*   before the combine all-to-all (div = 1, idx = inv_pos).  No         */
+/*   reference counterpart: the reference has no expert parallelism.     */
+/* --------------------------------------------------------------------- */
+int spmoe_gather_rows(const void* src, const int32_t* idx, int n, int div, int64_t row_bytes,
+                      void* dst, void* stream);
+
+/* --------------------------------------------------------------------- */
 /* K6  greedy_accept                                                      */
 /*   replaces the Bernoulli acceptance of Simulation.run                  */
 /*   (simcore.py:440-446) with the SD greedy rule:      */

@@ -46,6 +46,7 @@ SIGNATURES: dict[str, tuple] = {
     "spmoe_expert_ffn_tc_fused": (_i, [_p, _i64, _p, _u64, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _i, _p, _p]),
     "spmoe_k3_timing": (_i, [_p, _p]),
     "spmoe_moe_combine": (_i, [_p, _p, _p, _i, _i, _i, _p, _p, _p, _p, _p]),
+    "spmoe_gather_rows": (_i, [_p, _p, _i, _i, _i64, _p, _p]),
     "spmoe_greedy_accept": (_i, [_p, _i64, _p, _i, _i, _i, _p, _p, _p]),
     "spmoe_argmax_rows": (_i, [_p, _i64, _i, _i, _p, _p]),
     "spmoe_h2d_batch": (_i, [_p, _p, _p, _i, _p]),

@@ -495,6 +495,22 @@ __global__ void fill_normal_kernel(uint16_t* __restrict__ dst, int64_t n, uint64
   }
 }
 
+// ---------------------------------------------------------------------------
+// Row gather for the expert-parallel exchange: dst[j] = src[idx[j] / div].
+// W = 16-byte words when rows allow it, else 4-byte words; one CTA per row
+// batch, consecutive threads on consecutive words (coalesced).
+// ---------------------------------------------------------------------------
+template <typename W>
+__global__ void gather_rows_kernel(const W* __restrict__ src, const int32_t* __restrict__ idx, int n,
+                                   int div, int64_t words, W* __restrict__ dst) {
+  for (int j = blockIdx.x; j < n; j += gridDim.x) {
+    const int64_t r = idx[j] / div;
+    const W* s = src + r * words;
+    W* d = dst + (int64_t)j * words;
+    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) d[w] = s[w];
+  }
+}
+
 }  // namespace
 
 K3Timing& spmoe::k3_timing() {
@@ -588,6 +604,23 @@ int spmoe_expert_ffn(const uint16_t* pool, int64_t slot_elems, const int32_t* sl
                              expert_offsets, h_scratch, y, max_tokens_per_expert, stream);
   if (tm.end) cudaEventRecord(tm.end, (cudaStream_t)stream);
   return st;
+}
+
+int spmoe_gather_rows(const void* src, const int32_t* idx, int n, int div, int64_t row_bytes,
+                      void* dst, void* stream) {
+  if (n < 0 || div < 1 || row_bytes <= 0 || (row_bytes & 3)) return (int)cudaErrorInvalidValue;
+  if (n == 0) return 0;
+  if (!src || !idx || !dst) return (int)cudaErrorInvalidValue;
+  const int grid = n < 4 * num_sms() ? n : 4 * num_sms();
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool vec = !(row_bytes & 15) && !((uintptr_t)src & 15) && !((uintptr_t)dst & 15);
+  if (vec)
+    gather_rows_kernel<uint4><<<grid, 256, 0, s>>>((const uint4*)src, idx, n, div, row_bytes / 16,
+                                                   (uint4*)dst);
+  else
+    gather_rows_kernel<uint32_t><<<grid, 256, 0, s>>>((const uint32_t*)src, idx, n, div,
+                                                      row_bytes / 4, (uint32_t*)dst);
+  return launch_status();
 }
 
 int spmoe_k3_timing(void* start, void* end) {

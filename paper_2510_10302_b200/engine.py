@@ -141,6 +141,8 @@ class SpecMoEEngine:
         capture_layers: tuple[int, ...] = (),
         cuda_graphs: bool = True,
         ffn_impl: str = "auto",
+        expert_parallel: bool = False,
+        ep_group=None,
     ):
         if ffn_impl not in ("auto", "tcgen05", "cuda_core"):
             raise ValueError("ffn_impl must be auto | tcgen05 | cuda_core")
@@ -155,12 +157,23 @@ class SpecMoEEngine:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.seed = policy.seed if seed is None else seed
         self.capacity = cache_capacity_slots(self.model, hw, policy)
-        if self.capacity < arch.num_experts:
+        # expert parallelism (ep.py): this rank computes only its own block of
+        # every layer's routed experts; its slot pool caches only those
+        self.ep = None
+        per_layer = arch.num_experts
+        if expert_parallel:
+            from .ep import ExpertParallelExchange
+
+            if policy.policy is not Policy.ON_DEMAND:
+                raise ValidationError("expert_parallel runs the on_demand policy (no cross-rank prefetch)")
+            self.ep = ExpertParallelExchange(arch.num_experts, arch.top_k, ep_group)
+            per_layer = len(self.ep.local_experts)
+        if self.capacity < per_layer:
             raise ValidationError(
-                f"cache capacity {self.capacity} is below experts_per_layer {arch.num_experts}; "
+                f"cache capacity {self.capacity} is below experts_per_layer {per_layer}; "
                 "a single layer could not be loaded"
             )
-        self.capacity = min(self.capacity, arch.num_layers * arch.num_experts)
+        self.capacity = min(self.capacity, arch.num_layers * per_layer)
         torch.cuda.set_device(self.device)
         if model_state is not None:
             # reuse another engine's pinned host pool and device weights
@@ -197,6 +210,7 @@ class SpecMoEEngine:
         T_max = max(batch * (N + 1), batch * 2, 1)
         self.scratch = _Scratch(arch, T_max, self.device)
         self.prefill_scratch: _Scratch | None = None
+        self.ep_scratch: _Scratch | None = None
         pk = policy.prefetch_k
         self.predictor = DraftGuidedPredictor(entries=max(N, 1) * arch.num_layers + 1, width=batch * pk)
         self.pred_w = torch.empty((batch, pk), dtype=torch.float32, device=self.device)
@@ -316,7 +330,8 @@ class SpecMoEEngine:
         of those experts (host-known), used to plan the tcgen05 split-K."""
         if self._use_tc(F, maxtok):
             rows = xn.shape[0] * k
-            su, sd = K.tc_plan(counts if counts is not None else [maxtok], self.arch.hidden, F, self.num_sms)
+            # launch-independent split: bits do not depend on launch grouping
+            su, sd = K.tc_plan_static(self.arch.hidden, F, self.num_sms)
             K.expert_ffn_tc(pool, slots, mask, xn, F, k, offsets, perm, s.xp[:rows], h, y, s.ysplit, su, sd)
         else:
             K.expert_ffn(pool, slots, mask, xn, F, k, offsets, perm, h, y, maxtok)
@@ -327,14 +342,15 @@ class SpecMoEEngine:
         self._ffn(blob, [0], 1, xn, F, 1, off, perm, s.hd, s.yd, T, s)
         return K.moe_combine(s.yd, perm, None, T, self.arch.hidden, 1, residual=resid, out=out)
 
-    def _timed_ffn(self, experts, counts, slots, mask, xn, offsets, perm, s, maxtok) -> None:
+    def _timed_ffn(self, experts, counts, slots, mask, xn, offsets, perm, s, maxtok, k=None) -> None:
         """K3 over ``experts``; with ``time_k3`` set, brackets the launch pair
         with CUDA events and books its algorithmic bytes (weights of every
         expert in the mask read once + activations in/out) for the roofline."""
         a = self.arch
+        k = a.top_k if k is None else k
         cnt = [int(counts[e]) for e in experts]
         if not self.time_k3:
-            self._ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok, s, cnt)
+            self._ffn(self.pool, slots, mask, xn, a.ffn, k, offsets, perm, s.h, s.y, maxtok, s, cnt)
             return
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ea.record()  # creates the events; the launcher re-records them
@@ -342,7 +358,7 @@ class SpecMoEEngine:
         # the C launcher records ea right before its first kernel and eb after
         # its last, so host-side launch preparation is not counted
         self._lib.spmoe_k3_timing(ea.cuda_event, eb.cuda_event)
-        self._ffn(self.pool, slots, mask, xn, a.ffn, a.top_k, offsets, perm, s.h, s.y, maxtok, s, cnt)
+        self._ffn(self.pool, slots, mask, xn, a.ffn, k, offsets, perm, s.h, s.y, maxtok, s, cnt)
         rows = int(sum(int(counts[e]) for e in experts))
         act = rows * (a.hidden * 2 + 2 * a.ffn * 2 + a.hidden * 4)  # x in, h out+in, y out
         self.k3_events.append((ea, eb, len(experts) * a.expert_bytes + act, len(experts), rows))
@@ -400,7 +416,21 @@ class SpecMoEEngine:
             self.decisions.append(("verify", l, [int(v) for v in ids]))
         if self.record_routing:
             self._iter_logits.append(s.logits[:T].clone())
-        required = sorted(set(int(e) for e in ids))
+        if self.ep is not None:
+            return self._moe_verify_ep(l, xn, resid, s, w, idx, sg, ids)
+        offsets, perm, inv = K.moe_permute(idx, E, out=(s.offsets, s.perm[: T * k], s.inv[: T * k]))
+        counts = np.bincount(ids, minlength=E)
+        slots = self._run_experts(l, counts, xn, k, offsets, perm, s)
+        return self._shared_and_combine(l, xn, resid, s, w, idx, sg, s.y, inv, slots)
+
+    def _run_experts(self, l: int, counts: np.ndarray, x: torch.Tensor, k: int, offsets, perm, s: _Scratch) -> list:
+        """Cache decisions + K3 for the experts with ``counts > 0`` at layer l:
+        touch the union in ascending order, demand-load the misses behind
+        queued prefetches, run the resident experts first and each late
+        expert after its slot's ready event (§4.3), then record the
+        slots' read events.  Returns the slot of every expert (0 if unused)."""
+        E = self.arch.num_experts
+        required = [int(e) for e in np.nonzero(counts)[0]]
         stream_ptr = self.stream.cuda_stream
         hits, missing = [], []
         for e in required:
@@ -413,13 +443,11 @@ class SpecMoEEngine:
         if missing:
             for e, sl in zip(missing, self.cache.demand_load([ExpertId(l, e) for e in missing])):
                 slot[e] = sl
-        offsets, perm, inv = K.moe_permute(idx, E, out=(s.offsets, s.perm[: T * k], s.inv[: T * k]))
-        counts = np.bincount(ids, minlength=E)
         slots = [slot.get(e, 0) for e in range(E)]
         maxtok = int(counts.max()) if counts.size else 0
         if ready:
             mask = sum(1 << e for e in ready)
-            self._timed_ffn(ready, counts, slots, mask, xn, offsets, perm, s, maxtok)
+            self._timed_ffn(ready, counts, slots, mask, x, offsets, perm, s, maxtok, k)
         for kind, group in (("prefetch", late_prefetch), ("demand", missing)):
             for e in group:
                 ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -427,9 +455,15 @@ class SpecMoEEngine:
                 self.cache.wait_slot(slot[e], stream_ptr)
                 eb.record()
                 self.stalls.append(_Stall(kind, l, ea, eb))
-                self._timed_ffn([e], counts, slots, 1 << e, xn, offsets, perm, s, int(counts[e]))
+                self._timed_ffn([e], counts, slots, 1 << e, x, offsets, perm, s, int(counts[e]), k)
         for e in required:
             self.cache.mark_read(slot[e], stream_ptr)
+        return slots
+
+    def _shared_and_combine(self, l, xn, resid, s, w, idx, sg, y, inv, slots):
+        a = self.arch
+        lw = self.weights.layers[l]
+        T, H = xn.shape
         ys = None
         if lw.shared is not None:
             off, pm = s.dense(T)
@@ -438,11 +472,35 @@ class SpecMoEEngine:
         if l in self.capture_layers:
             cap = {"layer": l, "xn": xn.clone(), "resid": resid.clone(), "idx": idx.clone(), "w": w.clone(),
                    "slots": list(slots), "sg": None if sg is None else sg.clone()}
-        out = K.moe_combine(s.y, inv, w, T, H, k, residual=resid, y_shared=ys, shared_gate=sg, out=resid)
+        out = K.moe_combine(y, inv, w, T, H, a.top_k, residual=resid, y_shared=ys, shared_gate=sg, out=resid)
         if l in self.capture_layers:
             cap["out"] = out.clone()
             self.captures.append(cap)
         return out
+
+    def _moe_verify_ep(self, l, xn, resid, s, w, idx, sg, ids) -> torch.Tensor:
+        """Expert-parallel verify MoE (ep.py): dispatch routed rows to the
+        experts' owners, run this rank's experts on what it received, send the
+        outputs back, combine.  Every rank must call this for every layer."""
+        a = self.arch
+        T, H = xn.shape
+        k, E = a.top_k, a.num_experts
+        offsets, perm, inv = K.moe_permute(idx, E, out=(s.offsets, s.perm[: T * k], s.inv[: T * k]))
+        counts = np.bincount(ids, minlength=E)
+        x_recv, e_recv, e_host = self.ep.dispatch(xn, idx.view(-1), perm, counts)
+        R = x_recv.shape[0]
+        slots = [0] * E
+        if R:
+            if self.ep_scratch is None or self.ep_scratch.T < R:
+                self.ep_scratch = _Scratch(a, max(R, self.ep.world * self.scratch.T), self.device)
+            es = self.ep_scratch
+            off2, perm2, inv2 = K.moe_permute(e_recv.view(R, 1), E, out=(es.offsets, es.perm[:R], es.inv[:R]))
+            slots = self._run_experts(l, np.bincount(e_host, minlength=E), x_recv, 1, off2, perm2, es)
+            y_recv = K.gather_rows(es.y, inv2, 1)
+        else:
+            y_recv = torch.empty((0, H), dtype=torch.float32, device=self.device)
+        y_back = self.ep.combine(y_recv)
+        return self._shared_and_combine(l, xn, resid, s, w, idx, sg, y_back, inv, slots)
 
     def _gating_predict(self, layer: int, xn: torch.Tensor) -> None:
         """gating_next_layer baseline: predict layer+1 from this layer's MLP

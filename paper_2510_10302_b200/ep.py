@@ -1,0 +1,137 @@
+"""Expert-parallel verify MoE (SURVEY.md §8 row e, the optional mode).
+
+The reference has no expert parallelism (it simulates one device,
+``simcore.py:182-515``); this is the B200 multi-GPU variant of the verify
+MoE layer (Eq. 1): the routed experts of every layer are split into
+contiguous blocks, rank r owning ``[lo_r, hi_r)``, and each verify layer does
+
+    K1 route (local tokens) -> K2 permute (expert order = owner order)
+    -> gather rows -> all-to-all dispatch (rows + expert ids)
+    -> K2/K3 on the received rows with the rank's own expert slots
+    -> gather back to receive order -> all-to-all combine
+    -> K4 weighted combine + residual (K2's inverse map indexes the returned
+       rows directly, because the send order IS K2's permuted order).
+
+Because expert ids are contiguous per owner, K2's stable expert order is
+already grouped by destination rank: no extra sort, the send counts are
+prefix sums of the per-expert counts the host already holds for its cache
+decisions.  One process per GPU; the collectives go through
+``torch.distributed`` (NCCL over NVLink on a GPU box, gloo in the CPU tests,
+where ``gather`` is injected).  World size 1 degenerates to local copies.
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import numpy as np
+import torch
+
+
+def shard_range(num_experts: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced expert block ``[lo, hi)`` owned by ``rank``."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank / world")
+    if num_experts < world:
+        raise ValueError(f"expert parallelism needs experts_per_layer ({num_experts}) >= world size ({world})")
+    return rank * num_experts // world, (rank + 1) * num_experts // world
+
+
+def owner_table(num_experts: int, world: int) -> np.ndarray:
+    """``owner[e]`` = the rank hosting routed expert e."""
+    own = np.empty(num_experts, dtype=np.int64)
+    for r in range(world):
+        lo, hi = shard_range(num_experts, r, world)
+        own[lo:hi] = r
+    return own
+
+
+def send_counts_of(counts: np.ndarray, world: int) -> list[int]:
+    """Rows sent to each rank from per-expert routed counts (K2 order)."""
+    E = counts.shape[0]
+    return [int(counts[slice(*shard_range(E, r, world))].sum()) for r in range(world)]
+
+
+def _default_gather(src: torch.Tensor, idx: torch.Tensor, div: int, out: torch.Tensor | None = None):
+    from .kernels import gather_rows
+
+    return gather_rows(src, idx, div, out=out)
+
+
+class ExpertParallelExchange:
+    """The two all-to-alls of one expert-parallel MoE layer.
+
+    ``dispatch(x, idx_flat, perm, counts)`` sends each routed (token, choice)
+    row to the owner of its expert and returns the received rows, their
+    global expert ids (device and host copies).  ``combine(y_recv)`` sends
+    the expert outputs back; the result is ``[T*k, H]`` in the sender's K2
+    permuted order, ready for K4 with K2's inverse map.
+    """
+
+    def __init__(self, num_experts: int, top_k: int, group=None,
+                 gather: Callable | None = None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        # without a process group the exchange is a local copy (world 1)
+        self.local_only = not dist.is_initialized()
+        self.world = 1 if self.local_only else dist.get_world_size(group)
+        self.rank = 0 if self.local_only else dist.get_rank(group)
+        self.E, self.k = num_experts, top_k
+        self.lo, self.hi = shard_range(num_experts, self.rank, self.world)
+        self.gather = gather or _default_gather
+        self._send: list[int] = []
+        self._recv: list[int] = []
+        self.bytes_sent = 0
+
+    @property
+    def local_experts(self) -> range:
+        return range(self.lo, self.hi)
+
+    def _a2a(self, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits) -> None:
+        if self.local_only:
+            out.copy_(inp)
+            return
+        self.dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+
+    def _exchange_counts(self, send: list[int], device) -> list[int]:
+        if self.local_only:
+            return list(send)
+        # NCCL needs device tensors; gloo host tensors
+        dev = device if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        s = torch.tensor(send, dtype=torch.int64, device=dev)
+        r = torch.empty_like(s)
+        self.dist.all_to_all_single(r, s, group=self.group)
+        return [int(v) for v in r.tolist()]
+
+    def dispatch(self, x: torch.Tensor, idx_flat: torch.Tensor, perm: torch.Tensor, counts: np.ndarray):
+        """x ``[T, H]``, idx_flat ``[T*k]`` int32 global expert ids, perm =
+        K2's ``perm_token`` (flat positions in expert order), counts = routed
+        rows per expert (host).  Returns ``(x_recv [R, H], e_recv [R] int32,
+        e_recv_host np.ndarray)``."""
+        T, H = x.shape
+        n = T * self.k
+        self._send = send_counts_of(np.asarray(counts), self.world)
+        if sum(self._send) != n:
+            raise ValueError("per-expert counts do not cover the routed rows")
+        self._recv = self._exchange_counts(self._send, x.device)
+        R = sum(self._recv)
+        x_send = self.gather(x, perm[:n], self.k)
+        e_send = self.gather(idx_flat[:n], perm[:n], 1)
+        x_recv = torch.empty((R, H), dtype=x.dtype, device=x.device)
+        e_recv = torch.empty((R,), dtype=idx_flat.dtype, device=x.device)
+        self._a2a(x_recv, x_send, self._recv, self._send)
+        self._a2a(e_recv, e_send, self._recv, self._send)
+        e_host = e_recv.cpu().numpy()
+        if R and (e_host.min() < self.lo or e_host.max() >= self.hi):
+            raise RuntimeError("received rows for experts this rank does not own")
+        self.bytes_sent += (n - self._send[self.rank]) * H * x.element_size()
+        return x_recv, e_recv, e_host
+
+    def combine(self, y_recv: torch.Tensor) -> torch.Tensor:
+        """y_recv ``[R, H]`` in receive order -> ``[T*k, H]`` in send order."""
+        n = sum(self._send)
+        out = torch.empty((n,) + tuple(y_recv.shape[1:]), dtype=y_recv.dtype, device=y_recv.device)
+        self._a2a(out, y_recv, self._send, self._recv)
+        return out

@@ -291,4 +291,5 @@ def test_permute_all_tokens_one_expert(oracle):
     torch.cuda.synchronize()
     o2, p2, i2 = oracle.moe_permute(idx, 8)
     assert np.array_equal(bits(off), o2) and np.array_equal(bits(perm), p2) and np.array_equal(bits(inv), i2)
-    assert bits(off)[3] == 0 and bits(off)[6] - bits(off)[5] == 72
+    o = bits(off)
+    assert o[2] == 0 and o[3] - o[2] == 72 and o[6] - o[5] == 72 and o[8] == 144

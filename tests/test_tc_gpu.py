@@ -90,3 +90,20 @@ def test_tc_split_invariance(oracle):
 def test_tc_planned_split_single_expert(oracle):
     """The planner's down-phase split for a lone late expert stays in tolerance."""
     check(*run_tc(oracle, 2, 256, 1024, 1, 1, seed=13))
+
+
+@pytest.mark.parametrize("H,F", [(4096, 14336), (2048, 1408)])
+def test_tc_static_plan_grouping_invariant(oracle, H, F):
+    """With the engine's launch-independent split (kernels.tc_plan_static),
+    running every expert in one launch or each expert in its own launch
+    (late prefetch / demand order) gives bit-identical outputs."""
+    from paper_2510_10302_b200 import kernels as K
+
+    E, k, T = 8, 2, 5
+    split = K.tc_plan_static(H, F)
+    one = run_tc(oracle, T, H, F, E, k, seed=21, split=split)
+    each = run_tc(oracle, T, H, F, E, k, seed=21, split=split, masks=[1 << e for e in range(E)])
+    mixed = run_tc(oracle, T, H, F, E, k, seed=21, split=split, masks=[0b00110101, 1 << 1, 1 << 3, 0b11000000])
+    for got in (each, mixed):
+        assert np.array_equal(got[0], one[0]) and np.array_equal(got[1], one[1])
+    check(*one)
