@@ -187,8 +187,9 @@ int spmoe_moe_combine(const float* y, const int32_t* inv_pos, const float* weigh
 /* gather_rows  (expert-parallel exchange, SURVEY §8 e)                   */
 /*   dst[j] = src[idx[j] / div] for j < n, rows of row_bytes (multiple of */
 /*   4).  Packs routed rows in K2's expert order before the dispatch     */
-/*   all-to-all (div = k, idx = perm_token) and restores receive order   */
-/*   before the combine all-to-all (div = 1, idx = inv_pos).  No         */
+/*   all-to-all (div = 1, idx = perm_token, the token of each permuted   */
+/*   row) and restores receive order before the combine all-to-all      */
+/*   (div = 1, idx = inv_pos).  No                                       */
 /*   reference counterpart: the reference has no expert parallelism.     */
 /* --------------------------------------------------------------------- */
 int spmoe_gather_rows(const void* src, const int32_t* idx, int n, int div, int64_t row_bytes,
@@ -227,6 +228,80 @@ int spmoe_h2d_batch(void* const* dst, const void* const* src, const size_t* byte
 /* --------------------------------------------------------------------- */
 int spmoe_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, uint64_t offset,
                            float std, void* stream);
+
+/* --------------------------------------------------------------------- */
+/* XC: lossless exponent coding of expert blobs on the host link          */
+/*   The offload tier moves every routed expert over PCIe               */
+/*   (IoChannel.transfer prefetch.py:45-74; t_io = size/bw + overhead,   */
+/*   config.py:229-231), so the bytes per expert set TPOT.  A bf16       */
+/*   weight is sign(1) | exponent(8) | mantissa(7); the exponent of      */
+/*   trained or N(0, s^2) weights has ~2.5 bits of entropy.  XC stores   */
+/*   each value as one sign|mantissa byte plus a 2-bit exponent code     */
+/*   (the 3 most frequent exponents of its segment, code 3 = escape),   */
+/*   escapes as a 4-bit secondary code (the next 15 exponents, 15 =      */
+/*   exception) and exceptions as (position, exponent) words.  Decoding  */
+/*   is exact: decode(encode(x)) == x bit for bit.  Per-value coding     */
+/*   only: no cross-value or cross-expert modelling.                     */
+/* --------------------------------------------------------------------- */
+#define SPMOE_XC_MAGIC 0x31435853u /* "SXC1" */
+#define SPMOE_XC_BLOCK 4096        /* values per coding block */
+#define SPMOE_XC_MAX_SEG 4
+
+/*
+ * One segment = one weight matrix of n bf16 values (n % SPMOE_XC_BLOCK == 0),
+ * nb = n / SPMOE_XC_BLOCK blocks.  Streams (byte offsets from the blob start,
+ * each 256-byte aligned):
+ *   sm    [n]      u8   (v >> 8 & 0x80) | (v & 0x7f)
+ *   pc    [n/16]   u32  word w holds the 2-bit codes of values 16w..16w+15,
+ *                       value 16w+j at bits 2j..2j+1; code c < 3 means
+ *                       exponent prim[c], 3 = escape
+ *   sec   [sec_words] u32  block b's escapes, in value order, as 4-bit codes
+ *                       starting at word bsec[b] (nibble q at bits 4(q%8) of
+ *                       word bsec[b] + q/8); code c < 15 = exponent sec[c],
+ *                       15 = exception
+ *   bsec  [nb+1]   u32  first sec word of each block (exclusive prefix)
+ *   bexc  [nb+1]   u32  first exception of each block (exclusive prefix)
+ *   exc   [n_exc]  u32  (position-in-block << 8) | exponent, ascending
+ * Code tables: the segment's exponents ordered by (count desc, exponent asc);
+ * prim = ranks 0-2, sec = ranks 3-17.
+ */
+typedef struct spmoe_xc_segment {
+  uint64_t n;
+  uint64_t off_sm, off_pc, off_sec, off_bsec, off_bexc, off_exc;
+  uint32_t sec_words, n_exc;
+  uint8_t prim[4]; /* [3] unused (0) */
+  uint8_t sec[16]; /* [15] unused (0) */
+  uint32_t pad;
+} spmoe_xc_segment; /* 88 bytes */
+
+typedef struct spmoe_xc_header {
+  uint32_t magic; /* SPMOE_XC_MAGIC */
+  uint32_t nseg;  /* 1..SPMOE_XC_MAX_SEG; segments decode back to back */
+  uint64_t blob_bytes; /* header + streams (what crosses the host link) */
+  uint64_t raw_bytes;  /* 2 * sum(n) */
+  spmoe_xc_segment seg[SPMOE_XC_MAX_SEG];
+} spmoe_xc_header; /* 376 bytes; the first stream starts at 512 */
+
+/* Device workspace bytes spmoe_xc_plan needs for these segments. */
+size_t spmoe_xc_work_bytes(int nseg, const int64_t* seg_n);
+/*
+ * Encoder step 1 (synchronous on `stream`): histogram each segment's
+ * exponents, choose its code tables, count each block's escape words and
+ * exceptions, and fill *hdr (host) with the blob layout.  src: the nseg
+ * segments back to back on the device.  work: device, spmoe_xc_work_bytes.
+ * Returns 1 (invalid value) if a segment size is not a multiple of
+ * SPMOE_XC_BLOCK.
+ */
+int spmoe_xc_plan(const uint16_t* src, int nseg, const int64_t* seg_n, void* work,
+                  spmoe_xc_header* hdr, void* stream);
+/* Encoder step 2: write the blob (hdr->blob_bytes bytes, device) for the
+ * plan in hdr / work (synchronous). */
+int spmoe_xc_encode(const uint16_t* src, const spmoe_xc_header* hdr, const void* work,
+                    uint8_t* blob, void* stream);
+/* Decode a device-resident blob whose header (host copy) is hdr into dst
+ * (hdr->raw_bytes bytes, device).  Stream-ordered; no host sync. */
+int spmoe_xc_decode(const uint8_t* blob, const spmoe_xc_header* hdr, uint16_t* dst,
+                    void* stream);
 
 /* --------------------------------------------------------------------- */
 /* Native runtime: LRU slot cache + prefetch worker (prefetch.py,        */
@@ -330,6 +405,26 @@ int spmoe_rt_transfer_experts(spmoe_rt* rt, int i, int32_t* experts, int cap);
  * stream at creation) to `event` (a timing cudaEvent_t on any stream), so
  * compute slots and transfers share one clock.  -1 if not measurable. */
 double spmoe_rt_since_epoch_ms(spmoe_rt* rt, void* event);
+/* Bytes of transfer record i that crossed the host link (XC blob bytes
+ * with a codec, raw expert bytes without); -1 if out of range. */
+int64_t spmoe_rt_transfer_wire_bytes(spmoe_rt* rt, int i);
+
+/*
+ * XC host tier (see "XC" above): from now on expert (l, e)'s host row at
+ * host_pool + host_index[l*E+e] * row_stride holds an XC blob of the
+ * slot's raw bytes.  Each copy goes to one of n_staging device buffers of
+ * staging_bytes (round robin, reused once the decode that read it is done)
+ * on the copy stream; decode_stream waits for it (and for the slot's
+ * readers), decodes into the slot and records the slot's ready event, so
+ * wait_slot / slot_ready keep their meaning.  Call once, before any copy.
+ * Returns cudaErrorInvalidValue if a row is not a valid blob of slot_bytes
+ * raw bytes or does not fit a staging buffer.
+ */
+int spmoe_rt_set_codec(spmoe_rt* rt, size_t row_stride, void* staging, size_t staging_bytes,
+                       int n_staging, void* decode_stream);
+/* Host-link bytes since the last reset: {prefetch, demand}. */
+void spmoe_rt_wire_bytes(spmoe_rt* rt, int64_t* out2);
+
 /* Drop the transfer log (waits for logged copies to finish). */
 void spmoe_rt_clear_log(spmoe_rt* rt);
 

@@ -36,12 +36,14 @@ _SIGS = {
     "oracle_fill_normal_bf16": (None, [_p, _i64, _u64, _u64, _f]),
     "oracle_set_threads": (None, [_i]),
     "oracle_num_threads": (_i, []),
+    "oracle_xc_encode": (_u64, [_p, _i, _p, _p, _u64, _p]),
+    "oracle_xc_decode": (_i, [_p, _p]),
 }
 
 
 def build() -> Path:
-    src = HERE / "spmoe_oracle.c"
-    if not LIB.exists() or LIB.stat().st_mtime < src.stat().st_mtime:
+    srcs = [HERE / "spmoe_oracle.c", HERE / "xc_oracle.c", HERE.parent / "include" / "spmoe.h"]
+    if not LIB.exists() or any(LIB.stat().st_mtime < s.stat().st_mtime for s in srcs):
         subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
     return LIB
 
@@ -177,3 +179,27 @@ def f32_to_bf16_bits(a: np.ndarray) -> np.ndarray:
 
 def bf16_bits_to_f32(a: np.ndarray) -> np.ndarray:
     return (np.ascontiguousarray(a, np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+# ---------------------------------------------------------------------------
+# XC expert-blob codec (oracle/xc_oracle.c)
+# ---------------------------------------------------------------------------
+def xc_encode(values, seg_n) -> np.ndarray:
+    """bf16 bits (uint16, segments back to back) -> XC blob (uint8)."""
+    v = _c(np.asarray(values).reshape(-1), np.uint16)
+    segs = np.asarray(seg_n, dtype=np.int64)
+    size = lib().oracle_xc_encode(_ptr(v), len(segs), _ptr(segs), None, 0, None)
+    if size == 0:
+        raise ValueError("segment sizes must be positive multiples of 4096")
+    out = np.empty((size,), np.uint8)
+    lib().oracle_xc_encode(_ptr(v), len(segs), _ptr(segs), _ptr(out), size, None)
+    return out
+
+
+def xc_decode(blob) -> np.ndarray:
+    blob = _c(blob, np.uint8)
+    raw = int(np.frombuffer(blob[16:24].tobytes(), dtype=np.uint64)[0])
+    out = np.empty((raw // 2,), np.uint16)
+    if lib().oracle_xc_decode(_ptr(blob), _ptr(out)) != 0:
+        raise ValueError("malformed XC blob")
+    return out

@@ -75,6 +75,13 @@ SIGNATURES: dict[str, tuple] = {
     "spmoe_rt_transfer_log": (_i, [_p, _p, _p, _i]),
     "spmoe_rt_transfer_experts": (_i, [_p, _i, _p, _i]),
     "spmoe_rt_clear_log": (None, [_p]),
+    "spmoe_rt_transfer_wire_bytes": (_i64, [_p, _i]),
+    "spmoe_rt_set_codec": (_i, [_p, _sz, _p, _sz, _i, _p]),
+    "spmoe_rt_wire_bytes": (None, [_p, _p]),
+    "spmoe_xc_work_bytes": (_sz, [_i, _p]),
+    "spmoe_xc_plan": (_i, [_p, _i, _p, _p, _p, _p]),
+    "spmoe_xc_encode": (_i, [_p, _p, _p, _p, _p]),
+    "spmoe_xc_decode": (_i, [_p, _p, _p, _p]),
     "spmoe_rt_since_epoch_ms": (C.c_double, [_p, _p]),
     "spmoe_host_alloc_mapped": (_i, [_sz, _p, _p]),
     "spmoe_host_free": (_i, [_p]),

@@ -339,9 +339,24 @@ class NativeExpertCache:
                     "start_ms": t[2 * i],
                     "end_ms": t[2 * i + 1],
                     "experts": tuple(ex[j] for j in range(ne)),
+                    "wire_bytes": int(self._lib.spmoe_rt_transfer_wire_bytes(self._h, i)),
                 }
             )
         return out
+
+    def set_codec(self, row_stride: int, staging_ptr: int, staging_bytes: int, n_staging: int,
+                  decode_stream_ptr: int) -> None:
+        """Host rows are XC blobs from now on (spmoe_rt_set_codec)."""
+        from . import _native
+
+        _native.check("spmoe_rt_set_codec", self._lib.spmoe_rt_set_codec(
+            self._h, row_stride, staging_ptr, staging_bytes, n_staging, decode_stream_ptr))
+
+    def wire_bytes(self) -> dict[str, int]:
+        """Bytes that crossed the host link since the last reset."""
+        o = (C.c_int64 * 2)()
+        self._lib.spmoe_rt_wire_bytes(self._h, o)
+        return {"prefetch": int(o[0]), "demand": int(o[1])}
 
     def clear_log(self) -> None:
         self._lib.spmoe_rt_clear_log(self._h)

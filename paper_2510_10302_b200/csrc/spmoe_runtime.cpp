@@ -47,6 +47,7 @@ struct Transfer {
   int seq;
   std::vector<int> experts;
   cudaEvent_t start, end;
+  int64_t wire_bytes;  // bytes that crossed the host link
 };
 
 }  // namespace
@@ -72,10 +73,21 @@ struct spmoe_rt {
   std::vector<cudaEvent_t> ready_ev, read_ev;
   std::vector<char> ready_rec, read_rec;
 
+  // XC host tier (spmoe_rt_set_codec): host rows are XC blobs; each copy
+  // lands in a staging buffer and the decode stream expands it into the slot
+  bool codec = false;
+  size_t row_stride = 0;
+  std::vector<char*> staging;
+  size_t staging_bytes = 0;
+  std::vector<cudaEvent_t> stage_full, stage_free;
+  std::vector<char> stage_used;
+  int stage_next = 0;
+  cudaStream_t decode_stream = nullptr;
+
   // counters
   int64_t hits = 0, misses = 0, evictions = 0, prefetch_evictions = 0, prefetch_insertions = 0,
           demand_insertions = 0, tasks_completed = 0, tasks_aborted = 0, prefetch_bytes = 0,
-          demand_bytes = 0, evictions_of_queued = 0;
+          demand_bytes = 0, evictions_of_queued = 0, prefetch_wire = 0, demand_wire = 0;
 
   // worker
   std::mutex mu_;
@@ -183,6 +195,49 @@ struct spmoe_rt {
     return e;
   }
 
+  const char* host_row(int key) const {
+    const int hidx = host_index.empty() ? key : host_index[key];
+    return host_pool + (size_t)hidx * (codec ? row_stride : slot_bytes);
+  }
+
+  // Raw tier: one H2D copy per expert straight into its slot, after the
+  // slot's last readers (read event) are done.
+  cudaError_t copy_raw(int s, const char* src, int64_t& wire) {
+    cudaError_t st = cudaSuccess;
+    if (read_rec[s]) st = cudaStreamWaitEvent(copy_stream, read_ev[s], 0);
+    if (st == cudaSuccess)
+      st = cudaMemcpyAsync(dev_pool + (size_t)s * slot_bytes, src, slot_bytes, cudaMemcpyHostToDevice,
+                           copy_stream);
+    if (st == cudaSuccess) st = cudaEventRecord(ready_ev[s], copy_stream);
+    wire += (int64_t)slot_bytes;
+    return st;
+  }
+
+  // XC tier: H2D of the blob into the next staging buffer (once the decode
+  // that last used it is done), then on the decode stream: wait for the
+  // copy and for the slot's readers, expand into the slot, free the buffer,
+  // mark the slot ready.  The link never waits for a slot's readers.
+  cudaError_t copy_xc(int s, const char* src, int64_t& wire) {
+    const spmoe_xc_header* h = (const spmoe_xc_header*)src;
+    const int i = stage_next;
+    stage_next = (stage_next + 1) % (int)staging.size();
+    cudaError_t st = cudaSuccess;
+    if (stage_used[i]) st = cudaStreamWaitEvent(copy_stream, stage_free[i], 0);
+    if (st == cudaSuccess)
+      st = cudaMemcpyAsync(staging[i], src, h->blob_bytes, cudaMemcpyHostToDevice, copy_stream);
+    if (st == cudaSuccess) st = cudaEventRecord(stage_full[i], copy_stream);
+    if (st == cudaSuccess) st = cudaStreamWaitEvent(decode_stream, stage_full[i], 0);
+    if (st == cudaSuccess && read_rec[s]) st = cudaStreamWaitEvent(decode_stream, read_ev[s], 0);
+    if (st == cudaSuccess)
+      st = (cudaError_t)spmoe_xc_decode((const uint8_t*)staging[i], h,
+                                        (uint16_t*)(dev_pool + (size_t)s * slot_bytes), decode_stream);
+    if (st == cudaSuccess) st = cudaEventRecord(stage_free[i], decode_stream);
+    stage_used[i] = 1;
+    if (st == cudaSuccess) st = cudaEventRecord(ready_ev[s], decode_stream);
+    wire += (int64_t)h->blob_bytes;
+    return st;
+  }
+
   // Issue the copies of `keys` (already installed) on the copy stream.
   int issue_copies(const std::vector<int>& keys, int layer, int kind) {
     if (keys.empty()) return 0;
@@ -190,6 +245,7 @@ struct spmoe_rt {
     tr.layer = layer;
     tr.kind = kind;
     tr.seq = seq_++;
+    tr.wire_bytes = 0;
     for (int k : keys) tr.experts.push_back(k % E);
     tr.start = new_timing_event();
     tr.end = new_timing_event();
@@ -197,24 +253,24 @@ struct spmoe_rt {
     for (size_t i = 0; i < keys.size() && st == cudaSuccess; ++i) {
       const int k = keys[i];
       const int s = slot_of[k];
-      if (read_rec[s]) st = cudaStreamWaitEvent(copy_stream, read_ev[s], 0);
-      if (st != cudaSuccess) break;
-      const int hidx = host_index.empty() ? k : host_index[k];
-      st = cudaMemcpyAsync(dev_pool + (size_t)s * slot_bytes,
-                           host_pool + (size_t)hidx * slot_bytes, slot_bytes,
-                           cudaMemcpyHostToDevice, copy_stream);
-      if (st != cudaSuccess) break;
-      st = cudaEventRecord(ready_ev[s], copy_stream);
+      st = codec ? copy_xc(s, host_row(k), tr.wire_bytes) : copy_raw(s, host_row(k), tr.wire_bytes);
       ready_rec[s] = 1;
-      if (!batched && kind == 0 && i + 1 < keys.size()) {
+      if (st == cudaSuccess && !batched && kind == 0 && i + 1 < keys.size()) {
         // unbatched I/O (PolicySpec.batched_io = false): one copy launch at
         // a time, each completed before the next is issued
         st = cudaStreamSynchronize(copy_stream);
       }
     }
-    if (st == cudaSuccess) st = cudaEventRecord(tr.end, copy_stream);
+    // the transfer ends when its last expert is usable (after its decode)
+    if (st == cudaSuccess) st = cudaEventRecord(tr.end, codec ? decode_stream : copy_stream);
     const int64_t nbytes = (int64_t)keys.size() * (int64_t)slot_bytes;
-    if (kind == 0) prefetch_bytes += nbytes; else demand_bytes += nbytes;
+    if (kind == 0) {
+      prefetch_bytes += nbytes;
+      prefetch_wire += tr.wire_bytes;
+    } else {
+      demand_bytes += nbytes;
+      demand_wire += tr.wire_bytes;
+    }
     log_.push_back(std::move(tr));
     return (int)st;
   }
@@ -332,6 +388,9 @@ void spmoe_rt_destroy(spmoe_rt* rt) {
   if (!rt) return;
   spmoe_rt_worker_stop(rt);
   cudaStreamSynchronize(rt->copy_stream);
+  if (rt->decode_stream) cudaStreamSynchronize(rt->decode_stream);
+  for (auto e : rt->stage_full) cudaEventDestroy(e);
+  for (auto e : rt->stage_free) cudaEventDestroy(e);
   for (auto e : rt->ready_ev) cudaEventDestroy(e);
   for (auto e : rt->read_ev) cudaEventDestroy(e);
   for (auto& t : rt->log_) {
@@ -432,6 +491,45 @@ void spmoe_rt_reset_stats(spmoe_rt* rt) {
   rt->prefetch_insertions = rt->demand_insertions = 0;
   rt->tasks_completed = rt->tasks_aborted = 0;
   rt->prefetch_bytes = rt->demand_bytes = rt->evictions_of_queued = 0;
+  rt->prefetch_wire = rt->demand_wire = 0;
+}
+
+int spmoe_rt_set_codec(spmoe_rt* rt, size_t row_stride, void* staging, size_t staging_bytes, int n_staging,
+                       void* decode_stream) {
+  if (!rt || !staging || n_staging < 1 || !decode_stream || row_stride < sizeof(spmoe_xc_header))
+    return (int)cudaErrorInvalidValue;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  if (rt->seq_ > 0 || rt->codec) return (int)cudaErrorInvalidValue;  // before any copy, once
+  rt->row_stride = row_stride;
+  rt->codec = true;
+  // every referenced row must be a well-formed blob that fits a staging buffer
+  for (int key = 0; key < rt->L * rt->E; ++key) {
+    const spmoe_xc_header* h = (const spmoe_xc_header*)rt->host_row(key);
+    if (h->magic != SPMOE_XC_MAGIC || h->blob_bytes > staging_bytes || h->blob_bytes > row_stride ||
+        h->raw_bytes != rt->slot_bytes) {
+      rt->codec = false;
+      return (int)cudaErrorInvalidValue;
+    }
+  }
+  rt->staging_bytes = staging_bytes;
+  rt->decode_stream = (cudaStream_t)decode_stream;
+  for (int i = 0; i < n_staging; ++i) {
+    rt->staging.push_back((char*)staging + (size_t)i * staging_bytes);
+    cudaEvent_t a, b;
+    cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+    rt->stage_full.push_back(a);
+    rt->stage_free.push_back(b);
+    rt->stage_used.push_back(0);
+  }
+  return 0;
+}
+
+void spmoe_rt_wire_bytes(spmoe_rt* rt, int64_t* out2) {
+  if (!rt || !out2) return;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  out2[0] = rt->prefetch_wire;
+  out2[1] = rt->demand_wire;
 }
 
 int spmoe_rt_demand_load(spmoe_rt* rt, const int32_t* layers, const int32_t* experts, int n,
@@ -596,6 +694,13 @@ int spmoe_rt_transfer_log(spmoe_rt* rt, int32_t* rec4, double* t2, int cap) {
     ++n;
   }
   return n;
+}
+
+int64_t spmoe_rt_transfer_wire_bytes(spmoe_rt* rt, int i) {
+  if (!rt) return -1;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  if (i < 0 || i >= (int)rt->log_.size()) return -1;
+  return rt->log_[i].wire_bytes;
 }
 
 int spmoe_rt_transfer_experts(spmoe_rt* rt, int i, int32_t* experts, int cap) {

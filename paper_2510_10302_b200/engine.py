@@ -143,6 +143,8 @@ class SpecMoEEngine:
         ffn_impl: str = "auto",
         expert_parallel: bool = False,
         ep_group=None,
+        host_codec: str | None = "auto",
+        n_staging: int = 3,
     ):
         if ffn_impl not in ("auto", "tcgen05", "cuda_core"):
             raise ValueError("ffn_impl must be auto | tcgen05 | cuda_core")
@@ -181,7 +183,13 @@ class SpecMoEEngine:
             self.host_pool, self.weights = model_state
             self._owns_model = False
         else:
-            self.host_pool = HostExpertPool(arch, host_distinct, share=host_share, leader=host_leader)
+            if host_codec == "auto":
+                # XC whenever the expert's matrices are whole coding blocks
+                from .codec import codec_applies, expert_segments
+
+                host_codec = "xc" if codec_applies(expert_segments(arch.ffn, arch.hidden)) else None
+            self.host_pool = HostExpertPool(arch, host_distinct, share=host_share, leader=host_leader,
+                                            codec=host_codec)
             self.weights = build_weights(arch, self.seed, self.device, self.host_pool, draft_perturb=draft_perturb)
             self._owns_model = True
         self.pool = torch.empty((self.capacity, arch.expert_elems), dtype=torch.bfloat16, device=self.device)
@@ -197,6 +205,15 @@ class SpecMoEEngine:
             copy_stream_ptr=self.copy_stream.cuda_stream,
             batched_io=policy.batched_io,
         )
+        self.staging = None
+        self.decode_stream = None
+        if self.host_pool.codec == "xc":
+            # XC host tier: blobs land in staging buffers on the copy stream
+            # and are expanded into their slots on the decode stream
+            stride = self.host_pool.row_stride
+            self.staging = torch.empty((n_staging * stride,), dtype=torch.uint8, device=self.device)
+            self.decode_stream = torch.cuda.Stream(device=self.device)
+            self.cache.set_codec(stride, self.staging.data_ptr(), stride, n_staging, self.decode_stream.cuda_stream)
         self.window_tokens = window_tokens
         self.cutoff = (
             effective_cutoff(self.model, hw, timings, policy, window_tokens)
@@ -487,7 +504,7 @@ class SpecMoEEngine:
         k, E = a.top_k, a.num_experts
         offsets, perm, inv = K.moe_permute(idx, E, out=(s.offsets, s.perm[: T * k], s.inv[: T * k]))
         counts = np.bincount(ids, minlength=E)
-        x_recv, e_recv, e_host = self.ep.dispatch(xn, idx.view(-1), perm, counts)
+        x_recv, e_recv, e_host = self.ep.dispatch(xn, perm, counts)
         R = x_recv.shape[0]
         slots = [0] * E
         if R:
@@ -924,6 +941,8 @@ class SpecMoEEngine:
         pre_ms = sum(t.duration for t in pre) * 1e3
         h2d_bytes = sum(t.nbytes for t in transfers)
         h2d_ms = sum(t.duration for t in transfers) * 1e3
+        wire = self.cache.wire_bytes()
+        wire_bytes = wire["prefetch"] + wire["demand"]
         iters = [
             IterationRecord(r.index, it[0] / 1e3, it[1] / 1e3, it[2] / 1e3, r.position, r.drafted, r.accepted, r.emitted)
             for r, it in zip(self.iter_records, ts["iters"])
@@ -943,7 +962,13 @@ class SpecMoEEngine:
             "prefetch_copy_ms": pre_ms,
             "hidden_prefetch_fraction": (1.0 - ts["stall_ms"]["prefetch"] / pre_ms) if pre_ms > 0 else None,
             "h2d_bytes": h2d_bytes,
+            # expert bytes made resident per second of copy time (decoded)
             "h2d_gbs": (h2d_bytes / (h2d_ms / 1e3) / 1e9) if h2d_ms > 0 else None,
+            "host_codec": self.host_pool.codec,
+            "h2d_wire_bytes": wire_bytes,
+            # bytes that crossed the host link per second of copy time
+            "h2d_wire_gbs": (wire_bytes / (h2d_ms / 1e3) / 1e9) if h2d_ms > 0 else None,
+            "h2d_wire_ratio": (wire_bytes / h2d_bytes) if h2d_bytes else None,
             "n_prefetch_transfers": len(pre),
             "n_demand_transfers": len(dem),
             "wall_s": wall_s,

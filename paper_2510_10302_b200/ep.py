@@ -6,7 +6,7 @@ MoE layer (Eq. 1): the routed experts of every layer are split into
 contiguous blocks, rank r owning ``[lo_r, hi_r)``, and each verify layer does
 
     K1 route (local tokens) -> K2 permute (expert order = owner order)
-    -> gather rows -> all-to-all dispatch (rows + expert ids)
+    -> all-gather per-expert counts -> gather rows -> all-to-all dispatch
     -> K2/K3 on the received rows with the rank's own expert slots
     -> gather back to receive order -> all-to-all combine
     -> K4 weighted combine + residual (K2's inverse map indexes the returned
@@ -61,9 +61,10 @@ def _default_gather(src: torch.Tensor, idx: torch.Tensor, div: int, out: torch.T
 class ExpertParallelExchange:
     """The two all-to-alls of one expert-parallel MoE layer.
 
-    ``dispatch(x, idx_flat, perm, counts)`` sends each routed (token, choice)
-    row to the owner of its expert and returns the received rows, their
-    global expert ids (device and host copies).  ``combine(y_recv)`` sends
+    ``dispatch(x, perm_token, counts)`` sends each routed (token, choice)
+    row to the owner of its expert and returns the received rows and their
+    global expert ids (device and host copies), derived from the all-gathered
+    per-expert counts.  ``combine(y_recv)`` sends
     the expert outputs back; the result is ``[T*k, H]`` in the sender's K2
     permuted order, ready for K4 with K2's inverse map.
     """
@@ -95,37 +96,42 @@ class ExpertParallelExchange:
             return
         self.dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
 
-    def _exchange_counts(self, send: list[int], device) -> list[int]:
+    def _all_counts(self, counts: np.ndarray, device) -> np.ndarray:
+        """Every rank's per-expert routed counts ``[world, E]`` (one
+        all-gather of E ints): gives both exchange splits and the expert id
+        of every received row without sending ids."""
+        counts = np.asarray(counts, dtype=np.int64).reshape(1, -1)
         if self.local_only:
-            return list(send)
+            return counts
         # NCCL needs device tensors; gloo host tensors
         dev = device if self.dist.get_backend(self.group) == "nccl" else "cpu"
-        s = torch.tensor(send, dtype=torch.int64, device=dev)
-        r = torch.empty_like(s)
-        self.dist.all_to_all_single(r, s, group=self.group)
-        return [int(v) for v in r.tolist()]
+        mine = torch.from_numpy(counts.copy()).to(dev)
+        allc = torch.empty((self.world, counts.shape[1]), dtype=torch.int64, device=dev)
+        self.dist.all_gather_into_tensor(allc, mine, group=self.group)
+        return allc.cpu().numpy()
 
-    def dispatch(self, x: torch.Tensor, idx_flat: torch.Tensor, perm: torch.Tensor, counts: np.ndarray):
-        """x ``[T, H]``, idx_flat ``[T*k]`` int32 global expert ids, perm =
-        K2's ``perm_token`` (flat positions in expert order), counts = routed
-        rows per expert (host).  Returns ``(x_recv [R, H], e_recv [R] int32,
-        e_recv_host np.ndarray)``."""
+    def dispatch(self, x: torch.Tensor, perm_token: torch.Tensor, counts: np.ndarray):
+        """x ``[T, H]``; perm_token = K2's ``perm_token`` (the token of every
+        permuted row, rows grouped by expert ascending); counts = routed rows
+        per expert (host).  Returns ``(x_recv [R, H], e_recv [R] int32,
+        e_recv_host np.ndarray)``; received rows are grouped by sender rank,
+        then by expert ascending."""
         T, H = x.shape
         n = T * self.k
-        self._send = send_counts_of(np.asarray(counts), self.world)
-        if sum(self._send) != n:
+        counts = np.asarray(counts, dtype=np.int64)
+        if int(counts.sum()) != n:
             raise ValueError("per-expert counts do not cover the routed rows")
-        self._recv = self._exchange_counts(self._send, x.device)
+        allc = self._all_counts(counts, x.device)
+        self._send = send_counts_of(counts, self.world)
+        self._recv = [int(allc[s, self.lo:self.hi].sum()) for s in range(self.world)]
         R = sum(self._recv)
-        x_send = self.gather(x, perm[:n], self.k)
-        e_send = self.gather(idx_flat[:n], perm[:n], 1)
+        x_send = self.gather(x, perm_token[:n], 1)
         x_recv = torch.empty((R, H), dtype=x.dtype, device=x.device)
-        e_recv = torch.empty((R,), dtype=idx_flat.dtype, device=x.device)
         self._a2a(x_recv, x_send, self._recv, self._send)
-        self._a2a(e_recv, e_send, self._recv, self._send)
-        e_host = e_recv.cpu().numpy()
-        if R and (e_host.min() < self.lo or e_host.max() >= self.hi):
-            raise RuntimeError("received rows for experts this rank does not own")
+        local = np.arange(self.lo, self.hi, dtype=np.int32)
+        e_host = np.concatenate([np.repeat(local, allc[s, self.lo:self.hi]) for s in range(self.world)]
+                                ).astype(np.int32) if R else np.zeros((0,), np.int32)
+        e_recv = torch.from_numpy(e_host).to(x.device)
         self.bytes_sent += (n - self._send[self.rank]) * H * x.element_size()
         return x_recv, e_recv, e_host
 

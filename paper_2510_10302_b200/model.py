@@ -118,6 +118,10 @@ ARCH_PRESETS: dict[str, ArchSpec] = {
         name="mixtral_8x7b", vocab=32000, hidden=4096, num_layers=32, num_heads=32,
         num_kv_heads=8, head_dim=128, ffn=14336, num_experts=8, top_k=2, rope_theta=1e6,
         max_seq=1024,
+        # measured acceptance vs spread (profiles/r1_acceptance_spread.jsonl,
+        # 20 SD iterations x 2 prompts): 0.02 -> 0.83-0.90, 0.005 -> 0.94-0.96,
+        # the paper's ~97 %
+        expert_spread=0.005,
     ),
     # BASELINE config #3: DeepSeek-V2-Lite MoE shapes (64 routed + 2 shared of
     # 1408, top-6, no top-k renorm); 27 MoE layers as in the reference ModelSpec
@@ -207,28 +211,54 @@ class HostExpertPool:
     L*E rows, experts alias rows (bounded host RAM; the bytes moved per copy
     are unchanged).  Allocated with cudaHostAlloc (exact size, portable,
     mapped) through the native library.
+
+    ``codec="xc"``: rows hold XC blobs (codec.py) instead of raw bf16; the
+    row stride is the largest blob, known only after the experts exist, so
+    :func:`build_weights` sizes the blobs first and then calls
+    :meth:`allocate`.
     """
 
     def __init__(self, arch: ArchSpec, distinct: int | None = None, share: str | None = None,
-                 leader: bool = True):
+                 leader: bool = True, codec: str | None = None):
         """``share`` = name of a /dev/shm pool shared by the per-GPU processes
         of one box (replica mode): the local leader creates and fills it
         (``writable``), followers attach once the leader publishes it."""
         from . import _native
 
+        if codec not in (None, "xc"):
+            raise ValueError("codec must be None or 'xc'")
         self.arch = arch
         n = arch.num_layers * arch.num_experts
         self.rows = n if not distinct else min(int(distinct), n)
         self.index = [i % self.rows for i in range(n)]
         self.slot_bytes = arch.expert_bytes
-        self.nbytes = self.rows * self.slot_bytes
+        self.codec = codec
         self._lib = _native.load()
         self._shared = None
+        self._share = share
         self.writable = leader
-        if share:
+        self.ptr = None
+        self.row_stride = 0
+        self.wire = [arch.expert_bytes] * self.rows  # bytes of each row that cross the link
+        if codec is None:
+            self.allocate(arch.expert_bytes)
+
+    def allocate(self, row_stride: int) -> None:
+        """Back the pool with ``rows * row_stride`` pinned bytes (followers of
+        a shared pool block here until the leader has created it)."""
+        from . import _native
+
+        if self.ptr is not None:
+            raise RuntimeError("host pool already allocated")
+        if row_stride % 2:
+            raise ValueError("row stride must be even")
+        self.row_stride = int(row_stride)
+        self.nbytes = self.rows * self.row_stride
+        if self._share:
             from .replicas import SharedHostPool
 
-            self._shared = SharedHostPool(share, self.rows, arch.expert_elems, leader=leader, publish=False)
+            self._shared = SharedHostPool(self._share, self.rows, self.row_stride // 2, leader=self.writable,
+                                          publish=False)
             self.ptr = self._shared.ptr
             self.array = self._shared.array
         else:
@@ -239,9 +269,10 @@ class HostExpertPool:
                 self._lib.spmoe_host_alloc_mapped(self.nbytes, C.byref(host), C.byref(dev)),
             )
             self.ptr = host.value
-            buf = (C.c_uint16 * (self.rows * arch.expert_elems)).from_address(self.ptr)
-            self.array = np.ctypeslib.as_array(buf).reshape(self.rows, arch.expert_elems)
+            buf = (C.c_uint16 * (self.rows * (self.row_stride // 2))).from_address(self.ptr)
+            self.array = np.ctypeslib.as_array(buf).reshape(self.rows, self.row_stride // 2)
         self.tensor = torch.from_numpy(self.array.view(np.int16)).view(torch.bfloat16)
+        self.bytes = torch.from_numpy(self.array.view(np.uint8))
 
     def publish(self) -> None:
         """Leader: mark a shared pool complete (followers unblock)."""
@@ -252,12 +283,31 @@ class HostExpertPool:
         return self.index[layer * self.arch.num_experts + expert]
 
     def blob(self, layer: int, expert: int) -> torch.Tensor:
+        """Raw pool row (bf16 expert blob; XC bytes viewed as bf16 with a codec)."""
         return self.tensor[self.row_of(layer, expert)]
+
+    def row_bytes(self, row: int) -> np.ndarray:
+        """The bytes of ``row`` that cross the host link (uint8 view)."""
+        return self.array[row].view(np.uint8)[: self.wire[row]]
+
+    def raw_row(self, row: int, device=None) -> np.ndarray:
+        """Decoded bf16 bits (uint16) of ``row``: the row itself for a raw
+        pool, the GPU decoder's output for an XC pool."""
+        if self.codec is None:
+            return self.array[row]
+        from . import codec as X
+
+        hdr = X.header_at(self.ptr + row * self.row_stride)
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        blob = self.bytes[row, : int(hdr.blob_bytes)].to(dev)
+        out = X.decode(blob, hdr)
+        return out.view(torch.int16).cpu().numpy().view(np.uint16)
 
     def close(self) -> None:
         if getattr(self, "ptr", None):
             self.tensor = None
             self.array = None
+            self.bytes = None
             if self._shared is not None:
                 self._shared.close(unlink=self.writable)
             else:
@@ -316,6 +366,39 @@ def build_weights(
     layers = []
     stage = torch.empty((min(chunk_experts, E), arch.expert_elems), dtype=bf, device=device)
     base_cache: dict[int, torch.Tensor] = {}
+
+    def gen_expert(dst: torch.Tensor, row: int) -> None:
+        # expert content is a pure function of its host-pool row, so an
+        # aliased row means the same weights for every layer using it
+        nonlocal base_cache
+        fill_expert_blob(dst, arch, seed, row)
+        if arch.expert_spread is not None:
+            # upcycled experts: the home layer's shared component plus a
+            # per-expert deviation of relative size expert_spread
+            base = base_cache.get(row // E)
+            if base is None:
+                base = torch.empty((arch.expert_elems,), dtype=bf, device=device)
+                fill_blob_generic(base, F, H, tensor_seed(seed, K_BASE, row // E), std,
+                                  arch.expert_out_scale * arch.res_scale)
+                base_cache = {row // E: base}
+            dst.copy_((base.float() + dst.float() * arch.expert_spread).to(bf))
+
+    enc = None
+    if host_pool is not None and host_pool.codec == "xc":
+        from .codec import XcEncoder, expert_segments
+
+        enc = XcEncoder(expert_segments(F, H), device)
+        if host_pool.ptr is None:
+            # pass 1: every distinct row's blob size -> the pool's row stride
+            # (deterministic, so every replica derives the same stride)
+            biggest = 0
+            for row in range(host_pool.rows):
+                gen_expert(stage[0], row)
+                hdr = enc.plan(stage[0])
+                host_pool.wire[row] = int(hdr.blob_bytes)
+                biggest = max(biggest, int(hdr.blob_bytes))
+            host_pool.allocate((biggest + 4095) // 4096 * 4096)
+            base_cache = {}
     written: set[int] = set()
     for l in range(arch.num_layers):
         wqkv = _fill(torch.empty((arch.qkv_dim, H), dtype=bf, device=device), tensor_seed(seed, K_QKV, l), std)
@@ -332,25 +415,20 @@ def build_weights(
             for j in range(n):
                 row = host_pool.row_of(l, e0 + j) if host_pool is not None else l * E + e0 + j
                 rows.append(row)
-                # expert content is a pure function of its host-pool row, so an
-                # aliased row means the same weights for every layer using it
-                fill_expert_blob(stage[j], arch, seed, row)
-                if arch.expert_spread is not None:
-                    # upcycled experts: the home layer's shared component plus a
-                    # per-expert deviation of relative size expert_spread
-                    base = base_cache.get(row // E)
-                    if base is None:
-                        base = torch.empty((arch.expert_elems,), dtype=bf, device=device)
-                        fill_blob_generic(base, F, H, tensor_seed(seed, K_BASE, row // E), std,
-                                          arch.expert_out_scale * arch.res_scale)
-                        base_cache = {row // E: base}
-                    stage[j].copy_((base.float() + stage[j].float() * arch.expert_spread).to(bf))
+                gen_expert(stage[j], row)
                 acc += stage[j].float()
             if host_pool is not None and host_pool.writable:
                 for j, row in enumerate(rows):
-                    if row not in written:
+                    if row in written:
+                        continue
+                    if enc is None:
                         host_pool.tensor[row].copy_(stage[j], non_blocking=False)
-                        written.add(row)
+                    else:
+                        hdr = enc.plan(stage[j])
+                        blob = enc.encode(stage[j], hdr)
+                        host_pool.wire[row] = blob.numel()
+                        host_pool.bytes[row, : blob.numel()].copy_(blob, non_blocking=False)
+                    written.add(row)
         mean = (acc / E).to(bf)
         del acc
         shared = None

@@ -42,6 +42,13 @@ def make_engine(policy_kind="draft_prefetch", capacity=12, cutoff=3, N=4, batch=
     return SpecMoEEngine(a, hw, t, pol, batch=batch, record=record, capture_layers=capture, ffn_impl=ffn_impl, **kw)
 
 
+def host_raw(eng, oracle, row):
+    """Raw bf16 bits of a host-pool row, independently of the GPU decoder:
+    the row itself (raw tier) or the CPU oracle's decode of its XC blob."""
+    hp = eng.host_pool
+    return hp.array[row] if hp.codec is None else oracle.xc_decode(hp.row_bytes(row))
+
+
 def prompts(batch, P=12, vocab=512, seed=0):
     g = torch.Generator().manual_seed(seed)
     return torch.randint(0, vocab, (batch, P), generator=g)
@@ -59,7 +66,7 @@ def check_layer_captures(eng, oracle, tol=None):
         assert np.array_equal(bits(cap["idx"]), idx_o), f"routing mismatch at layer {l}"
         assert np.array_equal(bits(cap["w"]).view(np.uint32), w_o.view(np.uint32))
         off, perm, inv = oracle.moe_permute(idx_o, a.num_experts)
-        blobs = [eng.host_pool.array[eng.host_pool.row_of(l, e)] for e in range(a.num_experts)]
+        blobs = [host_raw(eng, oracle, eng.host_pool.row_of(l, e)) for e in range(a.num_experts)]
         _, y = oracle.expert_ffn(blobs, xn, a.ffn, off, perm)
         out = oracle.moe_combine(y, inv, w_o, xn.shape[0], a.hidden, a.top_k, residual=bits(cap["resid"]))
         if tol is None:
@@ -246,7 +253,7 @@ def test_engine_shared_expert_arch(oracle):
             w_o, idx_o, _, sg_o = oracle.router_topk(xn, bits(lw.router), a.top_k, a.renorm, bits(lw.shared_gate))
             assert np.array_equal(bits(cap["idx"]), idx_o)
             off, perm, inv = oracle.moe_permute(idx_o, a.num_experts)
-            blobs = [eng.host_pool.array[eng.host_pool.row_of(l, e)] for e in range(a.num_experts)]
+            blobs = [host_raw(eng, oracle, eng.host_pool.row_of(l, e)) for e in range(a.num_experts)]
             _, y = oracle.expert_ffn(blobs, xn, a.ffn, off, perm)
             T = xn.shape[0]
             _, ys = oracle.expert_ffn([bits(lw.shared[0])], xn, a.shared_ffn, np.array([0, T], np.int32),

@@ -82,7 +82,8 @@ def _worker(rank, world, port, q, E, k, H, T_of_rank):
             flat = idx.reshape(-1)
             perm = np.argsort(flat, kind="stable").astype(np.int32)  # K2's expert order
             counts = np.bincount(flat, minlength=E)
-            x_recv, e_recv, e_host = ex.dispatch(x, torch.from_numpy(flat.copy()), torch.from_numpy(perm), counts)
+            # K2's perm_token: the token of every permuted row
+            x_recv, e_recv, e_host = ex.dispatch(x, torch.from_numpy(perm // k), counts)
             assert x_recv.shape[0] == e_host.shape[0]
             assert ((e_host >= ex.lo) & (e_host < ex.hi)).all()
             y_recv = _expert_fn(x_recv, e_recv)
