@@ -300,10 +300,23 @@ def main():
                         cache_capacity_experts=capacity)
     t_setup = time.perf_counter()
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
-    # replicas on one box share ONE pinned host expert pool through /dev/shm
-    share = f"{arch.name}_s1234_{os.environ.get('MASTER_PORT', '0')}" if local_world > 1 else None
+    # replicas on one box share one pinned host expert pool per NUMA node
+    # through /dev/shm; each process runs on its GPU's socket
+    from paper_2510_10302_b200.replicas import bind_to_node, gpu_numa_node, numa_pool_roles
+
+    node = gpu_numa_node(local)
+    bind_to_node(node)
+    share, leader = None, True
+    if local_world > 1:
+        nodes = [node] * world
+        if world > 1:
+            allnodes = [None] * world
+            dist.all_gather_object(allnodes, (local, node))
+            nodes = [n for _, n in sorted(allnodes)][:local_world]
+        node, leader = numa_pool_roles(nodes, local)
+        share = f"{arch.name}_s1234_{os.environ.get('MASTER_PORT', '0')}_n{node}"
     eng = SpecMoEEngine(arch, hw, timings, policy, batch=cfg["batch"], max_tokens=cfg["prompt"] + 64 * (cfg["N"] + 1),
-                        window_tokens=cfg["N"], host_share=share, host_leader=(local == 0),
+                        window_tokens=cfg["N"], host_share=share, host_leader=leader,
                         ffn_impl=args.ffn_impl, host_codec=None if args.host_codec == "none" else "xc")
     g = torch.Generator().manual_seed(1000 + rank)
     prompts = torch.randint(0, arch.vocab, (cfg["batch"], cfg["prompt"]), generator=g)
@@ -390,7 +403,8 @@ def main():
             "global_batch": B * world,
             "prompt_len": cfg["prompt"],
             "l2": "inputs larger than L2: each step streams >=20 GB of expert weights (126 MB L2)",
-            "parallelism": f"replicas x{world} (independent SD streams, per-GPU caches)",
+            "parallelism": f"replicas x{world} (independent SD streams, per-GPU caches, host pool per NUMA node)",
+            "numa_node": node,
         },
         "tpot_ms": dev_ms / args.steps / (emitted / args.steps / B) if emitted else None,
         "tokens_emitted": emitted_all,
@@ -432,6 +446,7 @@ def main():
             "launches": roof.get("launches"),
             "bytes_per_launch": roof.get("bytes_per_launch"),
             "ms_per_launch": roof.get("ms_per_launch"),
+            "by_shape": roof.get("by_shape"),
         },
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": d2h_step},
         "gpu_launches": launches,
@@ -444,6 +459,10 @@ def main():
         out["roofline"]["traffic_source"] = t.get("source")
     if rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
+        try:  # the CPU path may use every host core, not just the GPU's socket
+            os.sched_setaffinity(0, range(threads))
+        except OSError:
+            threads = len(os.sched_getaffinity(0))
         emitted_per_iter = emitted / args.steps
         sample_layers = 2
         hp = eng.host_pool

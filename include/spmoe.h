@@ -216,6 +216,31 @@ int spmoe_argmax_rows(const float* logits, int64_t ld, int rows, int V, int32_t*
                       void* stream);
 
 /* --------------------------------------------------------------------- */
+/* Layer block around the MoE (the draft forward    */
+/* and the target verify pass outside the MoE; simcore.py:323-359).       */
+/* Latency-bound helpers that replace ~30 framework kernels per layer.    */
+/* --------------------------------------------------------------------- */
+/* out[r] = bf16(x[r] * rsqrt(mean(x[r]^2) + eps) * w), rows of H (H % 8 == 0). */
+int spmoe_rms_norm(const uint16_t* x, const uint16_t* w, int rows, int H, float eps, uint16_t* out,
+                   void* stream);
+/*
+ * qkv     [B*T, (nh + 2*nkv)*hd] bf16  fused projection output
+ * cos/sin [max_pos, hd] f32 rotate-half RoPE tables
+ * start   [B] i64 device: position of each sequence's first new token
+ * q_out   [B, nh, T, hd] bf16 out (rotated queries)
+ * k_cache, v_cache [B, nkv, S, hd] bf16: rotated keys / values appended
+ *         at positions start[b] .. start[b] + T - 1
+ */
+int spmoe_rope_kv(const uint16_t* qkv, const float* cos_t, const float* sin_t, const int64_t* start,
+                  int B, int T, int nh, int nkv, int hd, int S, uint16_t* q_out, uint16_t* k_cache,
+                  uint16_t* v_cache, void* stream);
+/* Causal GQA attention of the T new queries over keys 0 .. start[b] + t;
+ * out [B, T, nh*hd] bf16; hd in {64, 128}; online softmax in fp32. */
+int spmoe_attention(const uint16_t* q, const uint16_t* k_cache, const uint16_t* v_cache,
+                    const int64_t* start, int B, int T, int nh, int nkv, int hd, int S, float scale,
+                    uint16_t* out, void* stream);
+
+/* --------------------------------------------------------------------- */
 /* K5  h2d_batch                                                          */
 /*   IoChannel.transfer / worker_step batched copy (prefetch.py:60-74,    */
 /*   191-214); Algorithm 2 line 12 copy_non_blocking.     */
@@ -302,6 +327,11 @@ int spmoe_xc_encode(const uint16_t* src, const spmoe_xc_header* hdr, const void*
  * (hdr->raw_bytes bytes, device).  Stream-ordered; no host sync. */
 int spmoe_xc_decode(const uint8_t* blob, const spmoe_xc_header* hdr, uint16_t* dst,
                     void* stream);
+/* Decode only segments [first, first + count) of the blob; dst is the base
+ * of the WHOLE decoded blob (each segment lands at its own offset).  Lets a
+ * copy path decode a segment as soon as its bytes have landed. */
+int spmoe_xc_decode_segments(const uint8_t* blob, const spmoe_xc_header* hdr, int first, int count,
+                             uint16_t* dst, void* stream);
 
 /* --------------------------------------------------------------------- */
 /* Native runtime: LRU slot cache + prefetch worker (prefetch.py,        */
@@ -408,6 +438,10 @@ double spmoe_rt_since_epoch_ms(spmoe_rt* rt, void* event);
 /* Bytes of transfer record i that crossed the host link (XC blob bytes
  * with a codec, raw expert bytes without); -1 if out of range. */
 int64_t spmoe_rt_transfer_wire_bytes(spmoe_rt* rt, int i);
+/* ms from the runtime epoch to the end of record i's last H2D copy (the
+ * link is free from then on; with the XC tier the record's end_ms follows
+ * after the last decode); -1 if not complete. */
+double spmoe_rt_transfer_copy_end_ms(spmoe_rt* rt, int i);
 
 /*
  * XC host tier (see "XC" above): from now on expert (l, e)'s host row at

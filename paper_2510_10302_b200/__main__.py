@@ -61,7 +61,7 @@ def cmd_run(a) -> int:
         write_report_csv([rep], out / "report.csv")
         write_transfer_log_csv(rep, out / "transfers.csv")
         eng.export_trace(out / "trace.txt")
-        write_profiled_config(out / "profiled.yaml", eng.model, hw, measure_timings(eng), policy)
+        write_profiled_config(out / "profiled.yaml", eng.model, eng.effective_hw(), measure_timings(eng), policy)
         print(rep.to_text(), end="")
     finally:
         eng.close()

@@ -50,6 +50,9 @@ SIGNATURES: dict[str, tuple] = {
     "spmoe_greedy_accept": (_i, [_p, _i64, _p, _i, _i, _i, _p, _p, _p]),
     "spmoe_argmax_rows": (_i, [_p, _i64, _i, _i, _p, _p]),
     "spmoe_h2d_batch": (_i, [_p, _p, _p, _i, _p]),
+    "spmoe_rms_norm": (_i, [_p, _p, _i, _i, _f, _p, _p]),
+    "spmoe_rope_kv": (_i, [_p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p]),
+    "spmoe_attention": (_i, [_p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p, _p]),
     "spmoe_fill_normal_bf16": (_i, [_p, _i64, _u64, _u64, _f, _p]),
     "spmoe_rt_create": (_p, [_i, _i, _i, _p, _p, _p, _sz, _p, _i]),
     "spmoe_rt_destroy": (None, [_p]),
@@ -76,12 +79,14 @@ SIGNATURES: dict[str, tuple] = {
     "spmoe_rt_transfer_experts": (_i, [_p, _i, _p, _i]),
     "spmoe_rt_clear_log": (None, [_p]),
     "spmoe_rt_transfer_wire_bytes": (_i64, [_p, _i]),
+    "spmoe_rt_transfer_copy_end_ms": (C.c_double, [_p, _i]),
     "spmoe_rt_set_codec": (_i, [_p, _sz, _p, _sz, _i, _p]),
     "spmoe_rt_wire_bytes": (None, [_p, _p]),
     "spmoe_xc_work_bytes": (_sz, [_i, _p]),
     "spmoe_xc_plan": (_i, [_p, _i, _p, _p, _p, _p]),
     "spmoe_xc_encode": (_i, [_p, _p, _p, _p, _p]),
     "spmoe_xc_decode": (_i, [_p, _p, _p, _p]),
+    "spmoe_xc_decode_segments": (_i, [_p, _p, _i, _i, _p, _p]),
     "spmoe_rt_since_epoch_ms": (C.c_double, [_p, _p]),
     "spmoe_host_alloc_mapped": (_i, [_sz, _p, _p]),
     "spmoe_host_free": (_i, [_p]),

@@ -17,7 +17,8 @@ CSRC = PKG_DIR / "csrc"
 REPO = PKG_DIR.parent
 LIB_PATH = PKG_DIR / "libspmoe.so"
 
-SOURCES = [CSRC / "spmoe_kernels.cu", CSRC / "spmoe_tc.cu", CSRC / "spmoe_codec.cu", CSRC / "spmoe_runtime.cpp"]
+SOURCES = [CSRC / "spmoe_kernels.cu", CSRC / "spmoe_tc.cu", CSRC / "spmoe_codec.cu", CSRC / "spmoe_attn.cu",
+           CSRC / "spmoe_runtime.cpp"]
 HEADERS = [CSRC / "spmoe_common.cuh", REPO / "include" / "spmoe.h"]
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -340,6 +340,7 @@ class NativeExpertCache:
                     "end_ms": t[2 * i + 1],
                     "experts": tuple(ex[j] for j in range(ne)),
                     "wire_bytes": int(self._lib.spmoe_rt_transfer_wire_bytes(self._h, i)),
+                    "copy_end_ms": float(self._lib.spmoe_rt_transfer_copy_end_ms(self._h, i)),
                 }
             )
         return out

@@ -62,8 +62,9 @@ def measure_timings(engine, steps: int = 3) -> ProfiledTimings:
     target_layer = max(0.0, ts["verify_ms"] / 1e3 - stall) / n_it / L
     per_expert = [t.duration / max(1, len(t.experts)) for t in rep.transfers if t.experts]
     t_io = sorted(per_expert)[len(per_expert) // 2] if per_expert else engine.timings.t_io_expert
-    # the reference invariant t_io >= size / bandwidth (validate_timings)
-    t_io = max(t_io, engine.arch.expert_bytes / engine.hw.pcie_bandwidth)
+    # the reference invariant t_io >= size / bandwidth (validate_timings),
+    # with the bandwidth in raw expert bytes (XC tier: link peak / wire ratio)
+    t_io = max(t_io, engine.arch.expert_bytes / engine.effective_hw().pcie_bandwidth)
     return ProfiledTimings(t_comp_target=target_layer, t_comp_draft=draft_layer, t_io_expert=t_io,
                            t_predict=K1_LATENCY_S)
 

@@ -215,6 +215,17 @@ __global__ void __launch_bounds__(kThreads) xc_write_kernel(const WriteParams p)
 }
 
 // ----------------------------------------------------------------- decode
+// Persistent CTAs, each owning a contiguous range of coding blocks.  Thread 0
+// streams the next blocks' sm / pc / escape words into a shared-memory ring
+// with bulk async copies (cp.async.bulk + mbarrier complete_tx) while the
+// CTA decodes the current block, so HBM latency is hidden behind decode
+// work.  Thread t decodes values 8t..8t+7 and 2048+8t..2048+8t+7 of the
+// block: every 16-byte output store of a warp is contiguous.
+constexpr int kDecStages = 3;
+constexpr int kSecBytes = SPMOE_XC_BLOCK / 2 + 16;  // all escaped + alignment slack
+constexpr int kStageBytes = SPMOE_XC_BLOCK + SPMOE_XC_BLOCK / 4 + kSecBytes;
+constexpr int kMaxBlocksPerCta = 1023;
+
 struct DecSeg {
   const uint8_t* sm;
   const uint32_t* pc;
@@ -231,61 +242,235 @@ struct DecSeg {
 struct DecParams {
   DecSeg seg[SPMOE_XC_MAX_SEG];
   int nseg;
+  uint32_t total;
 };
 
-__global__ void __launch_bounds__(kThreads) xc_decode_kernel(const DecParams p) {
-  __shared__ uint32_t s_sec[kMaxSecWords];
-  __shared__ uint8_t s_tab[16];
-  __shared__ int warp_sums[kThreads / 32 + 1];
+__device__ __forceinline__ uint32_t smem_u32(const void* q) { return (uint32_t)__cvta_generic_to_shared(q); }
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ int seg_of(const DecParams& p, uint32_t gb) {
   int si = 0;
 #pragma unroll
   for (int i = 1; i < SPMOE_XC_MAX_SEG; ++i)
-    if (i < p.nseg && blockIdx.x >= p.seg[i].blk0) si = i;
-  const DecSeg& S = p.seg[si];
-  const uint32_t lb = blockIdx.x - S.blk0;
-  const int64_t vbase = (int64_t)lb * SPMOE_XC_BLOCK + threadIdx.x * kPerThread;
-  const uint32_t w = __ldg(S.pc + vbase / 16);
-  const uint4 smv = __ldg(reinterpret_cast<const uint4*>(S.sm) + vbase / 16);
-  const uint32_t s0 = __ldg(S.bsec + lb), nw = __ldg(S.bsec + lb + 1) - s0;
-  for (uint32_t i = threadIdx.x; i < nw; i += kThreads) s_sec[i] = __ldg(S.sec + s0 + i);
-  if (threadIdx.x < 16) s_tab[threadIdx.x] = S.sec_tab[threadIdx.x];
-  const uint32_t esc = w & (w >> 1) & 0x55555555u;
-  int tot;
-  int q = block_exclusive_scan(__popc(esc), warp_sums, &tot);  // syncs: s_sec/s_tab visible
-  const uint32_t smw[4] = {smv.x, smv.y, smv.z, smv.w};
-  uint32_t out[8];
+    if (i < p.nseg && gb >= p.seg[i].blk0) si = i;
+  return si;
+}
+
+// Exponent of secondary code nib (0..14) from the segment's table held in
+// four registers (byte i of t[i/4]); two byte-permutes and a select, no
+// shared-memory lookup.
+__device__ __forceinline__ uint32_t sec_exp(const uint32_t (&t)[4], uint32_t nib) {
+  const uint32_t lo = __byte_perm(t[0], t[1], nib & 7u);
+  const uint32_t hi = __byte_perm(t[2], t[3], nib & 7u);
+  return (nib < 8u ? lo : hi) & 0xffu;
+}
+
+// Exception exponent of block position pos (code 15), from the block's
+// ascending (position << 8 | exponent) list.
+__device__ __noinline__ uint32_t exc_exp(const uint32_t* bexc, const uint32_t* exc, uint32_t lb, uint32_t pos) {
+  const uint32_t x0 = __ldg(bexc + lb), x1 = __ldg(bexc + lb + 1);
+  for (uint32_t x = x0; x < x1; ++x) {
+    const uint32_t ent = __ldg(exc + x);
+    if ((ent >> 8) == pos) return ent & 0xffu;
+  }
+  return 0u;
+}
+
+// Decode 8 values of one segment.  c16 = their 2-bit codes, sm_lo/sm_hi =
+// their sign|mantissa bytes, q = nibble index of their first escape in the
+// block's escape words s_sec.  Pairs are built with byte permutes and a
+// 16-entry pair table (exponent fields of two codes, escapes 0); escaped
+// values then OR in their exponent: the k-th escape of the group reads
+// nibble k of the 8-nibble window starting at q, branch-free.
+__device__ __forceinline__ uint4 decode8(uint32_t c16, uint32_t sm_lo, uint32_t sm_hi, const uint32_t* s_sec,
+                                         int q, const uint32_t* lut2, const uint32_t (&tab)[4], const DecSeg& S,
+                                         uint32_t lb, uint32_t pos0) {
+  uint32_t o[4];
 #pragma unroll
-  for (int j = 0; j < kPerThread; ++j) {
-    const uint32_t c = (w >> (2 * j)) & 3u;
-    const uint32_t b = (smw[j >> 2] >> (8 * (j & 3))) & 0xffu;
-    uint32_t e;
-    if (c < 3u) {
-      e = (S.prim >> (8 * c)) & 0xffu;
-    } else {
-      const uint32_t nib = (s_sec[q >> 3] >> ((q & 7) * 4)) & 15u;
-      ++q;
-      if (nib < 15u) {
-        e = s_tab[nib];
-      } else {
-        // exception: (position << 8) | exponent, ascending in the block
-        const uint32_t pos = threadIdx.x * kPerThread + j;
-        const uint32_t x0 = __ldg(S.bexc + lb), x1 = __ldg(S.bexc + lb + 1);
-        e = 0;
-        for (uint32_t x = x0; x < x1; ++x) {
-          const uint32_t ent = __ldg(S.exc + x);
-          if ((ent >> 8) == pos) {
-            e = ent & 0xffu;
-            break;
-          }
+  for (int pr = 0; pr < 4; ++pr) {
+    const uint32_t smw = pr < 2 ? sm_lo : sm_hi;
+    const uint32_t k = 2 * (pr & 1);
+    // bytes k, k+1 of smw -> the low bytes of the two 16-bit halves
+    const uint32_t w = __byte_perm(smw, 0u, k | (4u << 4) | ((k + 1) << 8) | (4u << 12));
+    o[pr] = ((w & 0x00800080u) << 8) | (w & 0x007f007fu) | lut2[(c16 >> (4 * pr)) & 15u];
+  }
+  const uint32_t esc = c16 & (c16 >> 1) & 0x5555u;
+  if (esc) {
+    const uint32_t w0 = s_sec[q >> 3], w1 = s_sec[(q >> 3) + 1];
+    const uint32_t win = __funnelshift_r(w0, w1, (q & 7) * 4);  // nibbles q .. q+7
+    bool exc = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t r = __popc(esc & ((1u << (2 * j)) - 1u));
+      const uint32_t nib = (win >> (4 * r)) & 15u;
+      const bool is = (esc >> (2 * j)) & 1u;
+      exc |= is && nib == 15u;
+      const uint32_t e = is ? sec_exp(tab, nib) : 0u;
+      o[j >> 1] |= (e << 7) << (16 * (j & 1));
+    }
+    if (exc) {
+#pragma unroll 1
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t r = __popc(esc & ((1u << (2 * j)) - 1u));
+        if (((esc >> (2 * j)) & 1u) && ((win >> (4 * r)) & 15u) == 15u) {
+          const uint32_t e = exc_exp(S.bexc, S.exc, lb, pos0 + j);
+          const uint32_t add = (e << 7) << (16 * (j & 1));
+          const int wsel = j >> 1;
+          o[0] |= wsel == 0 ? add : 0u;
+          o[1] |= wsel == 1 ? add : 0u;
+          o[2] |= wsel == 2 ? add : 0u;
+          o[3] |= wsel == 3 ? add : 0u;
         }
       }
     }
-    const uint32_t v = ((b & 0x80u) << 8) | (e << 7) | (b & 0x7fu);
-    if (j & 1) out[j >> 1] |= v << 16; else out[j >> 1] = v;
   }
-  uint4* d = reinterpret_cast<uint4*>(S.dst + vbase);
-  d[0] = make_uint4(out[0], out[1], out[2], out[3]);
-  d[1] = make_uint4(out[4], out[5], out[6], out[7]);
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+// Decode CTAs are 128 threads; thread t owns values 1024g + 8t .. +7 for the
+// four groups g of its block (every 16-byte store of a warp is contiguous).
+constexpr int kDecThreads = 128;
+
+__global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams p) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ uint64_t full[kDecStages];
+  __shared__ uint32_t s_bsec[kMaxBlocksPerCta + 1];
+  __shared__ uint32_t s_lut2[SPMOE_XC_MAX_SEG][16];
+  __shared__ uint2 warp_sums[2][kDecThreads / 32];
+  const uint32_t b0 = (uint32_t)(((uint64_t)blockIdx.x * p.total) / gridDim.x);
+  const uint32_t b1 = (uint32_t)(((uint64_t)(blockIdx.x + 1) * p.total) / gridDim.x);
+  const int n = (int)(b1 - b0);
+  // escape-word offsets of this CTA's blocks (and the one after the last)
+  for (int i = threadIdx.x; i <= n; i += kDecThreads) {
+    const uint32_t gb = b0 + i;
+    const DecSeg& S = p.seg[seg_of(p, i < n ? gb : gb - 1)];
+    s_bsec[i] = __ldg(S.bsec + (gb - S.blk0));
+  }
+  if (threadIdx.x < SPMOE_XC_MAX_SEG * 16) {
+    const int g = threadIdx.x / 16, c = threadIdx.x % 16;
+    const DecSeg& S = p.seg[g];
+    const uint32_t c0 = c & 3u, c1 = c >> 2;
+    const uint32_t e0 = c0 < 3 ? ((S.prim >> (8 * c0)) & 0xffu) << 7 : 0u;
+    const uint32_t e1 = c1 < 3 ? ((S.prim >> (8 * c1)) & 0xffu) << 7 : 0u;
+    s_lut2[g][c] = e0 | (e1 << 16);
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kDecStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // thread 0: start the copies of local block i into stage i % kDecStages
+  auto issue = [&](int i) {
+    const uint32_t gb = b0 + i;
+    const DecSeg& S = p.seg[seg_of(p, gb)];
+    const uint32_t lb = gb - S.blk0;
+    uint8_t* st = ring + (i % kDecStages) * kStageBytes;
+    // block i's escape words [s0, s1) end where block i+1's begin, except at
+    // a segment boundary, where the segment's own table entry nblk is used
+    const uint32_t s0 = s_bsec[i];
+    const uint32_t s1 = (lb + 1 == S.nblk) ? __ldg(S.bsec + S.nblk) : s_bsec[i + 1];
+    const uint32_t a = (s0 * 4) & ~15u;
+    const uint32_t len = (((s1 * 4) + 15) & ~15u) - a;
+    uint64_t* bar = &full[i % kDecStages];
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"((uint32_t)(SPMOE_XC_BLOCK + SPMOE_XC_BLOCK / 4) + len)
+                 : "memory");
+    bulk_g2s(st, S.sm + (uint64_t)lb * SPMOE_XC_BLOCK, SPMOE_XC_BLOCK, bar);
+    bulk_g2s(st + SPMOE_XC_BLOCK, S.pc + (uint64_t)lb * (SPMOE_XC_BLOCK / 16), SPMOE_XC_BLOCK / 4, bar);
+    if (len) bulk_g2s(st + SPMOE_XC_BLOCK + SPMOE_XC_BLOCK / 4, (const uint8_t*)S.sec + a, len, bar);
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kDecStages - 1 && i < n; ++i) issue(i);
+
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int si = -1;
+  uint32_t tab[4] = {0, 0, 0, 0};
+  for (int i = 0; i < n; ++i) {
+    const uint32_t gb = b0 + i;
+    const int sj = seg_of(p, gb);
+    const DecSeg& S = p.seg[sj];
+    if (sj != si) {
+      si = sj;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        tab[k] = (uint32_t)S.sec_tab[4 * k] | ((uint32_t)S.sec_tab[4 * k + 1] << 8) |
+                 ((uint32_t)S.sec_tab[4 * k + 2] << 16) | ((uint32_t)S.sec_tab[4 * k + 3] << 24);
+    }
+    const uint32_t lb = gb - S.blk0;
+    const uint8_t* st = ring + (i % kDecStages) * kStageBytes;
+    mbar_wait_parity(&full[i % kDecStages], (uint32_t)(i / kDecStages) & 1u);
+    const uint32_t* s_pc = (const uint32_t*)(st + SPMOE_XC_BLOCK);
+    const uint32_t sh = 16 * (t & 1);
+    uint32_t c[4];
+    int v01 = 0, v23 = 0;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      c[g] = (s_pc[64 * g + (t >> 1)] >> sh) & 0xffffu;
+      const int e = __popc(c[g] & (c[g] >> 1) & 0x5555u);
+      if (g < 2) v01 |= e << (16 * g); else v23 |= e << (16 * (g - 2));
+    }
+    // escapes of the four groups, two packed per int: two warp scans
+    int i01 = v01, i23 = v23;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u01 = __shfl_up_sync(0xffffffffu, i01, o);
+      const int u23 = __shfl_up_sync(0xffffffffu, i23, o);
+      if (lane >= o) {
+        i01 += u01;
+        i23 += u23;
+      }
+    }
+    uint2* ws = warp_sums[i & 1];
+    if (lane == 31) ws[warp] = make_uint2((uint32_t)i01, (uint32_t)i23);
+    // one barrier per block: publishes the warp sums and proves every thread
+    // is done with block i-1, so its stage can be refilled
+    __syncthreads();
+    if (threadIdx.x == 0 && i + kDecStages - 1 < n) issue(i + kDecStages - 1);
+    uint32_t b01 = 0, b23 = 0, t01 = 0, t23 = 0;
+#pragma unroll
+    for (int w = 0; w < kDecThreads / 32; ++w) {
+      const uint2 s_ = ws[w];
+      b01 += w < warp ? s_.x : 0u;
+      b23 += w < warp ? s_.y : 0u;
+      t01 += s_.x;
+      t23 += s_.y;
+    }
+    const uint32_t p01 = b01 + (uint32_t)(i01 - v01), p23 = b23 + (uint32_t)(i23 - v23);
+    // escapes of group g precede those of group g+1 (value order)
+    const uint32_t tg0 = t01 & 0xffffu, tg1 = t01 >> 16, tg2 = t23 & 0xffffu;
+    int q[4];
+    q[0] = (int)(p01 & 0xffffu);
+    q[1] = (int)(tg0 + (p01 >> 16));
+    q[2] = (int)(tg0 + tg1 + (p23 & 0xffffu));
+    q[3] = (int)(tg0 + tg1 + tg2 + (p23 >> 16));
+    const uint32_t* s_sec = (const uint32_t*)(st + SPMOE_XC_BLOCK + SPMOE_XC_BLOCK / 4) + (s_bsec[i] & 3u);
+    uint16_t* d = S.dst + (uint64_t)lb * SPMOE_XC_BLOCK;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const uint2 m = *(const uint2*)(st + 1024 * g + 8 * t);
+      const uint4 o = decode8(c[g], m.x, m.y, s_sec, q[g], s_lut2[sj], tab, S, lb, 1024 * g + 8 * t);
+      reinterpret_cast<uint4*>(d + 1024 * g)[t] = o;
+    }
+  }
 }
 
 inline uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
@@ -444,18 +629,21 @@ int spmoe_xc_encode(const uint16_t* src, const spmoe_xc_header* hdr, const void*
   return (int)cudaStreamSynchronize(st);
 }
 
-int spmoe_xc_decode(const uint8_t* blob, const spmoe_xc_header* hdr, uint16_t* dst, void* stream) {
-  if (!blob || !hdr || !dst || hdr->magic != SPMOE_XC_MAGIC || hdr->nseg < 1 || hdr->nseg > SPMOE_XC_MAX_SEG)
+int spmoe_xc_decode_segments(const uint8_t* blob, const spmoe_xc_header* hdr, int first, int count,
+                              uint16_t* dst, void* stream) {
+  if (!blob || !hdr || !dst || hdr->magic != SPMOE_XC_MAGIC || hdr->nseg < 1 || hdr->nseg > SPMOE_XC_MAX_SEG ||
+      first < 0 || count < 1 || first + count > (int)hdr->nseg)
     return (int)cudaErrorInvalidValue;
   DecParams p;
   std::memset(&p, 0, sizeof(p));
-  p.nseg = (int)hdr->nseg;
+  p.nseg = count;
   uint32_t blk = 0;
   uint16_t* d = dst;
-  for (uint32_t i = 0; i < hdr->nseg; ++i) {
-    const spmoe_xc_segment& g = hdr->seg[i];
+  for (int i = 0; i < first; ++i) d += hdr->seg[i].n;
+  for (int j = 0; j < count; ++j) {
+    const spmoe_xc_segment& g = hdr->seg[first + j];
     if (g.n == 0 || g.n % SPMOE_XC_BLOCK) return (int)cudaErrorInvalidValue;
-    DecSeg& S = p.seg[i];
+    DecSeg& S = p.seg[j];
     S.sm = blob + g.off_sm;
     S.pc = (const uint32_t*)(blob + g.off_pc);
     S.sec = (const uint32_t*)(blob + g.off_sec);
@@ -470,8 +658,31 @@ int spmoe_xc_decode(const uint8_t* blob, const spmoe_xc_header* hdr, uint16_t* d
     blk += S.nblk;
     d += g.n;
   }
-  xc_decode_kernel<<<blk, kThreads, 0, (cudaStream_t)stream>>>(p);
+  p.total = blk;
+  static int sms = 0;
+  static bool attr = false;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int smem = kDecStages * kStageBytes;
+  if (!attr) {
+    cudaFuncSetAttribute(xc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  // 8 CTAs of 128 threads per SM (ring + tables ~26 KB each), at most
+  // kMaxBlocksPerCta blocks each
+  uint32_t grid = (uint32_t)std::max(1, 8 * sms);
+  grid = std::max(grid, (blk + kMaxBlocksPerCta - 1) / kMaxBlocksPerCta);
+  grid = std::min(grid, blk);
+  xc_decode_kernel<<<grid, kDecThreads, smem, (cudaStream_t)stream>>>(p);
   return (int)cudaGetLastError();
+}
+
+int spmoe_xc_decode(const uint8_t* blob, const spmoe_xc_header* hdr, uint16_t* dst, void* stream) {
+  if (!hdr) return (int)cudaErrorInvalidValue;
+  return spmoe_xc_decode_segments(blob, hdr, 0, (int)hdr->nseg, dst, stream);
 }
 
 }  // extern "C"

@@ -47,6 +47,7 @@ struct Transfer {
   int seq;
   std::vector<int> experts;
   cudaEvent_t start, end;
+  cudaEvent_t copy_end;  // after the last H2D (XC tier: before its decode)
   int64_t wire_bytes;  // bytes that crossed the host link
 };
 
@@ -79,7 +80,7 @@ struct spmoe_rt {
   size_t row_stride = 0;
   std::vector<char*> staging;
   size_t staging_bytes = 0;
-  std::vector<cudaEvent_t> stage_full, stage_free;
+  std::vector<cudaEvent_t> stage_full, stage_free;  // stage_full: [stage][segment]
   std::vector<char> stage_used;
   int stage_next = 0;
   cudaStream_t decode_stream = nullptr;
@@ -214,23 +215,30 @@ struct spmoe_rt {
   }
 
   // XC tier: H2D of the blob into the next staging buffer (once the decode
-  // that last used it is done), then on the decode stream: wait for the
-  // copy and for the slot's readers, expand into the slot, free the buffer,
-  // mark the slot ready.  The link never waits for a slot's readers.
+  // that last used it is done), one copy per segment; on the decode stream:
+  // wait for the slot's readers, then decode each segment as soon as its
+  // bytes have landed, free the buffer, mark the slot ready.  The link never
+  // waits for a slot's readers, and after the last byte lands only the last
+  // segment (W2) remains to decode.
   cudaError_t copy_xc(int s, const char* src, int64_t& wire) {
     const spmoe_xc_header* h = (const spmoe_xc_header*)src;
     const int i = stage_next;
     stage_next = (stage_next + 1) % (int)staging.size();
+    const int ns = (int)h->nseg;
     cudaError_t st = cudaSuccess;
     if (stage_used[i]) st = cudaStreamWaitEvent(copy_stream, stage_free[i], 0);
-    if (st == cudaSuccess)
-      st = cudaMemcpyAsync(staging[i], src, h->blob_bytes, cudaMemcpyHostToDevice, copy_stream);
-    if (st == cudaSuccess) st = cudaEventRecord(stage_full[i], copy_stream);
-    if (st == cudaSuccess) st = cudaStreamWaitEvent(decode_stream, stage_full[i], 0);
     if (st == cudaSuccess && read_rec[s]) st = cudaStreamWaitEvent(decode_stream, read_ev[s], 0);
-    if (st == cudaSuccess)
-      st = (cudaError_t)spmoe_xc_decode((const uint8_t*)staging[i], h,
-                                        (uint16_t*)(dev_pool + (size_t)s * slot_bytes), decode_stream);
+    uint16_t* dst = (uint16_t*)(dev_pool + (size_t)s * slot_bytes);
+    for (int g = 0; g < ns && st == cudaSuccess; ++g) {
+      const uint64_t lo = g == 0 ? 0 : h->seg[g].off_sm;
+      const uint64_t hi = g + 1 < ns ? h->seg[g + 1].off_sm : h->blob_bytes;
+      cudaEvent_t full = stage_full[i * SPMOE_XC_MAX_SEG + g];
+      st = cudaMemcpyAsync(staging[i] + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, copy_stream);
+      if (st == cudaSuccess) st = cudaEventRecord(full, copy_stream);
+      if (st == cudaSuccess) st = cudaStreamWaitEvent(decode_stream, full, 0);
+      if (st == cudaSuccess)
+        st = (cudaError_t)spmoe_xc_decode_segments((const uint8_t*)staging[i], h, g, 1, dst, decode_stream);
+    }
     if (st == cudaSuccess) st = cudaEventRecord(stage_free[i], decode_stream);
     stage_used[i] = 1;
     if (st == cudaSuccess) st = cudaEventRecord(ready_ev[s], decode_stream);
@@ -249,6 +257,7 @@ struct spmoe_rt {
     for (int k : keys) tr.experts.push_back(k % E);
     tr.start = new_timing_event();
     tr.end = new_timing_event();
+    tr.copy_end = new_timing_event();
     cudaError_t st = cudaEventRecord(tr.start, copy_stream);
     for (size_t i = 0; i < keys.size() && st == cudaSuccess; ++i) {
       const int k = keys[i];
@@ -262,6 +271,7 @@ struct spmoe_rt {
       }
     }
     // the transfer ends when its last expert is usable (after its decode)
+    if (st == cudaSuccess) st = cudaEventRecord(tr.copy_end, copy_stream);
     if (st == cudaSuccess) st = cudaEventRecord(tr.end, codec ? decode_stream : copy_stream);
     const int64_t nbytes = (int64_t)keys.size() * (int64_t)slot_bytes;
     if (kind == 0) {
@@ -396,6 +406,7 @@ void spmoe_rt_destroy(spmoe_rt* rt) {
   for (auto& t : rt->log_) {
     cudaEventDestroy(t.start);
     cudaEventDestroy(t.end);
+    cudaEventDestroy(t.copy_end);
   }
   if (rt->epoch_) cudaEventDestroy(rt->epoch_);
   delete rt;
@@ -515,10 +526,13 @@ int spmoe_rt_set_codec(spmoe_rt* rt, size_t row_stride, void* staging, size_t st
   rt->decode_stream = (cudaStream_t)decode_stream;
   for (int i = 0; i < n_staging; ++i) {
     rt->staging.push_back((char*)staging + (size_t)i * staging_bytes);
-    cudaEvent_t a, b;
-    cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+    for (int g = 0; g < SPMOE_XC_MAX_SEG; ++g) {
+      cudaEvent_t a;
+      cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+      rt->stage_full.push_back(a);
+    }
+    cudaEvent_t b;
     cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
-    rt->stage_full.push_back(a);
     rt->stage_free.push_back(b);
     rt->stage_used.push_back(0);
   }
@@ -656,6 +670,7 @@ void spmoe_rt_clear_log(spmoe_rt* rt) {
     cudaEventSynchronize(t.end);
     cudaEventDestroy(t.start);
     cudaEventDestroy(t.end);
+    cudaEventDestroy(t.copy_end);
   }
   rt->log_.clear();
 }
@@ -694,6 +709,16 @@ int spmoe_rt_transfer_log(spmoe_rt* rt, int32_t* rec4, double* t2, int cap) {
     ++n;
   }
   return n;
+}
+
+double spmoe_rt_transfer_copy_end_ms(spmoe_rt* rt, int i) {
+  if (!rt) return -1.0;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  if (i < 0 || i >= (int)rt->log_.size()) return -1.0;
+  float ms = -1.0f;
+  if (cudaEventQuery(rt->log_[i].copy_end) != cudaSuccess) return -1.0;
+  if (cudaEventElapsedTime(&ms, rt->epoch_, rt->log_[i].copy_end) != cudaSuccess) return -1.0;
+  return ms;
 }
 
 int64_t spmoe_rt_transfer_wire_bytes(spmoe_rt* rt, int i) {

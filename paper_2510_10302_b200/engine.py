@@ -320,6 +320,21 @@ class SpecMoEEngine:
         return t
 
     @property
+    def wire_ratio(self) -> float:
+        """Host-link bytes per raw expert byte (1.0 on the raw tier)."""
+        hp = self.host_pool
+        return (sum(hp.wire) / len(hp.wire)) / self.arch.expert_bytes if hp.codec else 1.0
+
+    def effective_hw(self) -> HardwareSpec:
+        """``hw`` with pcie_bandwidth in RAW expert bytes per second: the link
+        peak divided by the wire ratio, so the reference's floor
+        t_io >= expert_size / pcie_bandwidth (config.py:362-375) and the
+        cutoff model's I/O term describe the XC tier correctly."""
+        from dataclasses import replace
+
+        return replace(self.hw, pcie_bandwidth=self.hw.pcie_bandwidth / self.wire_ratio)
+
+    @property
     def model_state(self) -> tuple:
         """(host pool, device weights) to share with another engine."""
         return self.host_pool, self.weights
@@ -396,7 +411,20 @@ class SpecMoEEngine:
             "experts_per_launch": sum(x[3] for x in self.k3_events) / len(ms),
             "rows_per_launch": sum(x[4] for x in self.k3_events) / len(ms),
             "total_ms": tot_ms,
+            "by_shape": self._k3_by_shape(ms),
         }
+
+    def _k3_by_shape(self, ms) -> dict:
+        """Timed K3 launches grouped by (experts, routed rows): count, mean
+        microseconds and achieved GB/s of algorithmic bytes."""
+        groups: dict = {}
+        for (_, _, byts, ne, rows), t in zip(self.k3_events, ms):
+            g = groups.setdefault(f"{ne}x{rows}", [0, 0.0, 0])
+            g[0] += 1
+            g[1] += t
+            g[2] += byts
+        return {k: {"n": v[0], "us": round(v[1] / v[0] * 1e3, 1), "gbs": round(v[2] / (v[1] / 1e3) / 1e9, 1)}
+                for k, v in sorted(groups.items(), key=lambda kv: -kv[1][0])}
 
     def _route(self, l: int, xn: torch.Tensor, s: _Scratch):
         """K1 on the verify tokens; indices also land in the mapped route ring
@@ -943,6 +971,20 @@ class SpecMoEEngine:
         h2d_ms = sum(t.duration for t in transfers) * 1e3
         wire = self.cache.wire_bytes()
         wire_bytes = wire["prefetch"] + wire["demand"]
+        # link occupancy: union of [start, last H2D done] over the transfers
+        spans = sorted((r["start_ms"], r["copy_end_ms"]) for r in self.cache.transfer_log()
+                       if r["copy_end_ms"] >= 0)
+        link_ms, copy_ms, cur = 0.0, 0.0, None
+        for a_, b_ in spans:
+            copy_ms += b_ - a_
+            if cur is None or a_ > cur[1]:
+                if cur is not None:
+                    link_ms += cur[1] - cur[0]
+                cur = [a_, b_]
+            else:
+                cur[1] = max(cur[1], b_)
+        if cur is not None:
+            link_ms += cur[1] - cur[0]
         iters = [
             IterationRecord(r.index, it[0] / 1e3, it[1] / 1e3, it[2] / 1e3, r.position, r.drafted, r.accepted, r.emitted)
             for r, it in zip(self.iter_records, ts["iters"])
@@ -967,7 +1009,10 @@ class SpecMoEEngine:
             "host_codec": self.host_pool.codec,
             "h2d_wire_bytes": wire_bytes,
             # bytes that crossed the host link per second of copy time
-            "h2d_wire_gbs": (wire_bytes / (h2d_ms / 1e3) / 1e9) if h2d_ms > 0 else None,
+            "h2d_wire_gbs": (wire_bytes / (copy_ms / 1e3) / 1e9) if copy_ms > 0 else None,
+            # time the host link was copying, and as a fraction of device time
+            "link_busy_ms": link_ms,
+            "link_busy_frac": (link_ms / total_ms) if total_ms > 0 else None,
             "h2d_wire_ratio": (wire_bytes / h2d_bytes) if h2d_bytes else None,
             "n_prefetch_transfers": len(pre),
             "n_demand_transfers": len(dem),

@@ -407,6 +407,52 @@ def moe_combine(
     return out
 
 
+# ---------------------------------------------------------------------------
+# layer block around the MoE (csrc/spmoe_attn.cu)
+# ---------------------------------------------------------------------------
+def rms_norm(x: torch.Tensor, w: torch.Tensor, eps: float, out: torch.Tensor | None = None, stream=None):
+    """bf16 RMSNorm over the last dim (fp32 math, one rounding)."""
+    _need(w, BF16, "w", 1)
+    if x.dtype != BF16 or not x.is_cuda:
+        raise ValueError("x must be a CUDA bf16 tensor (no CPU fallback)")
+    x = x.contiguous()
+    H = x.shape[-1]
+    if out is None:
+        out = torch.empty_like(x)
+    LAUNCHES["count"] += 1
+    _native.call("spmoe_rms_norm", x.data_ptr(), w.data_ptr(), x.numel() // H, H, float(eps), out.data_ptr(),
+                 _stream(stream))
+    return out
+
+
+def rope_kv(qkv: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor, start: torch.Tensor, nh: int, nkv: int,
+            hd: int, k_cache: torch.Tensor, v_cache: torch.Tensor, stream=None) -> torch.Tensor:
+    """qkv ``[B, T, (nh+2nkv)*hd]`` -> rotated q ``[B, nh, T, hd]``; rotated k
+    and v appended to the layer caches ``[B, nkv, S, hd]`` at start[b]+t."""
+    B, T = qkv.shape[0], qkv.shape[1]
+    qkv = qkv.contiguous()
+    if start.dtype != torch.int64 or not start.is_cuda:
+        raise ValueError("start must be a CUDA int64 tensor")
+    q = torch.empty((B, nh, T, hd), dtype=BF16, device=qkv.device)
+    LAUNCHES["count"] += 1
+    _native.call("spmoe_rope_kv", qkv.data_ptr(), cos.data_ptr(), sin.data_ptr(), start.data_ptr(), B, T, nh, nkv,
+                 hd, k_cache.shape[2], q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), _stream(stream))
+    return q
+
+
+def attention_cached(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, start: torch.Tensor,
+                     stream=None) -> torch.Tensor:
+    """Causal GQA attention of q ``[B, nh, T, hd]`` over the caches; returns
+    ``[B, T, nh*hd]`` bf16."""
+    B, nh, T, hd = q.shape
+    nkv, S = k_cache.shape[1], k_cache.shape[2]
+    out = torch.empty((B, T, nh * hd), dtype=BF16, device=q.device)
+    LAUNCHES["count"] += 1
+    _native.call("spmoe_attention", q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), start.data_ptr(), B, T,
+                 nh, nkv, hd, S, float(hd ** -0.5), out.data_ptr(), _stream(stream))
+    return out
+
+
 def gather_rows(src: torch.Tensor, idx: torch.Tensor, div: int = 1, out: torch.Tensor | None = None,
                 stream=None) -> torch.Tensor:
     """``out[j] = src[idx[j] // div]`` (rows of any dtype, row bytes a

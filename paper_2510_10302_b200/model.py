@@ -537,22 +537,19 @@ def rope_tables(arch: ArchSpec, device) -> tuple[torch.Tensor, torch.Tensor]:
 
 
 def rms_norm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
-    xf = x.float()
-    y = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)
-    return (y * w.float()).to(x.dtype)
+    """bf16 RMSNorm (csrc/spmoe_attn.cu; fp32 math, one rounding)."""
+    from .kernels import rms_norm as _rms
 
-
-def _rotate_half(x: torch.Tensor) -> torch.Tensor:
-    h = x.shape[-1] // 2
-    return torch.cat([-x[..., h:], x[..., :h]], dim=-1)
+    return _rms(x, w, eps)
 
 
 class KVCache:
-    """Per-model KV cache ``[L, B, S, n_kv, hd]`` with per-sequence lengths."""
+    """Per-model KV cache ``[L, B, n_kv, S, hd]`` (keys of one head contiguous
+    for the attention kernel); positions are per-sequence lengths."""
 
     def __init__(self, arch: ArchSpec, batch: int, device, max_seq: int | None = None):
         S = max_seq or arch.max_seq
-        shape = (arch.num_layers, batch, S, arch.num_kv_heads, arch.head_dim)
+        shape = (arch.num_layers, batch, arch.num_kv_heads, S, arch.head_dim)
         self.k = torch.zeros(shape, dtype=torch.bfloat16, device=device)
         self.v = torch.zeros(shape, dtype=torch.bfloat16, device=device)
         self.max_seq = S
@@ -564,32 +561,16 @@ def attention(
     x_norm: torch.Tensor,  # [B, T, H]
     kv: KVCache,
     start: torch.Tensor,  # [B] int64 position of the first of the T tokens
-    kv_len_max: int,  # max over b of start[b] + T
+    kv_len_max: int,  # max over b of start[b] + T (the kernel masks per sequence)
 ) -> torch.Tensor:
+    """qkv projection (cuBLAS) -> fused RoPE + KV append -> causal GQA
+    attention over the cache -> W_o projection (cuBLAS)."""
+    from . import kernels as K
+
     a = w.arch
-    B, T, H = x_norm.shape
     lw = w.layers[layer]
     qkv = torch.matmul(x_norm, lw.wqkv.t())
-    nh, nkv, hd = a.num_heads, a.num_kv_heads, a.head_dim
-    q, k, v = torch.split(qkv, [nh * hd, nkv * hd, nkv * hd], dim=-1)
-    q = q.view(B, T, nh, hd)
-    k = k.view(B, T, nkv, hd)
-    v = v.view(B, T, nkv, hd)
-    pos = start.view(B, 1) + torch.arange(T, device=x_norm.device).view(1, T)  # [B, T]
-    cos = w.rope_cos[pos].unsqueeze(2)  # [B, T, 1, hd]
-    sin = w.rope_sin[pos].unsqueeze(2)
-    q = (q.float() * cos + _rotate_half(q.float()) * sin).to(torch.bfloat16)
-    k = (k.float() * cos + _rotate_half(k.float()) * sin).to(torch.bfloat16)
-    bidx = torch.arange(B, device=x_norm.device).view(B, 1).expand(B, T)
-    kv.k[layer][bidx, pos] = k
-    kv.v[layer][bidx, pos] = v
-    Lk = kv_len_max
-    keys = kv.k[layer][:, :Lk].permute(0, 2, 1, 3)  # [B, nkv, Lk, hd]
-    vals = kv.v[layer][:, :Lk].permute(0, 2, 1, 3)
-    kpos = torch.arange(Lk, device=x_norm.device).view(1, 1, Lk)
-    mask = (kpos <= pos.view(B, T, 1)).unsqueeze(1)  # [B, 1, T, Lk]
-    o = torch.nn.functional.scaled_dot_product_attention(
-        q.permute(0, 2, 1, 3), keys, vals, attn_mask=mask, enable_gqa=(nkv != nh)
-    )
-    o = o.permute(0, 2, 1, 3).reshape(B, T, nh * hd)
+    q = K.rope_kv(qkv, w.rope_cos, w.rope_sin, start, a.num_heads, a.num_kv_heads, a.head_dim, kv.k[layer],
+                  kv.v[layer])
+    o = K.attention_cached(q, kv.k[layer], kv.v[layer], start)
     return torch.matmul(o, lw.wo.t())

@@ -4,8 +4,11 @@ PCIe link.  There is no data-path collective; ranks only
 
 * split the request streams (:func:`assign_streams`),
 * agree on timing (max over ranks) and totals (sum) (:func:`reduce_run`),
-* share ONE page-locked host expert pool per box through /dev/shm instead of
-  pinning L·E·expert_bytes per process (:class:`SharedHostPool`).
+* share ONE page-locked host expert pool per NUMA node through /dev/shm
+  instead of pinning the pool per process (:class:`SharedHostPool`,
+  :func:`numa_pool_roles`): each GPU reads experts from DRAM on its own
+  socket, so 8 concurrent host links do not funnel through one socket's
+  memory controllers and the inter-socket link.
 
 All functions take a ``torch.distributed`` process group (NCCL on the GPU
 box, gloo in the CPU tests).
@@ -19,6 +22,58 @@ import time
 from pathlib import Path
 
 import numpy as np
+
+
+def gpu_numa_node(device_index: int) -> int:
+    """NUMA node of a GPU's PCIe root (sysfs); 0 when unknown (single-node
+    hosts, containers without sysfs)."""
+    try:
+        import torch
+
+        pr = torch.cuda.get_device_properties(device_index)
+        bus = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        v = int(Path(f"/sys/bus/pci/devices/{bus}/numa_node").read_text().strip())
+        return max(v, 0)
+    except Exception:
+        return 0
+
+
+def node_cpus(node: int) -> list[int]:
+    """CPUs of a NUMA node (sysfs cpulist), [] if unknown."""
+    try:
+        text = Path(f"/sys/devices/system/node/node{node}/cpulist").read_text().strip()
+    except OSError:
+        return []
+    cpus: list[int] = []
+    for part in text.split(","):
+        if "-" in part:
+            a, b = part.split("-")
+            cpus.extend(range(int(a), int(b) + 1))
+        elif part:
+            cpus.append(int(part))
+    return cpus
+
+
+def numa_pool_roles(nodes: list[int], local_rank: int) -> tuple[int, bool]:
+    """One shared host pool per NUMA node: ``nodes[r]`` = NUMA node of local
+    rank r's GPU.  Returns (this rank's node, whether it leads (creates and
+    fills) that node's pool: the lowest local rank on the node)."""
+    node = nodes[local_rank]
+    leader = min(r for r, n in enumerate(nodes) if n == node) == local_rank
+    return node, leader
+
+
+def bind_to_node(node: int) -> bool:
+    """Run this process on its GPU's NUMA node, so the host pool pages it
+    first-touches (and pins) are local to that socket.  False if unknown."""
+    cpus = node_cpus(node)
+    if not cpus:
+        return False
+    try:
+        os.sched_setaffinity(0, cpus)
+        return True
+    except OSError:
+        return False
 
 
 def assign_streams(n_streams: int, rank: int, world: int) -> list[int]:

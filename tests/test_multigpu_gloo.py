@@ -77,3 +77,16 @@ def test_gloo_world2_reduction_and_shared_pool():
         assert wall == pytest.approx(3.0)
         assert tok == 11  # sum over ranks
         assert checksum == expect_sum  # follower sees the leader's bytes
+
+
+def test_numa_pool_roles_one_leader_per_node():
+    from paper_2510_10302_b200.replicas import node_cpus, numa_pool_roles
+
+    nodes = [0, 0, 0, 0, 1, 1, 1, 1]
+    roles = [numa_pool_roles(nodes, r) for r in range(8)]
+    assert [n for n, _ in roles] == nodes
+    assert [r for r, (_, lead) in enumerate(roles) if lead] == [0, 4]
+    # interleaved placement: the lowest local rank on each node leads
+    assert [numa_pool_roles([1, 0, 1, 0], r)[1] for r in range(4)] == [True, True, False, False]
+    assert numa_pool_roles([0], 0) == (0, True)
+    assert len(node_cpus(0)) >= 1 and node_cpus(10_000) == []

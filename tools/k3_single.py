@@ -1,0 +1,79 @@
+"""K3 for ONE late expert (the bench's regime: each demand-loaded expert runs
+alone after its copy lands), Mixtral shapes, 1..4 routed tokens.  Times the
+tcgen05 launcher (static split plan), the fused tcgen05 kernel and the
+CUDA-core kernel with CUDA events, rotating over 8 slots (>= 2.8 GB, no L2
+reuse), each launch preceded by an idle gap (like a stream waiting on a
+copy event).  Usage: python tools/k3_single.py [iters]"""
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+import torch
+
+from paper_2510_10302_b200 import kernels as K
+
+
+def main(iters=20, gap_cycles=20000):
+    H, F = 4096, 14336
+    dev = "cuda"
+    S = 8
+    pool = torch.empty((S, 3 * F * H), dtype=torch.bfloat16, device=dev)
+    K.fill_normal_(pool, 7, 0, 0.02)
+    eb = 3 * F * H * 2
+    sync = torch.zeros((1,), dtype=torch.int32, device=dev)
+    side = torch.cuda.Stream()
+    side_buf = torch.zeros((1024,), device=dev)
+    out = []
+    for T in (1, 2, 3, 4):
+        g = torch.Generator().manual_seed(T)
+        x = torch.randn((T, H), generator=g).to(torch.bfloat16).to(dev)
+        idx = torch.zeros((T, 1), dtype=torch.int32, device=dev)
+        off, perm, inv = K.moe_permute(idx, 1)
+        h = torch.empty((T, F), dtype=torch.bfloat16, device=dev)
+        y = torch.empty((T, H), dtype=torch.float32, device=dev)
+        xp = torch.empty((T, H), dtype=torch.bfloat16, device=dev)
+        su, sd = K.tc_plan_static(H, F)
+        ws = torch.empty((max(1, K.tc_workspace_floats(T, H, F, su, sd)),), dtype=torch.float32, device=dev)
+        act = T * (H * 2 + 2 * F * 2 + H * 4)
+        row = {"T": T, "split": [su, sd], "gap_cycles": gap_cycles}
+        for name in ("tc", "tc_fused", "cuda_core"):
+            ms = []
+            for i in range(iters + 3):
+                slot = i % S
+                if gap_cycles < 0:
+                    # truly idle GPU for |gap| microseconds (empty streams), then
+                    # the launch waits on an event of another stream, as the
+                    # bench's late experts wait on their decode
+                    torch.cuda.synchronize()
+                    time.sleep(-gap_cycles / 1e6)
+                    with torch.cuda.stream(side):
+                        side_buf.add_(1)
+                        ev = torch.cuda.Event()
+                        ev.record(side)
+                    torch.cuda.current_stream().wait_event(ev)
+                else:
+                    torch.cuda._sleep(gap_cycles)  # busy gap
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                if name == "tc":
+                    K.expert_ffn_tc(pool, [slot], 1, x, F, 1, off, perm, xp, h, y, ws, su, sd)
+                elif name == "tc_fused":
+                    K.expert_ffn_tc_fused(pool, [slot], 1, x, F, 1, off, perm, xp, h, y, ws, sd, sync)
+                else:
+                    K.expert_ffn(pool, [slot], 1, x, F, 1, off, perm, h, y, T)
+                b.record()
+                ms.append((a, b))
+            torch.cuda.synchronize()
+            t = [a.elapsed_time(b) for a, b in ms[3:]]
+            med = float(np.median(t))
+            row[name] = {"us": round(med * 1e3, 1), "tbs": round((eb + act) / (med / 1e3) / 1e12, 3)}
+        out.append(row)
+        print(json.dumps(row), flush=True)
+    return out
+
+
+if __name__ == "__main__":
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 20, int(sys.argv[2]) if len(sys.argv) > 2 else 20000)
