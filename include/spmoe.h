@@ -261,43 +261,47 @@ int spmoe_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, uint64_t off
 /*   config.py:229-231), so the bytes per expert set TPOT.  A bf16       */
 /*   weight is sign(1) | exponent(8) | mantissa(7); the exponent of      */
 /*   trained or N(0, s^2) weights has ~2.5 bits of entropy.  XC stores   */
-/*   each value as one sign|mantissa byte plus a 2-bit exponent code     */
-/*   (the 3 most frequent exponents of its segment, code 3 = escape),   */
-/*   escapes as a 4-bit secondary code (the next 15 exponents, 15 =      */
-/*   exception) and exceptions as (position, exponent) words.  Decoding  */
-/*   is exact: decode(encode(x)) == x bit for bit.  Per-value coding     */
-/*   only: no cross-value or cross-expert modelling.                     */
+/*   each value as one sign|mantissa byte                                */
+/*   and the exponent as a per-segment canonical Huffman code (<= 12     */
+/*   bits, 32 independent lane substreams per 4096-value block so a warp */
+/*   decodes a block in parallel).  Decoding is exact: decode(encode(x)) */
+/*   == x bit for bit.  Per-value coding only: no cross-value or         */
+/*   cross-expert modelling.                                             */
 /* --------------------------------------------------------------------- */
-#define SPMOE_XC_MAGIC 0x31435853u /* "SXC1" */
+#define SPMOE_XC_MAGIC 0x32435853u /* "SXC2" */
 #define SPMOE_XC_BLOCK 4096        /* values per coding block */
+#define SPMOE_XC_LANES 32          /* exponent substreams per block */
+#define SPMOE_XC_LMAX 12           /* longest exponent code, bits */
 #define SPMOE_XC_MAX_SEG 4
 
 /*
  * One segment = one weight matrix of n bf16 values (n % SPMOE_XC_BLOCK == 0),
- * nb = n / SPMOE_XC_BLOCK blocks.  Streams (byte offsets from the blob start,
- * each 256-byte aligned):
- *   sm    [n]      u8   (v >> 8 & 0x80) | (v & 0x7f)
- *   pc    [n/16]   u32  word w holds the 2-bit codes of values 16w..16w+15,
- *                       value 16w+j at bits 2j..2j+1; code c < 3 means
- *                       exponent prim[c], 3 = escape
- *   sec   [sec_words] u32  block b's escapes, in value order, as 4-bit codes
- *                       starting at word bsec[b] (nibble q at bits 4(q%8) of
- *                       word bsec[b] + q/8); code c < 15 = exponent sec[c],
- *                       15 = exception
- *   bsec  [nb+1]   u32  first sec word of each block (exclusive prefix)
- *   bexc  [nb+1]   u32  first exception of each block (exclusive prefix)
- *   exc   [n_exc]  u32  (position-in-block << 8) | exponent, ascending
- * Code tables: the segment's exponents ordered by (count desc, exponent asc);
- * prim = ranks 0-2, sec = ranks 3-17.
+ * nb = n / SPMOE_XC_BLOCK blocks.  Exponents are coded with the segment's
+ * canonical Huffman code, lengths len[] (1..SPMOE_XC_LMAX, 0 = exponent
+ * absent) built deterministically from the exponent histogram (two-queue
+ * Huffman, ties to leaves and lower ids; lengths over LMAX capped and the
+ * Kraft excess repaid by lengthening the longest codes under LMAX, rarest
+ * then highest id first; codes assigned in (length, exponent) order).
+ * Streams (byte offsets from the blob start, each 256-byte aligned, in this
+ * order, so a segment's bytes are contiguous from its off_lut):
+ *   lut   [4096]    u16  decode table: entry p (the next 12 code bits, LSB
+ *                        first) = exponent | (code length << 8)
+ *   sm    [n]       u8   (v >> 8 & 0x80) | (v & 0x7f)
+ *   ex    [ex_words] u32 per block, SPMOE_XC_LANES lane substreams back to
+ *                        back; lane l holds the bit-reversed codes of values
+ *                        128 l .. 128 l + 127 of the block, LSB first,
+ *                        padded to a whole word (8 readable slack bytes after
+ *                        the stream)
+ *   bofs  [nb+1]    u32  first ex word of each block (exclusive prefix)
+ *   lanes [nb*32]   u8   word count of each lane substream
+ * Every bf16 bit pattern round-trips (zeros, denormals, inf, NaN).
  */
 typedef struct spmoe_xc_segment {
   uint64_t n;
-  uint64_t off_sm, off_pc, off_sec, off_bsec, off_bexc, off_exc;
-  uint32_t sec_words, n_exc;
-  uint8_t prim[4]; /* [3] unused (0) */
-  uint8_t sec[16]; /* [15] unused (0) */
-  uint32_t pad;
-} spmoe_xc_segment; /* 88 bytes */
+  uint64_t off_lut, off_sm, off_ex, off_bofs, off_lanes;
+  uint32_t ex_words, pad;
+  uint8_t len[256];
+} spmoe_xc_segment; /* 312 bytes */
 
 typedef struct spmoe_xc_header {
   uint32_t magic; /* SPMOE_XC_MAGIC */
@@ -305,7 +309,7 @@ typedef struct spmoe_xc_header {
   uint64_t blob_bytes; /* header + streams (what crosses the host link) */
   uint64_t raw_bytes;  /* 2 * sum(n) */
   spmoe_xc_segment seg[SPMOE_XC_MAX_SEG];
-} spmoe_xc_header; /* 376 bytes; the first stream starts at 512 */
+} spmoe_xc_header; /* 1272 bytes; the first stream starts at 1280 */
 
 /* Device workspace bytes spmoe_xc_plan needs for these segments. */
 size_t spmoe_xc_work_bytes(int nseg, const int64_t* seg_n);

@@ -1,21 +1,24 @@
 /*
  * xc_oracle.c — CPU ORACLE of the XC expert-blob codec (include/spmoe.h,
- * "XC").  TEST INFRASTRUCTURE ONLY: tests/ compare the sm_100a encoder's
- * blob byte for byte against oracle_xc_encode and the decoder's output
- * against the original bits; the product path never links this file.
+ * "XC", format SXC2).  TEST INFRASTRUCTURE ONLY: tests/ compare the sm_100a
+ * encoder's blob byte for byte against oracle_xc_encode and the decoder's
+ * output against the original bits; the product path never links this file.
  *
  * What it restates: the format is this build's (the reference moves raw
  * expert bytes, IoChannel.transfer prefetch.py:45-74), so there is no
  * reference golden vector; parity is pinned by the format's own invariant
  * decode(encode(x)) == x (checked here on CPU too) and by GPU == CPU blob
  * bytes.  Straight-line scalar code in value order:
- *   table  exponents by (count desc, exponent asc); prim = ranks 0-2,
- *          sec = ranks 3-17, anything else an exception;
- *   block  4096 values: sign|mantissa byte, 2-bit code per value, the
- *          block's escape nibbles padded to whole u32 words, exceptions as
- *          (position << 8) | exponent in value order;
- *   layout header at 0, streams at 512 and then every 256-byte boundary in
- *          the order sm, pc, sec, bsec, bexc, exc per segment.
+ *   code   exponent histogram -> two-queue Huffman lengths (ties: leaves
+ *          before internal nodes, lower ids first) -> lengths capped at
+ *          SPMOE_XC_LMAX with the Kraft excess repaid by lengthening the
+ *          longest sub-LMAX code (rarest, then highest id) -> canonical
+ *          codes in (length, exponent) order, written bit-reversed (LSB
+ *          first);
+ *   block  4096 values: sign|mantissa bytes; 32 lane substreams of the
+ *          codes of values 128 l .. 128 l + 127, each padded to a word;
+ *   layout header at 0, streams from 1280 on 256-byte boundaries in the
+ *          order lut, sm, ex (+ 8 slack bytes), bofs, lanes per segment.
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -23,39 +26,105 @@
 
 #include "../include/spmoe.h"
 
+#define LMAX SPMOE_XC_LMAX
+#define LANES SPMOE_XC_LANES
+#define PER_LANE (SPMOE_XC_BLOCK / LANES)
+
 static uint64_t a256(uint64_t x) { return (x + 255) & ~(uint64_t)255; }
 
-static void tables(const uint16_t* v, int64_t n, spmoe_xc_segment* g, uint8_t lut[256]) {
-  uint64_t hist[256];
-  memset(hist, 0, sizeof(hist));
-  for (int64_t i = 0; i < n; ++i) hist[(v[i] >> 7) & 0xff]++;
-  int order[256];
-  for (int i = 0; i < 256; ++i) order[i] = i;
-  /* insertion sort: count desc, exponent asc (stable on ascending ids) */
-  for (int i = 1; i < 256; ++i) {
-    int x = order[i], j = i - 1;
-    while (j >= 0 && hist[order[j]] < hist[x]) {
-      order[j + 1] = order[j];
+void oracle_xc_code_lengths(const uint64_t cnt[256], uint8_t len[256]) {
+  memset(len, 0, 256);
+  int sym[256], n = 0;
+  for (int s = 0; s < 256; ++s)
+    if (cnt[s]) sym[n++] = s;
+  if (n == 0) return;
+  if (n == 1) {
+    len[sym[0]] = 1;
+    return;
+  }
+  /* leaves sorted by (count asc, id asc): insertion sort, stable */
+  for (int i = 1; i < n; ++i) {
+    int x = sym[i], j = i - 1;
+    while (j >= 0 && cnt[sym[j]] > cnt[x]) {
+      sym[j + 1] = sym[j];
       --j;
     }
-    order[j + 1] = x;
+    sym[j + 1] = x;
   }
-  memset(g->prim, 0, sizeof(g->prim));
-  memset(g->sec, 0, sizeof(g->sec));
-  for (int i = 0; i < 256; ++i) lut[i] = (15 << 2) | 3;
-  for (int r = 0; r < 3; ++r) {
-    g->prim[r] = (uint8_t)order[r];
-    lut[order[r]] = (uint8_t)r;
+  uint64_t w[511];
+  int parent[511], depth[511];
+  for (int i = 0; i < n; ++i) w[i] = cnt[sym[i]];
+  int li = 0, ii = n, next = n;
+  for (int k = 0; k < n - 1; ++k) {
+    int pick[2];
+    for (int t = 0; t < 2; ++t) {
+      if (li < n && (ii == next || w[li] <= w[ii])) pick[t] = li++;
+      else pick[t] = ii++;
+    }
+    w[next] = w[pick[0]] + w[pick[1]];
+    parent[pick[0]] = parent[pick[1]] = next;
+    ++next;
   }
-  for (int r = 0; r < 15; ++r) {
-    g->sec[r] = (uint8_t)order[3 + r];
-    lut[order[3 + r]] = (uint8_t)((r << 2) | 3);
+  const int root = 2 * n - 2;
+  depth[root] = 0;
+  for (int v = root - 1; v >= 0; --v) depth[v] = depth[parent[v]] + 1;
+  int maxlen = 0;
+  for (int i = 0; i < n; ++i) {
+    const int d = depth[i];
+    len[sym[i]] = (uint8_t)(d > 255 ? 255 : d);
+    if (d > maxlen) maxlen = d;
+  }
+  if (maxlen <= LMAX) return;
+  int64_t kraft = 0;
+  for (int s = 0; s < 256; ++s) {
+    if (!len[s]) continue;
+    if (len[s] > LMAX) len[s] = LMAX;
+    kraft += (int64_t)1 << (LMAX - len[s]);
+  }
+  while (kraft > ((int64_t)1 << LMAX)) {
+    int best = -1;
+    for (int s = 0; s < 256; ++s) {
+      if (!len[s] || len[s] >= LMAX) continue;
+      if (best < 0 || len[s] > len[best] ||
+          (len[s] == len[best] && (cnt[s] < cnt[best] || (cnt[s] == cnt[best] && s > best))))
+        best = s;
+    }
+    kraft -= (int64_t)1 << (LMAX - len[best] - 1);
+    len[best]++;
+  }
+}
+
+/* canonical codes, bit-reversed for LSB-first packing */
+static void rev_codes(const uint8_t len[256], uint16_t rev[256]) {
+  memset(rev, 0, 512);
+  uint32_t code = 0;
+  int prev = 0;
+  for (int L = 1; L <= LMAX; ++L)
+    for (int s = 0; s < 256; ++s) {
+      if (len[s] != L) continue;
+      if (prev) code <<= (L - prev);
+      prev = L;
+      uint32_t r = 0;
+      for (int b = 0; b < L; ++b) r |= ((code >> b) & 1u) << (L - 1 - b);
+      rev[s] = (uint16_t)r;
+      ++code;
+    }
+}
+
+void oracle_xc_lut(const uint8_t len[256], uint16_t lut[1 << LMAX]) {
+  uint16_t rev[256];
+  rev_codes(len, rev);
+  memset(lut, 0, sizeof(uint16_t) << LMAX);
+  for (int s = 0; s < 256; ++s) {
+    const int L = len[s];
+    if (!L) continue;
+    for (uint32_t q = 0; q < (1u << (LMAX - L)); ++q) lut[rev[s] | (q << L)] = (uint16_t)(s | (L << 8));
   }
 }
 
 /* Encode nseg segments (back to back in src).  Returns the blob size; the
- * blob is written only if out != NULL and cap >= size.  hdr (nullable)
- * receives the header.  0 on invalid segment sizes. */
+ * blob is written only if out != NULL and cap >= size.  0 on invalid
+ * segment sizes. */
 uint64_t oracle_xc_encode(const uint16_t* src, int nseg, const int64_t* seg_n, uint8_t* out, uint64_t cap,
                           spmoe_xc_header* hdr_out) {
   if (nseg < 1 || nseg > SPMOE_XC_MAX_SEG) return 0;
@@ -65,33 +134,32 @@ uint64_t oracle_xc_encode(const uint16_t* src, int nseg, const int64_t* seg_n, u
   memset(&hdr, 0, sizeof(hdr));
   hdr.magic = SPMOE_XC_MAGIC;
   hdr.nseg = (uint32_t)nseg;
-  uint8_t luts[SPMOE_XC_MAX_SEG][256];
-  /* pass 1: tables, counts, layout */
+  uint16_t revs[SPMOE_XC_MAX_SEG][256];
+  /* pass 1: codes, sizes, layout */
   const uint16_t* s = src;
-  uint64_t pos = 512, raw = 0;
+  uint64_t pos = a256(sizeof(spmoe_xc_header)), raw = 0;
   for (int i = 0; i < nseg; ++i) {
     spmoe_xc_segment* g = &hdr.seg[i];
     const int64_t n = seg_n[i], nb = n / SPMOE_XC_BLOCK;
-    tables(s, n, g, luts[i]);
+    uint64_t cnt[256];
+    memset(cnt, 0, sizeof(cnt));
+    for (int64_t k = 0; k < n; ++k) cnt[(s[k] >> 7) & 0xff]++;
+    oracle_xc_code_lengths(cnt, g->len);
+    rev_codes(g->len, revs[i]);
     g->n = (uint64_t)n;
-    uint64_t words = 0, exc = 0;
-    for (int64_t b = 0; b < nb; ++b) {
-      uint64_t c = 0;
-      for (int64_t j = 0; j < SPMOE_XC_BLOCK; ++j) {
-        const uint8_t l = luts[i][(s[b * SPMOE_XC_BLOCK + j] >> 7) & 0xff];
-        if ((l & 3) == 3) ++c;
-        if (l == ((15 << 2) | 3)) ++exc;
+    uint64_t words = 0;
+    for (int64_t b = 0; b < nb; ++b)
+      for (int l = 0; l < LANES; ++l) {
+        uint64_t bits = 0;
+        for (int j = 0; j < PER_LANE; ++j) bits += g->len[(s[b * SPMOE_XC_BLOCK + l * PER_LANE + j] >> 7) & 0xff];
+        words += (bits + 31) / 32;
       }
-      words += (c + 7) / 8;
-    }
-    g->sec_words = (uint32_t)words;
-    g->n_exc = (uint32_t)exc;
+    g->ex_words = (uint32_t)words;
+    g->off_lut = pos; pos = a256(pos + (2u << LMAX));
     g->off_sm = pos; pos = a256(pos + (uint64_t)n);
-    g->off_pc = pos; pos = a256(pos + (uint64_t)n / 4);
-    g->off_sec = pos; pos = a256(pos + words * 4);
-    g->off_bsec = pos; pos = a256(pos + (uint64_t)(nb + 1) * 4);
-    g->off_bexc = pos; pos = a256(pos + (uint64_t)(nb + 1) * 4);
-    g->off_exc = pos; pos = a256(pos + exc * 4);
+    g->off_ex = pos; pos = a256(pos + words * 4 + 8);
+    g->off_bofs = pos; pos = a256(pos + (uint64_t)(nb + 1) * 4);
+    g->off_lanes = pos; pos = a256(pos + (uint64_t)nb * LANES);
     raw += 2 * (uint64_t)n;
     s += n;
   }
@@ -106,33 +174,36 @@ uint64_t oracle_xc_encode(const uint16_t* src, int nseg, const int64_t* seg_n, u
   for (int i = 0; i < nseg; ++i) {
     const spmoe_xc_segment* g = &hdr.seg[i];
     const int64_t n = (int64_t)g->n, nb = n / SPMOE_XC_BLOCK;
+    oracle_xc_lut(g->len, (uint16_t*)(out + g->off_lut));
     uint8_t* sm = out + g->off_sm;
-    uint32_t* pc = (uint32_t*)(out + g->off_pc);
-    uint32_t* sec = (uint32_t*)(out + g->off_sec);
-    uint32_t* bsec = (uint32_t*)(out + g->off_bsec);
-    uint32_t* bexc = (uint32_t*)(out + g->off_bexc);
-    uint32_t* exc = (uint32_t*)(out + g->off_exc);
-    uint32_t w = 0, x = 0;
+    uint32_t* ex = (uint32_t*)(out + g->off_ex);
+    uint32_t* bofs = (uint32_t*)(out + g->off_bofs);
+    uint8_t* lanes = out + g->off_lanes;
+    uint32_t w = 0;
     for (int64_t b = 0; b < nb; ++b) {
-      bsec[b] = w;
-      bexc[b] = x;
-      uint32_t q = 0;
-      for (int64_t j = 0; j < SPMOE_XC_BLOCK; ++j) {
-        const int64_t idx = b * SPMOE_XC_BLOCK + j;
-        const uint16_t v = s[idx];
-        const uint8_t l = luts[i][(v >> 7) & 0xff];
-        sm[idx] = (uint8_t)(((v >> 8) & 0x80) | (v & 0x7f));
-        pc[idx / 16] |= (uint32_t)(l & 3) << (2 * (idx % 16));
-        if ((l & 3) == 3) {
-          sec[w + q / 8] |= (uint32_t)(l >> 2) << (4 * (q % 8));
-          ++q;
-          if (l == ((15 << 2) | 3)) exc[x++] = ((uint32_t)j << 8) | ((v >> 7) & 0xff);
+      bofs[b] = w;
+      for (int l = 0; l < LANES; ++l) {
+        uint64_t buf = 0;
+        int nbits = 0;
+        const uint32_t w0 = w;
+        for (int j = 0; j < PER_LANE; ++j) {
+          const int64_t k = b * SPMOE_XC_BLOCK + l * PER_LANE + j;
+          const uint16_t v = s[k];
+          const int e = (v >> 7) & 0xff;
+          sm[k] = (uint8_t)(((v >> 8) & 0x80) | (v & 0x7f));
+          buf |= (uint64_t)revs[i][e] << nbits;
+          nbits += g->len[e];
+          if (nbits >= 32) {
+            ex[w++] = (uint32_t)buf;
+            buf >>= 32;
+            nbits -= 32;
+          }
         }
+        if (nbits > 0) ex[w++] = (uint32_t)buf;
+        lanes[b * LANES + l] = (uint8_t)(w - w0);
       }
-      w += (q + 7) / 8;
     }
-    bsec[nb] = w;
-    bexc[nb] = x;
+    bofs[nb] = w;
     s += n;
   }
   return pos;
@@ -148,33 +219,34 @@ int oracle_xc_decode(const uint8_t* blob, uint16_t* dst) {
     const spmoe_xc_segment* g = &hdr.seg[i];
     const int64_t n = (int64_t)g->n, nb = n / SPMOE_XC_BLOCK;
     if (n <= 0 || n % SPMOE_XC_BLOCK) return 1;
+    const uint16_t* lut = (const uint16_t*)(blob + g->off_lut);
     const uint8_t* sm = blob + g->off_sm;
-    const uint32_t* pc = (const uint32_t*)(blob + g->off_pc);
-    const uint32_t* sec = (const uint32_t*)(blob + g->off_sec);
-    const uint32_t* bsec = (const uint32_t*)(blob + g->off_bsec);
-    const uint32_t* bexc = (const uint32_t*)(blob + g->off_bexc);
-    const uint32_t* exc = (const uint32_t*)(blob + g->off_exc);
+    const uint32_t* ex = (const uint32_t*)(blob + g->off_ex);
+    const uint32_t* bofs = (const uint32_t*)(blob + g->off_bofs);
+    const uint8_t* lanes = blob + g->off_lanes;
     for (int64_t b = 0; b < nb; ++b) {
-      uint32_t q = 0, x = bexc[b];
-      for (int64_t j = 0; j < SPMOE_XC_BLOCK; ++j) {
-        const int64_t idx = b * SPMOE_XC_BLOCK + j;
-        const uint32_t c = (pc[idx / 16] >> (2 * (idx % 16))) & 3;
-        uint32_t e;
-        if (c < 3) {
-          e = g->prim[c];
-        } else {
-          const uint32_t nib = (sec[bsec[b] + q / 8] >> (4 * (q % 8))) & 15;
-          ++q;
-          if (nib < 15) {
-            e = g->sec[nib];
-          } else {
-            if (x >= bexc[b + 1] || (exc[x] >> 8) != (uint32_t)j) return 1;
-            e = exc[x++] & 0xff;
+      uint32_t w = bofs[b];
+      for (int l = 0; l < LANES; ++l) {
+        const uint32_t* p = ex + w;
+        uint64_t buf = (uint64_t)p[0] | ((uint64_t)p[1] << 32);
+        int nbits = 64, r = 2;
+        for (int j = 0; j < PER_LANE; ++j) {
+          const uint16_t e = lut[buf & ((1u << LMAX) - 1)];
+          const int L = e >> 8;
+          if (L == 0) return 1;
+          buf >>= L;
+          nbits -= L;
+          if (nbits < 32) {
+            buf |= (uint64_t)p[r++] << nbits;
+            nbits += 32;
           }
+          const int64_t k = b * SPMOE_XC_BLOCK + l * PER_LANE + j;
+          const uint8_t bb = sm[k];
+          d[k] = (uint16_t)(((bb & 0x80) << 8) | ((e & 0xff) << 7) | (bb & 0x7f));
         }
-        const uint8_t bb = sm[idx];
-        d[idx] = (uint16_t)(((bb & 0x80) << 8) | (e << 7) | (bb & 0x7f));
+        w += lanes[b * LANES + l];
       }
+      if (w != bofs[b + 1]) return 1;
     }
     d += n;
   }

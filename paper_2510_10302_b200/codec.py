@@ -2,11 +2,11 @@
 
 The offload tier's cost is bytes over PCIe (``IoChannel.transfer``,
 ``prefetch.py:45-74``; ``t_io = size / bw + overhead``, ``config.py:229-231``).
-XC (format in ``include/spmoe.h``) stores each bf16 weight as its
-sign|mantissa byte plus a 2-bit exponent code, with a 4-bit secondary code
-for exponents outside the segment's top three and exact exceptions beyond
-that, so a routed expert crosses the link as ~69 % of its raw bytes and is
-expanded bit-exactly into its HBM slot by the copy path's decode kernel.
+XC (format SXC2 in ``include/spmoe.h``) stores each bf16 weight as its
+sign|mantissa byte plus its exponent in the segment's canonical Huffman code
+(<= 12 bits, 32 lane substreams per 4096-value block), so a routed expert
+crosses the link as ~67.5 % of its raw bytes and is expanded bit-exactly
+into its HBM slot by the copy path's warp-per-block decode kernel.
 Only the encoder orchestration lives here; encode / decode run on the GPU
 (``csrc/spmoe_codec.cu``), there is no CPU codec in the product.
 """
@@ -21,7 +21,7 @@ import torch
 
 from . import _native
 
-XC_MAGIC = 0x31435853
+XC_MAGIC = 0x32435853  # "SXC2"
 XC_BLOCK = 4096
 XC_MAX_SEG = 4
 
@@ -29,17 +29,14 @@ XC_MAX_SEG = 4
 class XcSegment(C.Structure):
     _fields_ = [
         ("n", C.c_uint64),
+        ("off_lut", C.c_uint64),
         ("off_sm", C.c_uint64),
-        ("off_pc", C.c_uint64),
-        ("off_sec", C.c_uint64),
-        ("off_bsec", C.c_uint64),
-        ("off_bexc", C.c_uint64),
-        ("off_exc", C.c_uint64),
-        ("sec_words", C.c_uint32),
-        ("n_exc", C.c_uint32),
-        ("prim", C.c_uint8 * 4),
-        ("sec", C.c_uint8 * 16),
+        ("off_ex", C.c_uint64),
+        ("off_bofs", C.c_uint64),
+        ("off_lanes", C.c_uint64),
+        ("ex_words", C.c_uint32),
         ("pad", C.c_uint32),
+        ("len", C.c_uint8 * 256),
     ]
 
 
@@ -53,7 +50,7 @@ class XcHeader(C.Structure):
     ]
 
 
-assert C.sizeof(XcSegment) == 88 and C.sizeof(XcHeader) == 376
+assert C.sizeof(XcSegment) == 312 and C.sizeof(XcHeader) == 1272
 
 
 def expert_segments(ffn: int, hidden: int) -> list[int]:

@@ -230,8 +230,9 @@ struct spmoe_rt {
     if (st == cudaSuccess && read_rec[s]) st = cudaStreamWaitEvent(decode_stream, read_ev[s], 0);
     uint16_t* dst = (uint16_t*)(dev_pool + (size_t)s * slot_bytes);
     for (int g = 0; g < ns && st == cudaSuccess; ++g) {
-      const uint64_t lo = g == 0 ? 0 : h->seg[g].off_sm;
-      const uint64_t hi = g + 1 < ns ? h->seg[g + 1].off_sm : h->blob_bytes;
+      // a segment's streams are contiguous from its decode table on
+      const uint64_t lo = g == 0 ? 0 : h->seg[g].off_lut;
+      const uint64_t hi = g + 1 < ns ? h->seg[g + 1].off_lut : h->blob_bytes;
       cudaEvent_t full = stage_full[i * SPMOE_XC_MAX_SEG + g];
       st = cudaMemcpyAsync(staging[i] + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, copy_stream);
       if (st == cudaSuccess) st = cudaEventRecord(full, copy_stream);

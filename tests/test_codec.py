@@ -60,7 +60,7 @@ def test_oracle_round_trip(oracle, kind):
         segs = [BLOCK, BLOCK, BLOCK]
     blob = oracle.xc_encode(x, segs)
     magic, nseg, blob_bytes, raw_bytes = header_fields(blob)
-    assert magic == 0x31435853 and nseg == len(segs)
+    assert magic == 0x32435853 and nseg == len(segs)
     assert blob_bytes == blob.size and raw_bytes == 2 * x.size
     assert np.array_equal(oracle.xc_decode(blob), x)
 
@@ -69,8 +69,8 @@ def test_oracle_gaussian_ratio(oracle):
     x = gaussian_bits(3 * 64 * BLOCK)
     blob = oracle.xc_encode(x, [64 * BLOCK] * 3)
     ratio = blob.size / (2 * x.size)
-    # 8 + 2 + 0.27 * 4 bits per value (+ block tables) ~ 0.70
-    assert ratio < 0.72, ratio
+    # 8 + ~2.58 (Huffman exponent) + lane padding and counts bits per value
+    assert ratio < 0.70, ratio
 
 
 def test_oracle_rejects_partial_blocks(oracle):
@@ -83,7 +83,7 @@ def test_codec_header_struct_layout():
 
     from paper_2510_10302_b200.codec import XcHeader, XcSegment, codec_applies, expert_segments
 
-    assert C.sizeof(XcSegment) == 88 and C.sizeof(XcHeader) == 376
+    assert C.sizeof(XcSegment) == 312 and C.sizeof(XcHeader) == 1272
     assert codec_applies(expert_segments(14336, 4096)) and codec_applies(expert_segments(512, 256))
     assert not codec_applies([BLOCK + 1]) and not codec_applies([BLOCK] * 5)
 
@@ -147,7 +147,7 @@ def test_gpu_full_mixtral_expert_round_trip(native):
     enc = X.XcEncoder(X.expert_segments(a.ffn, a.hidden), "cuda")
     hdr = enc.plan(src)
     blob = enc.encode(src, hdr)
-    assert int(hdr.blob_bytes) < 0.72 * a.expert_bytes
+    assert int(hdr.blob_bytes) < 0.69 * a.expert_bytes
     out = torch.empty_like(src)
     X.decode(blob, hdr, out)
     torch.cuda.synchronize()

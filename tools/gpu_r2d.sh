@@ -15,6 +15,6 @@ for f in ("gpurun_out/bench_xc.json", "gpurun_out/bench_raw.json", "gpurun_out/b
     except Exception as e:
         print(f, "ERR", e)
 PY
-SPMOE_PROFILE_RANGE=1 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_xc.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/bench_ncu.json 2> gpurun_out/bench_ncu.err; tail -1 gpurun_out/bench_ncu.err
+SPMOE_PROFILE_RANGE=1 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_xc.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --cutoff 1 > gpurun_out/bench_ncu.json 2> gpurun_out/bench_ncu.err; tail -1 gpurun_out/bench_ncu.err
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()"
 echo done
