@@ -337,6 +337,9 @@ def main():
     eng.cache.reset_stats()
     eng.cache.clear_log()
     eng.time_k3 = True
+    if eng.host_pool.codec:
+        eng.cache.decode_stats()  # drop warm-up records
+        eng.cache.decode_timing(True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -365,6 +368,7 @@ def main():
     dev_ms = e0.elapsed_time(e1)
     rep = eng.report(wall_s=wall)
     roof = eng.k3_roofline()
+    dec = eng.cache.decode_stats() if eng.host_pool.codec else None
     stats = torch.tensor([dev_ms, wall, float(emitted)], dtype=torch.float64, device="cuda")
     if world > 1:
         mx = stats.clone()
@@ -448,8 +452,18 @@ def main():
             "ms_per_launch": roof.get("ms_per_launch"),
             "by_shape": roof.get("by_shape"),
         },
+        # the copy path's XC decode kernel (largest GPU-time share of the
+        # step in the ncu launch list; runs under the copies of later segments)
+        "roofline_decode": None if not dec or not dec["launches"] else {
+            "kernel": "xc_decode_kernel (XC blob -> raw expert bf16, per segment)",
+            "bound": "hbm", "achieved": dec["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": (dec["gbs"] or 0.0) / peaks["hbm_gbs"], "launches": dec["launches"],
+            "ms_per_step": dec["ms"] / args.steps,
+            "bytes_per_launch": dec["bytes"] / dec["launches"],
+        },
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": d2h_step},
-        "gpu_launches": launches,
+        # Python-issued kernels (K.LAUNCHES) + the runtime's XC decodes
+        "gpu_launches": launches + (dec["launches"] if dec else 0),
         "clocks": clk,
     }
     prof = ROOT / "profiles" / "ncu_k3_traffic.json"

@@ -460,6 +460,13 @@ double spmoe_rt_transfer_copy_end_ms(spmoe_rt* rt, int i);
  */
 int spmoe_rt_set_codec(spmoe_rt* rt, size_t row_stride, void* staging, size_t staging_bytes,
                        int n_staging, void* decode_stream);
+/* Profiling hook: with enable != 0, every XC segment decode issued from now
+ * on is bracketed by timing events on the decode stream. */
+int spmoe_rt_decode_timing(spmoe_rt* rt, int enable);
+/* Sum of the timed decode durations (ms), the bytes they read (blob) plus
+ * wrote (raw), and their count since the last call; clears the record
+ * (synchronizes on the recorded events). */
+int spmoe_rt_decode_stats(spmoe_rt* rt, double* ms, int64_t* bytes, int64_t* launches);
 /* Host-link bytes since the last reset: {prefetch, demand}. */
 void spmoe_rt_wire_bytes(spmoe_rt* rt, int64_t* out2);
 

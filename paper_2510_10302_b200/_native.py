@@ -82,6 +82,8 @@ SIGNATURES: dict[str, tuple] = {
     "spmoe_rt_transfer_copy_end_ms": (C.c_double, [_p, _i]),
     "spmoe_rt_set_codec": (_i, [_p, _sz, _p, _sz, _i, _p]),
     "spmoe_rt_wire_bytes": (None, [_p, _p]),
+    "spmoe_rt_decode_timing": (_i, [_p, _i]),
+    "spmoe_rt_decode_stats": (_i, [_p, _p, _p, _p]),
     "spmoe_xc_work_bytes": (_sz, [_i, _p]),
     "spmoe_xc_plan": (_i, [_p, _i, _p, _p, _p, _p]),
     "spmoe_xc_encode": (_i, [_p, _p, _p, _p, _p]),

@@ -353,6 +353,18 @@ class NativeExpertCache:
         _native.check("spmoe_rt_set_codec", self._lib.spmoe_rt_set_codec(
             self._h, row_stride, staging_ptr, staging_bytes, n_staging, decode_stream_ptr))
 
+    def decode_timing(self, enable: bool) -> None:
+        """Bracket every XC segment decode with timing events (profiling)."""
+        self._lib.spmoe_rt_decode_timing(self._h, 1 if enable else 0)
+
+    def decode_stats(self) -> dict:
+        """Timed decodes since the last call: total ms, bytes read + written,
+        launches, achieved GB/s."""
+        ms, b, n = C.c_double(), C.c_int64(), C.c_int64()
+        self._lib.spmoe_rt_decode_stats(self._h, C.byref(ms), C.byref(b), C.byref(n))
+        return {"ms": ms.value, "bytes": b.value, "launches": n.value,
+                "gbs": (b.value / (ms.value / 1e3) / 1e9) if ms.value > 0 else None}
+
     def wire_bytes(self) -> dict[str, int]:
         """Bytes that crossed the host link since the last reset."""
         o = (C.c_int64 * 2)()

@@ -210,19 +210,48 @@ constexpr int kStageWords = 768;
 constexpr int kDecWarps = 4;
 constexpr int kDecThreads = 32 * kDecWarps;
 constexpr int kWarpSmemWords = kStageWords + 2 + kLanes * kPitch;
-constexpr int kDecSmemBytes = 2 * kLutSize + kDecWarps * kWarpSmemWords * 4;
+constexpr int kDecSmemBytes = 4 * kLutSize + kDecWarps * kWarpSmemWords * 4;
+static_assert(kDecWarps * kWarpSmemWords * 4 >= 2 * kLutSize, "lut1 is built in the warp buffers");
 
 // grid.y = segment; each warp decodes whole blocks of its segment.
 __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
-  uint16_t* s_lut = reinterpret_cast<uint16_t*>(dsm);
+  // multi-symbol table: entry p (12 peeked bits) = up to three whole codes:
+  // sym0 | sym1 << 8 | sym2 << 16 | count << 24 | bits << 26
+  uint32_t* s_lut2 = reinterpret_cast<uint32_t*>(dsm);
+  uint8_t* wbase = dsm + 4 * kLutSize;
   const DecSeg& S = p.seg[blockIdx.y];
-  for (int i = threadIdx.x; i < kLutSize / 8; i += kDecThreads)
-    reinterpret_cast<uint4*>(s_lut)[i] = __ldg(reinterpret_cast<const uint4*>(S.lut) + i);
-  __syncthreads();
+  {
+    // the blob's single-symbol table (exponent | length << 8), parked in the
+    // warp buffers while the multi-symbol table is derived from it
+    uint16_t* s_lut = reinterpret_cast<uint16_t*>(wbase);
+    for (int i = threadIdx.x; i < kLutSize / 8; i += kDecThreads)
+      reinterpret_cast<uint4*>(s_lut)[i] = __ldg(reinterpret_cast<const uint4*>(S.lut) + i);
+    __syncthreads();
+    for (int q = threadIdx.x; q < kLutSize; q += kDecThreads) {
+      const uint32_t e0 = s_lut[q];
+      uint32_t tot = e0 >> 8, cnt = 1, syms = e0 & 0xffu;
+      if (tot == 0) tot = 1;  // unused pattern of an incomplete code: always progress
+      const uint32_t e1 = s_lut[(uint32_t)q >> tot], l1 = e1 >> 8;
+      if (l1 && tot + l1 <= (uint32_t)kLmax) {
+        syms |= (e1 & 0xffu) << 8;
+        cnt = 2;
+        tot += l1;
+        const uint32_t e2 = s_lut[(uint32_t)q >> tot], l2 = e2 >> 8;
+        if (l2 && tot + l2 <= (uint32_t)kLmax) {
+          syms |= (e2 & 0xffu) << 16;
+          cnt = 3;
+          tot += l2;
+        }
+      }
+      s_lut2[q] = syms | (cnt << 24) | (tot << 26);
+    }
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* stage = reinterpret_cast<uint32_t*>(dsm + 2 * kLutSize) + warp * kWarpSmemWords;
+  uint32_t* stage = reinterpret_cast<uint32_t*>(wbase) + warp * kWarpSmemWords;
   uint32_t* ew = stage + kStageWords + 2;
+  uint8_t* eb8 = reinterpret_cast<uint8_t*>(ew) + lane * (4 * kPitch);  // this lane's exponent row
   for (uint32_t blk = blockIdx.x * kDecWarps + warp; blk < S.nblk; blk += gridDim.x * kDecWarps) {
     // this lane's substream: block start + words of the lanes before it
     const uint32_t words = __ldg(S.lanes + (uint64_t)blk * kLanes + lane);
@@ -266,22 +295,21 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
     uint64_t buf = (uint64_t)wp[0] | ((uint64_t)wp[1] << 32);
     int nbits = 64;
     wp += 2;
-#pragma unroll 4
-    for (int q = 0; q < kPerLane / 4; ++q) {
-      uint32_t e4 = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t e = s_lut[(uint32_t)buf & (kLutSize - 1)];
-        const int L = (int)(e >> 8);
-        e4 |= (e & 0xffu) << (8 * j);
-        buf >>= L;
-        nbits -= L;
-        if (nbits < 32) {
-          buf |= (uint64_t)(*wp++) << nbits;
-          nbits += 32;
-        }
+    // up to three exponents per lookup; a row has 4 slack bytes past its
+    // 128 for the last lookup's extra symbols
+    for (int k = 0; k < kPerLane;) {
+      const uint32_t e = s_lut2[(uint32_t)buf & (kLutSize - 1)];
+      const int L = (int)(e >> 26), c = (int)((e >> 24) & 3u);
+      eb8[k] = (uint8_t)e;
+      eb8[k + 1] = (uint8_t)(e >> 8);
+      eb8[k + 2] = (uint8_t)(e >> 16);
+      k += c;
+      buf >>= L;
+      nbits -= L;
+      if (nbits < 32) {
+        buf |= (uint64_t)(*wp++) << nbits;
+        nbits += 32;
       }
-      ew[lane * kPitch + q] = e4;
     }
     __syncwarp();
     // assembly: 16 rounds of 8 consecutive values per lane, 16-byte stores

@@ -84,6 +84,14 @@ struct spmoe_rt {
   std::vector<char> stage_used;
   int stage_next = 0;
   cudaStream_t decode_stream = nullptr;
+  // optional decode-kernel timing (spmoe_rt_decode_timing): event pairs
+  // around each segment decode, with the bytes it read (blob) and wrote
+  bool time_decode = false;
+  struct DecodeTiming {
+    cudaEvent_t a, b;
+    int64_t bytes;
+  };
+  std::vector<DecodeTiming> dec_times;
 
   // counters
   int64_t hits = 0, misses = 0, evictions = 0, prefetch_evictions = 0, prefetch_insertions = 0,
@@ -237,8 +245,19 @@ struct spmoe_rt {
       st = cudaMemcpyAsync(staging[i] + lo, src + lo, hi - lo, cudaMemcpyHostToDevice, copy_stream);
       if (st == cudaSuccess) st = cudaEventRecord(full, copy_stream);
       if (st == cudaSuccess) st = cudaStreamWaitEvent(decode_stream, full, 0);
+      DecodeTiming dt{nullptr, nullptr, 0};
+      if (st == cudaSuccess && time_decode) {
+        cudaEventCreate(&dt.a);
+        cudaEventCreate(&dt.b);
+        dt.bytes = (int64_t)(hi - lo) + 2 * (int64_t)h->seg[g].n;
+        st = cudaEventRecord(dt.a, decode_stream);
+      }
       if (st == cudaSuccess)
         st = (cudaError_t)spmoe_xc_decode_segments((const uint8_t*)staging[i], h, g, 1, dst, decode_stream);
+      if (st == cudaSuccess && time_decode) {
+        st = cudaEventRecord(dt.b, decode_stream);
+        dec_times.push_back(dt);
+      }
     }
     if (st == cudaSuccess) st = cudaEventRecord(stage_free[i], decode_stream);
     stage_used[i] = 1;
@@ -537,6 +556,36 @@ int spmoe_rt_set_codec(spmoe_rt* rt, size_t row_stride, void* staging, size_t st
     rt->stage_free.push_back(b);
     rt->stage_used.push_back(0);
   }
+  return 0;
+}
+
+int spmoe_rt_decode_timing(spmoe_rt* rt, int enable) {
+  if (!rt) return (int)cudaErrorInvalidValue;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  rt->time_decode = enable != 0;
+  return 0;
+}
+
+int spmoe_rt_decode_stats(spmoe_rt* rt, double* ms_out, int64_t* bytes_out, int64_t* launches_out) {
+  if (!rt) return (int)cudaErrorInvalidValue;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  double ms = 0.0;
+  int64_t bytes = 0, n = 0;
+  for (auto& t : rt->dec_times) {
+    cudaEventSynchronize(t.b);
+    float x = 0.0f;
+    if (cudaEventElapsedTime(&x, t.a, t.b) == cudaSuccess) {
+      ms += x;
+      bytes += t.bytes;
+      ++n;
+    }
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  rt->dec_times.clear();
+  if (ms_out) *ms_out = ms;
+  if (bytes_out) *bytes_out = bytes;
+  if (launches_out) *launches_out = n;
   return 0;
 }
 

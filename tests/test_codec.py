@@ -185,6 +185,7 @@ def test_runtime_xc_tier_lands_exact_experts(oracle, native):
                           slot_bytes=slot_bytes, copy_stream_ptr=copy.cuda_stream)
     try:
         c.set_codec(stride, staging.data_ptr(), stride, 2, dec.cuda_stream)
+        c.decode_timing(True)
         cur = torch.cuda.current_stream().cuda_stream
         for l, e in [(0, 1), (1, 3), (0, 2), (1, 0), (0, 1), (1, 2)]:
             s = c.demand_load([ExpertId(l, e)])[0]
@@ -199,6 +200,11 @@ def test_runtime_xc_tier_lands_exact_experts(oracle, native):
         assert wire["demand"] == sum(blobs[l * E + e].size for l, e in seq)
         log = c.transfer_log()
         assert all(r["wire_bytes"] < slot_bytes for r in log)
+        # one timed decode per segment of every load; bytes = blob + raw
+        st = c.decode_stats()
+        assert st["launches"] == 3 * len(seq) and st["ms"] > 0
+        assert st["bytes"] == wire["demand"] + len(seq) * slot_bytes
+        assert c.decode_stats()["launches"] == 0
     finally:
         torch.cuda.synchronize()
         c.close()

@@ -37,7 +37,8 @@ def main(iters=12):
     hsrc = torch.empty((244 << 20,), dtype=torch.uint8).pin_memory()
     hdst = torch.empty((244 << 20,), dtype=torch.uint8, device=dev)
     cp = torch.cuda.Stream()
-    for mode in ("prequeued_w2", "prequeued_h2d", "prequeued_w2_h2d", "busy", "prequeued", "prequeued_big", "idle", "idle_event", "idle_small_first", "idle_big_first",
+    small_dst = torch.empty((8 << 20,), dtype=torch.uint8, device=dev)
+    for mode in ("prequeued_h2d_l2ring", "prequeued_w2", "prequeued_h2d", "prequeued_w2_h2d", "busy", "prequeued", "prequeued_big", "idle", "idle_event", "idle_small_first", "idle_big_first",
                  "idle_spin_side"):
         ts = []
         for i in range(iters + 2):
@@ -60,6 +61,12 @@ def main(iters=12):
                     cp.wait_event(ev)
                     with torch.cuda.stream(cp):
                         hdst.copy_(hsrc, non_blocking=True)
+                if mode == "prequeued_h2d_l2ring":
+                    # same bytes, landing in one 8 MB (L2-resident) buffer
+                    cp.wait_event(ev)
+                    with torch.cuda.stream(cp):
+                        for c in range(30):
+                            small_dst.copy_(hsrc[c << 23:(c + 1) << 23], non_blocking=True)
                 torch.cuda.current_stream().wait_event(ev)
             else:
                 torch.cuda.synchronize()

@@ -58,6 +58,8 @@ def point(arch, hw, state, *, N=4, batch=1, budget=0.25, cutoff=None, policy="dr
             "demand_insertions": rep.counters["demand_insertions"],
             "ms_per_iteration": rep.total_time * 1e3 / max(1, len(rep.iterations)),
             "ffn_impl": ffn_impl,
+            "host_codec": ex.get("host_codec"), "wire_ratio": ex.get("h2d_wire_ratio"),
+            "h2d_wire_gbs": ex.get("h2d_wire_gbs"),
         }
     finally:
         eng.close()
