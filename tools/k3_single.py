@@ -16,7 +16,7 @@ import torch
 from paper_2510_10302_b200 import kernels as K
 
 
-def main(iters=20, gap_cycles=20000):
+def main(iters=20, gap_cycles=20000, Ts=(1, 2, 3, 4), impls=("tc", "tc_fused", "cuda_core")):
     H, F = 4096, 14336
     dev = "cuda"
     S = 8
@@ -27,7 +27,7 @@ def main(iters=20, gap_cycles=20000):
     side = torch.cuda.Stream()
     side_buf = torch.zeros((1024,), device=dev)
     out = []
-    for T in (1, 2, 3, 4):
+    for T in Ts:
         g = torch.Generator().manual_seed(T)
         x = torch.randn((T, H), generator=g).to(torch.bfloat16).to(dev)
         idx = torch.zeros((T, 1), dtype=torch.int32, device=dev)
@@ -39,7 +39,7 @@ def main(iters=20, gap_cycles=20000):
         ws = torch.empty((max(1, K.tc_workspace_floats(T, H, F, su, sd)),), dtype=torch.float32, device=dev)
         act = T * (H * 2 + 2 * F * 2 + H * 4)
         row = {"T": T, "split": [su, sd], "gap_cycles": gap_cycles}
-        for name in ("tc", "tc_fused", "cuda_core"):
+        for name in impls:
             ms = []
             for i in range(iters + 3):
                 slot = i % S
@@ -76,4 +76,7 @@ def main(iters=20, gap_cycles=20000):
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 20, int(sys.argv[2]) if len(sys.argv) > 2 else 20000)
+    a = sys.argv[1:]
+    main(int(a[0]) if len(a) > 0 else 20, int(a[1]) if len(a) > 1 else 20000,
+         tuple(int(t) for t in a[2].split(",")) if len(a) > 2 else (1, 2, 3, 4),
+         tuple(a[3].split(",")) if len(a) > 3 else ("tc", "tc_fused", "cuda_core"))
