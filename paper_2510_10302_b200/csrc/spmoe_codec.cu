@@ -204,10 +204,10 @@ struct DecParams {
 // for both the lane-major writes and the value-order reads).
 constexpr int kPitch = kPerLane / 4 + 1;
 // A block's code words are staged in shared memory before the lanes walk
-// them (Gaussian weights: ~330 words; 768 = 6 bits per value); longer runs
+// them (Gaussian weights: ~346 words; 400 ~ 3.1 bits per value); longer runs
 // are read from global memory directly.
-constexpr int kStageWords = 768;
-constexpr int kDecWarps = 4;
+constexpr int kStageWords = 400;
+constexpr int kDecWarps = 16;
 constexpr int kDecThreads = 32 * kDecWarps;
 constexpr int kWarpSmemWords = kStageWords + 2 + kLanes * kPitch;
 constexpr int kDecSmemBytes = 4 * kLutSize + kDecWarps * kWarpSmemWords * 4;
@@ -588,8 +588,8 @@ int spmoe_xc_decode_segments(const uint8_t* blob, const spmoe_xc_header* hdr, in
     cudaFuncSetAttribute(xc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmemBytes);
     attr = true;
   }
-  // ~6 resident CTAs (24 warps, ~40 KB smem each) per SM over the launch
-  const uint32_t want = (uint32_t)std::max(1, 6 * num_sms() / count);
+  // 2 resident CTAs (32 warps, ~109 KB smem each) per SM over the launch
+  const uint32_t want = (uint32_t)std::max(1, 2 * num_sms() / count);
   const uint32_t gx = std::max(1u, std::min(want, (maxblk + kDecWarps - 1) / kDecWarps));
   xc_decode_kernel<<<dim3(gx, count), kDecThreads, kDecSmemBytes, (cudaStream_t)stream>>>(p);
   return (int)cudaGetLastError();
