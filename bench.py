@@ -302,11 +302,12 @@ def main():
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
     # replicas on one box share one pinned host expert pool per NUMA node
     # through /dev/shm; each process runs on its GPU's socket
-    from paper_2510_10302_b200.replicas import bind_to_node, gpu_numa_node, numa_pool_roles
+    from paper_2510_10302_b200.replicas import (bind_to_node, gpu_numa_node, mem_available_bytes, numa_pool_roles,
+                                                plan_host_pools, shm_free_bytes)
 
     node = gpu_numa_node(local)
     bind_to_node(node)
-    share, leader = None, True
+    share, leader, distinct = None, True, None
     if local_world > 1:
         nodes = [node] * world
         if world > 1:
@@ -314,9 +315,21 @@ def main():
             dist.all_gather_object(allnodes, (local, node))
             nodes = [n for _, n in sorted(allnodes)][:local_world]
         node, leader = numa_pool_roles(nodes, local)
-        share = f"{arch.name}_s1234_{os.environ.get('MASTER_PORT', '0')}_n{node}"
+        # rank 0 decides for the box (before any pool exists): shared shm
+        # pools if they fit, else private pinned pools bounded by free RAM
+        wire = 0.72 if args.host_codec != "none" else 1.0  # XC blob ~0.673 of raw
+        decision = [plan_host_pools(len(set(nodes)), int(wire * E_all * arch.expert_bytes), local_world, E_all,
+                                    shm_free_bytes(), mem_available_bytes())]
+        if world > 1:
+            dist.broadcast_object_list(decision, src=0)
+        use_shared, distinct = decision[0]
+        if use_shared:
+            share = f"{arch.name}_s1234_{os.environ.get('MASTER_PORT', '0')}_n{node}"
+        else:
+            leader = True
+            log(f"[bench] /dev/shm too small for shared pools: private pinned pools, distinct rows={distinct}")
     eng = SpecMoEEngine(arch, hw, timings, policy, batch=cfg["batch"], max_tokens=cfg["prompt"] + 64 * (cfg["N"] + 1),
-                        window_tokens=cfg["N"], host_share=share, host_leader=leader,
+                        window_tokens=cfg["N"], host_share=share, host_leader=leader, host_distinct=distinct,
                         ffn_impl=args.ffn_impl, host_codec=None if args.host_codec == "none" else "xc")
     g = torch.Generator().manual_seed(1000 + rank)
     prompts = torch.randint(0, arch.vocab, (cfg["batch"], cfg["prompt"]), generator=g)

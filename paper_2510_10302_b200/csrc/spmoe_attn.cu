@@ -110,11 +110,11 @@ __global__ void __launch_bounds__(256) rope_kv_kernel(const uint16_t* __restrict
 }
 
 // ------------------------------------------------------------ attention
-// One CTA (4 warps) per (b, head, chunk of QC queries).  Each warp owns a
+// One CTA (NW warps) per (b, head, chunk of QC queries).  Each warp owns a
 // strided subset of the keys and keeps, per query, an online-softmax state
 // (max, sum, acc[hd/32 per lane]); the warps merge through shared memory.
-template <int HD, int QC>
-__global__ void __launch_bounds__(128) attn_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ kc,
+template <int HD, int QC, int NW>
+__global__ void __launch_bounds__(32 * NW) attn_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ kc,
                                                    const uint16_t* __restrict__ vc, const int64_t* __restrict__ start,
                                                    int T, int nh, int nkv, int S, float scale,
                                                    uint16_t* __restrict__ out) {
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(128) attn_kernel(const uint16_t* __restrict__ 
   }
   const uint16_t* kb = kc + ((int64_t)b * nkv + kh) * S * HD;
   const uint16_t* vb = vc + ((int64_t)b * nkv + kh) * S * HD;
-  for (int key = warp; key < klen; key += 4) {
+  for (int key = warp; key < klen; key += NW) {
     float kv[PL], vv[PL];
 #pragma unroll
     for (int j = 0; j < PL; ++j) {
@@ -168,8 +168,8 @@ __global__ void __launch_bounds__(128) attn_kernel(const uint16_t* __restrict__ 
     }
   }
   // merge the 4 warps' states
-  __shared__ float sm_m[4][QC], sm_l[4][QC];
-  __shared__ float sm_acc[4][QC][HD];
+  __shared__ float sm_m[NW][QC], sm_l[NW][QC];
+  __shared__ float sm_acc[NW][QC][HD];
   if (lane == 0)
 #pragma unroll
     for (int i = 0; i < QC; ++i) {
@@ -185,10 +185,10 @@ __global__ void __launch_bounds__(128) attn_kernel(const uint16_t* __restrict__ 
     const int i = idx / HD, d = idx % HD;
     float mx = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) mx = fmaxf(mx, sm_m[w][i]);
+    for (int w = 0; w < NW; ++w) mx = fmaxf(mx, sm_m[w][i]);
     float den = 0.0f, num = 0.0f;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
+    for (int w = 0; w < NW; ++w) {
       if (sm_m[w][i] == -INFINITY) continue;
       const float c = __expf(sm_m[w][i] - mx);
       den += sm_l[w][i] * c;
@@ -231,9 +231,9 @@ int spmoe_attention(const uint16_t* q, const uint16_t* k_cache, const uint16_t* 
   const dim3 grid(B * nh * nqc);
   cudaStream_t st = (cudaStream_t)stream;
   if (hd == 128)
-    attn_kernel<128, QC><<<grid, 128, 0, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale, out);
+    attn_kernel<128, QC, 8><<<grid, 256, 0, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale, out);
   else
-    attn_kernel<64, QC><<<grid, 128, 0, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale, out);
+    attn_kernel<64, QC, 8><<<grid, 256, 0, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale, out);
   return (int)cudaGetLastError();
 }
 

@@ -76,6 +76,44 @@ def bind_to_node(node: int) -> bool:
         return False
 
 
+def shm_free_bytes(root: str = "/dev/shm") -> int:
+    """Free bytes of the shared-memory filesystem (0 if absent)."""
+    try:
+        st = os.statvfs(root)
+        return st.f_bavail * st.f_frsize
+    except OSError:
+        return 0
+
+
+def mem_available_bytes() -> int:
+    """MemAvailable from /proc/meminfo (0 if unknown)."""
+    try:
+        for line in Path("/proc/meminfo").read_text().splitlines():
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def plan_host_pools(n_pools: int, pool_bytes: int, n_procs: int, rows: int, shm_free: int, mem_free: int,
+                    headroom: float = 0.8) -> tuple[bool, int | None]:
+    """How the ranks of one box hold the host expert tier.
+
+    Shared /dev/shm pools (one per NUMA node) when they fit in ``headroom`` of
+    the shm filesystem; otherwise one private pinned pool per process, with
+    ``distinct`` rows (experts alias rows: bytes per copy unchanged) bounded
+    so that all private pools fit in ``headroom`` of the available RAM.
+    Returns (use_shared, distinct_rows or None)."""
+    if n_pools * pool_bytes <= headroom * shm_free:
+        return True, None
+    per_row = max(1, pool_bytes // max(1, rows))
+    budget = headroom * mem_free / max(1, n_procs) if mem_free else pool_bytes
+    if pool_bytes <= budget:
+        return False, None
+    return False, max(1, int(budget // per_row))
+
+
 def assign_streams(n_streams: int, rank: int, world: int) -> list[int]:
     """Request-stream ids owned by ``rank``: contiguous, balanced to one."""
     if world < 1 or not 0 <= rank < world:

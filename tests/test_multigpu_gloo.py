@@ -90,3 +90,17 @@ def test_numa_pool_roles_one_leader_per_node():
     assert [numa_pool_roles([1, 0, 1, 0], r)[1] for r in range(4)] == [True, True, False, False]
     assert numa_pool_roles([0], 0) == (0, True)
     assert len(node_cpus(0)) >= 1 and node_cpus(10_000) == []
+
+
+def test_plan_host_pools_shared_private_and_bounded():
+    from paper_2510_10302_b200.replicas import plan_host_pools
+
+    GB = 10**9
+    # two NUMA pools of 61 GB fit a 1 TB shm
+    assert plan_host_pools(2, 61 * GB, 8, 256, 1000 * GB, 1500 * GB) == (True, None)
+    # 64 GB docker shm: private pools, all 8 fit in 1.5 TB of RAM
+    assert plan_host_pools(2, 61 * GB, 8, 256, 64 * GB, 1500 * GB) == (False, None)
+    # small RAM: private pools with aliased rows so 8 x pool <= 80 % of RAM
+    use, distinct = plan_host_pools(2, 61 * GB, 8, 256, 64 * GB, 200 * GB)
+    assert not use and 1 <= distinct < 256
+    assert 8 * distinct * (61 * GB // 256) <= 0.8 * 200 * GB
