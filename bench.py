@@ -285,9 +285,17 @@ def main():
     from paper_2510_10302_b200.engine import SpecMoEEngine
     from paper_2510_10302_b200.model import get_arch
 
-    torch.cuda.set_device(local)
+    # SPMOE_BENCH_SHARE_GPU=1 (test hook): every rank on cuda:0 over gloo, so
+    # the replica plumbing (pool roles, placement plan, shared-pool attach,
+    # max-over-ranks reduction) can be exercised on a one-GPU box
+    share_gpu = os.environ.get("SPMOE_BENCH_SHARE_GPU") == "1"
+    dev_index = 0 if share_gpu else local
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     arch = get_arch(cfg["arch"])
     E_all = arch.num_layers * arch.num_experts
     capacity = max(arch.num_experts, int(round(cfg["budget"] * E_all)))
@@ -305,7 +313,7 @@ def main():
     from paper_2510_10302_b200.replicas import (bind_to_node, gpu_numa_node, mem_available_bytes, numa_pool_roles,
                                                 plan_host_pools, shm_free_bytes)
 
-    node = gpu_numa_node(local)
+    node = gpu_numa_node(dev_index)
     bind_to_node(node)
     share, leader, distinct = None, True, None
     if local_world > 1:
@@ -356,7 +364,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev_index)
     clocks.start()
     launches0 = K.LAUNCHES["count"]
     st = torch.cuda.current_stream()
@@ -382,7 +390,7 @@ def main():
     rep = eng.report(wall_s=wall)
     roof = eng.k3_roofline()
     dec = eng.cache.decode_stats() if eng.host_pool.codec else None
-    stats = torch.tensor([dev_ms, wall, float(emitted)], dtype=torch.float64, device="cuda")
+    stats = torch.tensor([dev_ms, wall, float(emitted)], dtype=torch.float64, device="cpu" if share_gpu else "cuda")
     if world > 1:
         mx = stats.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
