@@ -141,6 +141,7 @@ class SpecMoEEngine:
         capture_layers: tuple[int, ...] = (),
         cuda_graphs: bool = True,
         ffn_impl: str = "auto",
+        tc_min_tokens: int = 3,
         expert_parallel: bool = False,
         ep_group=None,
         host_codec: str | None = "auto",
@@ -149,6 +150,10 @@ class SpecMoEEngine:
         if ffn_impl not in ("auto", "tcgen05", "cuda_core"):
             raise ValueError("ffn_impl must be auto | tcgen05 | cuda_core")
         self.ffn_impl = ffn_impl
+        self.tc_min_tokens = tc_min_tokens
+        # test hook: treat every resident expert as late (one launch each), to
+        # check that outputs do not depend on launch grouping
+        self.force_late = False
         if not torch.cuda.is_available():
             raise RuntimeError("SpecMoEEngine needs a CUDA device (there is no CPU fallback)")
         self.num_sms = torch.cuda.get_device_properties(device if device is not None else 0).multi_processor_count
@@ -350,17 +355,26 @@ class SpecMoEEngine:
                 self.decisions.append(("task", layer, ids))
         self._pushed = []
 
-    def _use_tc(self, F: int, maxtok: int) -> bool:
-        """tcgen05 path unless pinned to the CUDA-core (bit-exact) path; the
-        CUDA-core kernel wins only when every expert sees a single token."""
+    def _use_tc(self, F: int, ntok: int) -> bool:
+        """Kernel for ONE expert with ``ntok`` routed tokens: tcgen05 unless
+        pinned to the CUDA-core (bit-exact) path or the expert has fewer than
+        ``tc_min_tokens`` tokens (1-2 token experts run faster on the
+        CUDA-core kernel in the SD loop: 111.5 vs 124.2 us in situ for 2
+        tokens).  Decided per expert, never per launch, so an expert's output
+        bits do not depend on which experts happen to share its launch (that
+        depends on copy timing)."""
         if self.ffn_impl == "cuda_core" or self.arch.hidden % 128 or F % 128:
             return False
-        return self.ffn_impl == "tcgen05" or maxtok > 1
+        return self.ffn_impl == "tcgen05" or ntok >= self.tc_min_tokens
 
-    def _ffn(self, pool, slots, mask, xn, F, k, offsets, perm, h, y, maxtok, s: _Scratch, counts=None) -> None:
-        """K3 for the experts in ``mask``; ``counts`` = routed tokens of each
-        of those experts (host-known), used to plan the tcgen05 split-K."""
-        if self._use_tc(F, maxtok):
+    def _ffn(self, pool, slots, mask, xn, F, k, offsets, perm, h, y, maxtok, s: _Scratch, counts=None,
+             use_tc: bool | None = None) -> None:
+        """K3 for the experts in ``mask`` (all on one path: ``use_tc``, by
+        default chosen from ``maxtok``); ``counts`` = routed tokens of each of
+        those experts (host-known)."""
+        if use_tc is None:
+            use_tc = self._use_tc(F, maxtok)
+        if use_tc:
             rows = xn.shape[0] * k
             # launch-independent split: bits do not depend on launch grouping
             su, sd = K.tc_plan_static(self.arch.hidden, F, self.num_sms)
@@ -375,14 +389,25 @@ class SpecMoEEngine:
         return K.moe_combine(s.yd, perm, None, T, self.arch.hidden, 1, residual=resid, out=out)
 
     def _timed_ffn(self, experts, counts, slots, mask, xn, offsets, perm, s, maxtok, k=None) -> None:
-        """K3 over ``experts``; with ``time_k3`` set, brackets the launch pair
-        with CUDA events and books its algorithmic bytes (weights of every
-        expert in the mask read once + activations in/out) for the roofline."""
+        """K3 over ``experts`` (one launch per kernel path: experts are
+        grouped by their own token counts); with ``time_k3`` set, brackets
+        each launch with CUDA events and books its algorithmic bytes (weights
+        of every expert in the mask read once + activations in/out) for the
+        roofline."""
         a = self.arch
         k = a.top_k if k is None else k
+        groups: dict[bool, list[int]] = {}
+        for e in experts:
+            groups.setdefault(self._use_tc(a.ffn, int(counts[e])), []).append(e)
+        for use_tc, grp in groups.items():
+            self._timed_ffn_group(grp, counts, slots, sum(1 << e for e in grp), xn, offsets, perm, s, k, use_tc)
+
+    def _timed_ffn_group(self, experts, counts, slots, mask, xn, offsets, perm, s, k, use_tc) -> None:
+        a = self.arch
         cnt = [int(counts[e]) for e in experts]
+        maxtok = max(cnt) if cnt else 0
         if not self.time_k3:
-            self._ffn(self.pool, slots, mask, xn, a.ffn, k, offsets, perm, s.h, s.y, maxtok, s, cnt)
+            self._ffn(self.pool, slots, mask, xn, a.ffn, k, offsets, perm, s.h, s.y, maxtok, s, cnt, use_tc)
             return
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ea.record()  # creates the events; the launcher re-records them
@@ -390,7 +415,7 @@ class SpecMoEEngine:
         # the C launcher records ea right before its first kernel and eb after
         # its last, so host-side launch preparation is not counted
         self._lib.spmoe_k3_timing(ea.cuda_event, eb.cuda_event)
-        self._ffn(self.pool, slots, mask, xn, a.ffn, k, offsets, perm, s.h, s.y, maxtok, s, cnt)
+        self._ffn(self.pool, slots, mask, xn, a.ffn, k, offsets, perm, s.h, s.y, maxtok, s, cnt, use_tc)
         rows = int(sum(int(counts[e]) for e in experts))
         act = rows * (a.hidden * 2 + 2 * a.ffn * 2 + a.hidden * 4)  # x in, h out+in, y out
         self.k3_events.append((ea, eb, len(experts) * a.expert_bytes + act, len(experts), rows))
@@ -484,7 +509,7 @@ class SpecMoEEngine:
         ready, late_prefetch = [], []
         for e in hits:
             slot[e] = self.cache.slot_of(l, e)
-            (ready if self.cache.slot_ready(slot[e]) else late_prefetch).append(e)
+            (ready if self.cache.slot_ready(slot[e]) and not self.force_late else late_prefetch).append(e)
         if missing:
             for e, sl in zip(missing, self.cache.demand_load([ExpertId(l, e) for e in missing])):
                 slot[e] = sl

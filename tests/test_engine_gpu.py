@@ -196,6 +196,30 @@ def test_engine_deterministic(oracle, ffn_impl):
     assert outs[0][1] == outs[1][1], "cache counters differ"
 
 
+@pytest.mark.parametrize("tc_min", [2, 3])
+def test_engine_tokens_independent_of_launch_grouping(oracle, tc_min):
+    """Which resident experts share a K3 launch depends on copy timing
+    (ready vs late slots); each expert's kernel path and split plan depend
+    only on its own token count, so forcing every expert into its own launch
+    gives the same tokens and the same verify-MoE bits."""
+    outs = []
+    for force_late in (False, True):
+        eng = make_engine(capture=(0, 1, 2, 3), ffn_impl="auto", batch=3, tc_min_tokens=tc_min)
+        try:
+            eng.force_late = force_late
+            eng.prefill(prompts(3))
+            for _ in range(4):
+                eng.step()
+            torch.cuda.synchronize()
+            caps = [bits(c["out"]) for c in eng.captures if "layer" in c]
+            outs.append(([list(sq) for sq in eng.seqs], caps))
+        finally:
+            eng.close()
+    assert outs[0][0] == outs[1][0], "tokens depend on launch grouping"
+    assert len(outs[0][1]) == len(outs[1][1])
+    assert all(np.array_equal(a, b) for a, b in zip(outs[0][1], outs[1][1]))
+
+
 def test_flag_handoff_push_task():
     """push_task_flag: the worker waits for a device-bumped counter in mapped
     memory before reading the predicted ids (graph-safe hand-off)."""
