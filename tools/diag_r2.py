@@ -87,7 +87,7 @@ def spread_sweep(steps=20):
     only: bytes and FLOPs are identical), bench prompt and policy."""
     from dataclasses import replace
 
-    for spread in (0.02, 0.01, 0.005):
+    for spread in (0.005, 0.003, 0.002, 0.001):
         arch = replace(get_arch("mixtral_8x7b"), expert_spread=spread)
         hw = HardwareSpec(gpu_memory=183_359 * 2**20, peak_non_expert_memory=24 * 10**9, pcie_bandwidth=55.5e9,
                           name="b200")
