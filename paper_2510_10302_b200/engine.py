@@ -141,7 +141,7 @@ class SpecMoEEngine:
         capture_layers: tuple[int, ...] = (),
         cuda_graphs: bool = True,
         ffn_impl: str = "auto",
-        tc_min_tokens: int = 3,
+        tc_min_tokens: int | None = None,
         expert_parallel: bool = False,
         ep_group=None,
         host_codec: str | None = "auto",
@@ -150,6 +150,12 @@ class SpecMoEEngine:
         if ffn_impl not in ("auto", "tcgen05", "cuda_core"):
             raise ValueError("ffn_impl must be auto | tcgen05 | cuda_core")
         self.ffn_impl = ffn_impl
+        # per-expert kernel rule (see _use_tc): Mixtral-size experts with 1-2
+        # routed tokens stream faster on the CUDA-core kernel; small experts
+        # (DeepSeek / Qwen, 17 MB) come in many-expert launches where the
+        # tcgen05 kernel wins at any token count (4.4 vs 2.9 TB/s)
+        if tc_min_tokens is None:
+            tc_min_tokens = 3 if arch.expert_bytes >= (1 << 27) else 1
         self.tc_min_tokens = tc_min_tokens
         # test hook: treat every resident expert as late (one launch each), to
         # check that outputs do not depend on launch grouping
