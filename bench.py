@@ -254,6 +254,8 @@ def main():
     ap.add_argument("--cutoff", type=int, default=None, help="explicit cutoff layer (default: solver)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ffn-impl", default="auto", choices=["auto", "tcgen05", "cuda_core"])
+    ap.add_argument("--tc-min-tokens", type=int, default=None,
+                    help="experts with fewer routed tokens take the CUDA-core K3 (default: per arch)")
     ap.add_argument("--host-codec", default="xc", choices=["xc", "none"],
                     help="host-tier expert encoding: xc (lossless exponent coding) or raw bf16")
     ap.add_argument("--write-calibration", action="store_true")
@@ -338,7 +340,8 @@ def main():
             log(f"[bench] /dev/shm too small for shared pools: private pinned pools, distinct rows={distinct}")
     eng = SpecMoEEngine(arch, hw, timings, policy, batch=cfg["batch"], max_tokens=cfg["prompt"] + 64 * (cfg["N"] + 1),
                         window_tokens=cfg["N"], host_share=share, host_leader=leader, host_distinct=distinct,
-                        ffn_impl=args.ffn_impl, host_codec=None if args.host_codec == "none" else "xc")
+                        ffn_impl=args.ffn_impl, host_codec=None if args.host_codec == "none" else "xc",
+                        tc_min_tokens=args.tc_min_tokens)
     g = torch.Generator().manual_seed(1000 + rank)
     prompts = torch.randint(0, arch.vocab, (cfg["batch"], cfg["prompt"]), generator=g)
     eng.prefill(prompts)

@@ -502,9 +502,10 @@ class SpecMoEEngine:
     def _run_experts(self, l: int, counts: np.ndarray, x: torch.Tensor, k: int, offsets, perm, s: _Scratch) -> list:
         """Cache decisions + K3 for the experts with ``counts > 0`` at layer l:
         touch the union in ascending order, demand-load the misses behind
-        queued prefetches, run the resident experts first and each late
-        expert after its slot's ready event (§4.3), then record the
-        slots' read events.  Returns the slot of every expert (0 if unused)."""
+        queued prefetches, run the resident experts first and the late ones
+        after their slots' ready events (§4.3; all late experts but
+        the last in one launch under the last one's copy, then the last),
+        then record the slots' read events.  Returns the slot of every expert (0 if unused)."""
         E = self.arch.num_experts
         required = [int(e) for e in np.nonzero(counts)[0]]
         stream_ptr = self.stream.cuda_stream
@@ -524,14 +525,25 @@ class SpecMoEEngine:
         if ready:
             mask = sum(1 << e for e in ready)
             self._timed_ffn(ready, counts, slots, mask, x, offsets, perm, s, maxtok, k)
-        for kind, group in (("prefetch", late_prefetch), ("demand", missing)):
-            for e in group:
+        # late experts land one by one (prefetches in flight first, then the
+        # demand batch in copy order); the layer cannot end before the LAST
+        # one lands, so every earlier late expert runs in ONE launch once the
+        # second-to-last has landed (under the last one's copy), and only the
+        # last expert's K3 stays on the critical path.  Same layer latency as
+        # running each expert on arrival, far fewer single-expert launches.
+        late = [("prefetch", e) for e in late_prefetch] + [("demand", e) for e in missing]
+        for batch in ([late[:-1], late[-1:]] if len(late) > 1 else [late]):
+            if not batch:
+                continue
+            for kind, e in batch:
                 ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 ea.record()
                 self.cache.wait_slot(slot[e], stream_ptr)
                 eb.record()
                 self.stalls.append(_Stall(kind, l, ea, eb))
-                self._timed_ffn([e], counts, slots, 1 << e, x, offsets, perm, s, int(counts[e]), k)
+            grp = [e for _, e in batch]
+            self._timed_ffn(grp, counts, slots, sum(1 << e for e in grp), x, offsets, perm, s,
+                            max(int(counts[e]) for e in grp), k)
         for e in required:
             self.cache.mark_read(slot[e], stream_ptr)
         return slots
