@@ -8,8 +8,8 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
 timeout 1500 python -m pytest tests/ -q -m gpu > gpurun_out/gt.log 2>&1; tail -3 gpurun_out/gt.log
-timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_xc.json 2> gpurun_out/bench_xc.err
-timeout 900 python bench.py --steps 10 --warmup 3 --host-codec none --no-cpu-baseline > gpurun_out/bench_raw.json 2> gpurun_out/bench_raw.err
+timeout 900 python bench.py --steps 20 --warmup 3 > gpurun_out/bench_xc.json 2> gpurun_out/bench_xc.err
+timeout 900 python bench.py --steps 20 --warmup 3 --host-codec none --no-cpu-baseline > gpurun_out/bench_raw.json 2> gpurun_out/bench_raw.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 python - <<'PY'
 import json
