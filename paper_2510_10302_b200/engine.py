@@ -274,6 +274,7 @@ class SpecMoEEngine:
         self.iter_records: list[IterationRecord] = []
         self.slots: list[ComputeSlot] = []
         self._slot_events: list = []
+        self.route_events: list = []  # (iteration, layer, event) with record_timeline
         self.iter_events: list[tuple[torch.cuda.Event, torch.cuda.Event, torch.cuda.Event]] = []
         self.draft_ms = 0.0
         self.verify_ms = 0.0
@@ -487,6 +488,9 @@ class SpecMoEEngine:
             self._gating_predict(l + 1, xn)
         self._lib.spmoe_event_synchronize(self._route_ev)
         ids = self.route_ring.view[0, : T * k].copy()
+        counts = np.bincount(ids, minlength=E)
+        # copies first: the host-side bookkeeping below overlaps the link
+        plan = self._cache_issue(l, counts) if self.ep is None else None
         self.history.record_many(l, ids)
         if self.record:
             self.decisions.append(("verify", l, [int(v) for v in ids]))
@@ -495,8 +499,7 @@ class SpecMoEEngine:
         if self.ep is not None:
             return self._moe_verify_ep(l, xn, resid, s, w, idx, sg, ids)
         offsets, perm, inv = K.moe_permute(idx, E, out=(s.offsets, s.perm[: T * k], s.inv[: T * k]))
-        counts = np.bincount(ids, minlength=E)
-        slots = self._run_experts(l, counts, xn, k, offsets, perm, s)
+        slots = self._run_plan(l, plan, counts, xn, k, offsets, perm, s)
         return self._shared_and_combine(l, xn, resid, s, w, idx, sg, s.y, inv, slots)
 
     def _run_experts(self, l: int, counts: np.ndarray, x: torch.Tensor, k: int, offsets, perm, s: _Scratch) -> list:
@@ -506,20 +509,33 @@ class SpecMoEEngine:
         after their slots' ready events (§4.3; all late experts but
         the last in one launch under the last one's copy, then the last),
         then record the slots' read events.  Returns the slot of every expert (0 if unused)."""
-        E = self.arch.num_experts
+        return self._run_plan(l, self._cache_issue(l, counts), counts, x, k, offsets, perm, s)
+
+    def _cache_issue(self, l: int, counts: np.ndarray) -> tuple:
+        """The layer's cache decisions, in the reference order: touch the
+        required experts ascending (lookup, cache.py:62-77), then demand-load
+        the misses as one batch behind queued prefetches (on_demand_load,
+        prefetch.py:276-301) -- issued before any other host work of the
+        layer so the link starts as soon as routing is known."""
         required = [int(e) for e in np.nonzero(counts)[0]]
-        stream_ptr = self.stream.cuda_stream
         hits, missing = [], []
         for e in required:
             (hits if self.cache.lookup(ExpertId(l, e), touch=True) else missing).append(e)
         slot = {}
+        if missing:
+            for e, sl in zip(missing, self.cache.demand_load([ExpertId(l, e) for e in missing])):
+                slot[e] = sl
         ready, late_prefetch = [], []
         for e in hits:
             slot[e] = self.cache.slot_of(l, e)
             (ready if self.cache.slot_ready(slot[e]) and not self.force_late else late_prefetch).append(e)
-        if missing:
-            for e, sl in zip(missing, self.cache.demand_load([ExpertId(l, e) for e in missing])):
-                slot[e] = sl
+        return required, slot, ready, late_prefetch, missing
+
+    def _run_plan(self, l: int, plan: tuple, counts: np.ndarray, x: torch.Tensor, k: int, offsets, perm,
+                  s: _Scratch) -> list:
+        required, slot, ready, late_prefetch, missing = plan
+        E = self.arch.num_experts
+        stream_ptr = self.stream.cuda_stream
         slots = [slot.get(e, 0) for e in range(E)]
         maxtok = int(counts.max()) if counts.size else 0
         if ready:
@@ -781,6 +797,11 @@ class SpecMoEEngine:
             self._slot_begin()
             self._gating_waits(l)
             self._verify_graphs[l].replay()
+            if self.record_timeline:
+                # end of the layer's pre-MoE block (routing known on the GPU)
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(self.stream)
+                self.route_events.append((len(self.iter_records), l, ev))
             self._moe_verify(l, self._vxn, self._vx, self.scratch, routed=self._vroute[l])
             self._slot_end("verify", P[0] - 1, l)
         hn = rms_norm(self._vx.view(B, T, H), self.weights.final_norm, a.rms_eps)

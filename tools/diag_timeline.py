@@ -38,6 +38,7 @@ def run(codec, state=None):
     t0 = min([r["start_ms"] for r in log] + [s[2] for s in slots])
     rows = []
     vs = {s[1]: s for s in slots if s[0] == "verify"}
+    routes = {l: eng.cache.since_epoch_ms(ev) for it, l, ev in eng.route_events}
     dem = {r["layer"]: r for r in log if r["kind"] == "on_demand"}
     for l in range(arch.num_layers):
         r, s = dem.get(l), vs.get(l)
@@ -47,6 +48,10 @@ def run(codec, state=None):
             "slot": [round(s[2] - t0, 2), round(s[3] - t0, 2)] if s else None,
             "copy": [round(r["start_ms"] - t0, 2), round(r["copy_end_ms"] - t0, 2), round(r["end_ms"] - t0, 2)] if r else None,
             "gap_to_next_copy": round(nxt["start_ms"] - r["copy_end_ms"], 3) if (r and nxt) else None,
+            # pre-MoE block of this layer (slot start -> routing known) and the
+            # host's reaction (routing known -> first copy of the layer issued)
+            "pre_moe_ms": round(routes[l] - (s[2]), 3) if (s and l in routes) else None,
+            "host_ms": round(r["start_ms"] - routes[l], 3) if (r and l in routes) else None,
         })
     ex = rep.extras
     print(json.dumps({"codec": codec, "device_ms": ex["device_ms"], "link_busy_ms": ex["link_busy_ms"],
