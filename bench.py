@@ -281,7 +281,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2510_10302_b200 import HardwareSpec, Policy, PolicySpec, ProfiledTimings
+    from paper_2510_10302_b200 import HardwareSpec, Policy, PolicySpec
     from paper_2510_10302_b200 import kernels as K
     from paper_2510_10302_b200.calibrate import b200_timings
     from paper_2510_10302_b200.engine import SpecMoEEngine
