@@ -54,15 +54,8 @@ assert C.sizeof(XcSegment) == 312 and C.sizeof(XcHeader) == 1272
 
 
 def expert_segments(ffn: int, hidden: int) -> list[int]:
-    """An expert blob W1 | W3 | W2 codes as four segments: one per matrix
-    (W2's scale differs, so it gets its own code tables), W2 in two row
-    halves.  The copy path decodes each segment as soon as its bytes land,
-    so only the last segment's decode (W2's second half, 1/6 of the expert)
-    remains after the expert's last byte arrives.  Falls back to three
-    segments when a half would not be whole coding blocks."""
-    half = ffn * hidden // 2
-    if half % XC_BLOCK == 0 and (ffn * hidden) % 2 == 0:
-        return [ffn * hidden, ffn * hidden, half, half]
+    """An expert blob W1 | W3 | W2 codes as three segments (one per matrix:
+    W2's scale differs, so it gets its own code tables)."""
     return [ffn * hidden] * 3
 
 
