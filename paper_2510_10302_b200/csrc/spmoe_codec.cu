@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* stage = reinterpret_cast<uint32_t*>(wbase) + warp * kWarpSmemWords;
   uint32_t* ew = stage + kStageWords + 2;
-  uint8_t* eb8 = reinterpret_cast<uint8_t*>(ew) + lane * (4 * kPitch);  // this lane's exponent row
+  uint32_t* erow = ew + lane * kPitch;  // this lane's exponent row
   for (uint32_t blk = blockIdx.x * kDecWarps + warp; blk < S.nblk; blk += gridDim.x * kDecWarps) {
     // this lane's substream: block start + words of the lanes before it
     const uint32_t words = __ldg(S.lanes + (uint64_t)blk * kLanes + lane);
@@ -297,13 +297,21 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
     wp += 2;
     // up to three exponents per lookup; a row has 4 slack bytes past its
     // 128 for the last lookup's extra symbols
+    // (exponents queue in a register and leave as whole words: one shared
+    // store per four symbols instead of three byte stores per lookup)
+    uint64_t q = 0;
+    int nq = 0, wi = 0;
     for (int k = 0; k < kPerLane;) {
       const uint32_t e = s_lut2[(uint32_t)buf & (kLutSize - 1)];
       const int L = (int)(e >> 26), c = (int)((e >> 24) & 3u);
-      eb8[k] = (uint8_t)e;
-      eb8[k + 1] = (uint8_t)(e >> 8);
-      eb8[k + 2] = (uint8_t)(e >> 16);
+      q |= (uint64_t)(e & 0xffffffu) << (8 * nq);  // bytes past c are zero
+      nq += c;
       k += c;
+      if (nq >= 4) {
+        erow[wi++] = (uint32_t)q;
+        q >>= 32;
+        nq -= 4;
+      }
       buf >>= L;
       nbits -= L;
       if (nbits < 32) {
@@ -311,6 +319,7 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
         nbits += 32;
       }
     }
+    if (nq > 0) erow[wi] = (uint32_t)q;
     __syncwarp();
     // assembly: 16 rounds of 8 consecutive values per lane, 16-byte stores
     uint16_t* dst = S.dst + (uint64_t)blk * SPMOE_XC_BLOCK;
