@@ -1,9 +1,9 @@
 """K3 for ONE late expert (the bench's regime: each demand-loaded expert runs
-alone after its copy lands), Mixtral shapes, 1..4 routed tokens.  Times the
+alone after its copy lands), Mixtral shapes, 1..4 routed tokens (optionally with a concurrent 244 MB H2D copy per launch).  Times the
 tcgen05 launcher (static split plan), the fused tcgen05 kernel and the
 CUDA-core kernel with CUDA events, rotating over 8 slots (>= 2.8 GB, no L2
 reuse), each launch preceded by an idle gap (like a stream waiting on a
-copy event).  Usage: python tools/k3_single.py [iters]"""
+copy event).  Usage: python tools/k3_single.py [iters gap Ts impls [h2d]]"""
 import json
 import sys
 import time
@@ -16,7 +16,7 @@ import torch
 from paper_2510_10302_b200 import kernels as K
 
 
-def main(iters=20, gap_cycles=20000, Ts=(1, 2, 3, 4), impls=("tc", "tc_fused", "cuda_core")):
+def main(iters=20, gap_cycles=20000, Ts=(1, 2, 3, 4), impls=("tc", "tc_fused", "cuda_core"), h2d=False):
     H, F = 4096, 14336
     dev = "cuda"
     S = 8
@@ -26,6 +26,9 @@ def main(iters=20, gap_cycles=20000, Ts=(1, 2, 3, 4), impls=("tc", "tc_fused", "
     sync = torch.zeros((1,), dtype=torch.int32, device=dev)
     side = torch.cuda.Stream()
     side_buf = torch.zeros((1024,), device=dev)
+    if h2d:  # a concurrent host->HBM copy in flight during every launch (the SD loop's situation)
+        hsrc = torch.empty((244 << 20,), dtype=torch.uint8).pin_memory()
+        hdst = torch.empty((244 << 20,), dtype=torch.uint8, device=dev)
     out = []
     for T in Ts:
         g = torch.Generator().manual_seed(T)
@@ -38,7 +41,7 @@ def main(iters=20, gap_cycles=20000, Ts=(1, 2, 3, 4), impls=("tc", "tc_fused", "
         su, sd = K.tc_plan_static(H, F)
         ws = torch.empty((max(1, K.tc_workspace_floats(T, H, F, su, sd)),), dtype=torch.float32, device=dev)
         act = T * (H * 2 + 2 * F * 2 + H * 4)
-        row = {"T": T, "split": [su, sd], "gap_cycles": gap_cycles}
+        row = {"T": T, "split": [su, sd], "gap_cycles": gap_cycles, "h2d": h2d}
         for name in impls:
             ms = []
             for i in range(iters + 3):
@@ -55,6 +58,10 @@ def main(iters=20, gap_cycles=20000, Ts=(1, 2, 3, 4), impls=("tc", "tc_fused", "
                         ev.record(side)
                     torch.cuda.current_stream().wait_event(ev)
                 else:
+                    if h2d:
+                        torch.cuda.synchronize()
+                        with torch.cuda.stream(side):
+                            hdst.copy_(hsrc, non_blocking=True)
                     torch.cuda._sleep(gap_cycles)  # busy gap
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
@@ -79,4 +86,5 @@ if __name__ == "__main__":
     a = sys.argv[1:]
     main(int(a[0]) if len(a) > 0 else 20, int(a[1]) if len(a) > 1 else 20000,
          tuple(int(t) for t in a[2].split(",")) if len(a) > 2 else (1, 2, 3, 4),
-         tuple(a[3].split(",")) if len(a) > 3 else ("tc", "tc_fused", "cuda_core"))
+         tuple(a[3].split(",")) if len(a) > 3 else ("tc", "tc_fused", "cuda_core"),
+         len(a) > 4 and a[4] == "h2d")

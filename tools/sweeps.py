@@ -4,9 +4,11 @@
             (solver's choice + explicit 0..L-1) -> TPOT, hit rate, hidden
             prefetch fraction;
   qwen:     Qwen1.5-MoE-A2.7B shapes, draft length N in {2,4,8}, batch
-            {1,2,4,8}, budget {12.5,25,50} % -> TPOT, tokens/s, hit rate.
+            {1,2,4,8}, budget {12.5,25,50} % -> TPOT, tokens/s, hit rate;
+  mixtral:  Mixtral-8x7B policy and cutoff points at 25 %;
+  mixtral_grid: Mixtral-8x7B budget {12.5,25,50,100} %, N {2,8}, batch {2,4}.
 
-python tools/sweeps.py deepseek|qwen [--out profiles/sweeps_r1.jsonl] [--steps 6]
+python tools/sweeps.py deepseek|qwen|mixtral|mixtral_grid [--out profiles/sweeps_r1.jsonl] [--steps 6]
 """
 
 from __future__ import annotations
@@ -67,7 +69,7 @@ def point(arch, hw, state, *, N=4, batch=1, budget=0.25, cutoff=None, policy="dr
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["deepseek", "qwen", "mixtral"])
+    ap.add_argument("which", choices=["deepseek", "qwen", "mixtral", "mixtral_grid"])
     ap.add_argument("--out", default="profiles/sweeps_r1.jsonl")
     ap.add_argument("--steps", type=int, default=6)
     # the bit-exact CUDA-core K3 gives every policy point the same token
@@ -75,7 +77,8 @@ def main():
     # into launches); tcgen05 split choices do, which perturbs acceptance
     ap.add_argument("--ffn-impl", default="cuda_core")
     a = ap.parse_args()
-    name = {"deepseek": "deepseek_v2_lite", "qwen": "qwen15_moe_a27b", "mixtral": "mixtral_8x7b"}[a.which]
+    name = {"deepseek": "deepseek_v2_lite", "qwen": "qwen15_moe_a27b", "mixtral": "mixtral_8x7b",
+            "mixtral_grid": "mixtral_8x7b"}[a.which]
     arch = get_arch(name)
     hw = HardwareSpec(gpu_memory=183_359 * 2**20, peak_non_expert_memory=24 * 10**9, pcie_bandwidth=55.5e9,
                       name="b200")
@@ -102,6 +105,15 @@ def main():
         for bud in (0.125, 0.5):
             pts.append(dict(budget=bud))
         pts.append(dict(policy="on_demand"))
+    elif a.which == "mixtral_grid":
+        # SURVEY 8(d) sweeps on config #2: budget (100 % = every expert
+        # resident after warm-up, the HBM-bound verify), draft length, batch
+        for bud in (0.125, 0.25, 0.5, 1.0):
+            pts.append(dict(budget=bud))
+        for N in (2, 8):
+            pts.append(dict(N=N))
+        for B in (2, 4):
+            pts.append(dict(batch=B))
     else:
         for pol in ("on_demand", "draft_prefetch", "gating_next_layer", "coarse_history"):
             pts.append(dict(policy=pol))
