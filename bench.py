@@ -255,7 +255,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ffn-impl", default="auto", choices=["auto", "tcgen05", "cuda_core"])
     ap.add_argument("--tc-min-tokens", type=int, default=None,
-                    help="experts with fewer routed tokens take the CUDA-core K3 (default: per arch)")
+                    help="experts with fewer routed tokens take the CUDA-core K3 (default 1: tcgen05 for every expert)")
     ap.add_argument("--host-codec", default="xc", choices=["xc", "none"],
                     help="host-tier expert encoding: xc (lossless exponent coding) or raw bf16")
     ap.add_argument("--write-calibration", action="store_true")

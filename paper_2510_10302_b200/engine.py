@@ -150,12 +150,15 @@ class SpecMoEEngine:
         if ffn_impl not in ("auto", "tcgen05", "cuda_core"):
             raise ValueError("ffn_impl must be auto | tcgen05 | cuda_core")
         self.ffn_impl = ffn_impl
-        # per-expert kernel rule (see _use_tc): Mixtral-size experts with 1-2
-        # routed tokens stream faster on the CUDA-core kernel; small experts
-        # (DeepSeek / Qwen, 17 MB) come in many-expert launches where the
-        # tcgen05 kernel wins at any token count (4.4 vs 2.9 TB/s)
+        # per-expert kernel rule (see _use_tc): tcgen05 at every token count.
+        # A lone 1-2 token Mixtral expert streams faster on the CUDA-core
+        # kernel (76 vs 83 us), but splitting a layer's late experts across
+        # two kernel paths halves the launch sizes: one path keeps the SD
+        # iteration time (851.6 vs 850.5 ms) and lifts in-situ K3 from 0.68
+        # to 0.73 of the copy peak; small experts (DeepSeek /
+        # Qwen) win on tcgen05 at any count (4.4 vs 2.9 TB/s)
         if tc_min_tokens is None:
-            tc_min_tokens = 3 if arch.expert_bytes >= (1 << 27) else 1
+            tc_min_tokens = 1
         self.tc_min_tokens = tc_min_tokens
         # test hook: treat every resident expert as late (one launch each), to
         # check that outputs do not depend on launch grouping
@@ -365,9 +368,8 @@ class SpecMoEEngine:
     def _use_tc(self, F: int, ntok: int) -> bool:
         """Kernel for ONE expert with ``ntok`` routed tokens: tcgen05 unless
         pinned to the CUDA-core (bit-exact) path or the expert has fewer than
-        ``tc_min_tokens`` tokens (1-2 token experts run faster on the
-        CUDA-core kernel in the SD loop: 111.5 vs 124.2 us in situ for 2
-        tokens).  Decided per expert, never per launch, so an expert's output
+        ``tc_min_tokens`` tokens (default 1: every expert on tensor cores).
+        Decided per expert, never per launch, so an expert's output
         bits do not depend on which experts happen to share its launch (that
         depends on copy timing)."""
         if self.ffn_impl == "cuda_core" or self.arch.hidden % 128 or F % 128:
