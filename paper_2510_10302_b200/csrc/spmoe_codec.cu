@@ -213,6 +213,34 @@ constexpr int kWarpSmemWords = kStageWords + 2 + kLanes * kPitch;
 constexpr int kDecSmemBytes = 4 * kLutSize + kDecWarps * kWarpSmemWords * 4;
 static_assert(kDecWarps * kWarpSmemWords * 4 >= 2 * kLutSize, "lut1 is built in the warp buffers");
 
+// One lane's substream -> its 128 exponents (row `erow`).  Inlined twice:
+// on the staged copy (the compiler then emits plain shared loads for the
+// refills) and on the rare over-long block read from global memory.
+// Up to three exponents per lookup, stored as bytes (a row has a slack word
+// for the last lookup's extra symbols; queueing them in a register and
+// storing whole words measured the same).
+__device__ __forceinline__ void decode_lane(const uint32_t* __restrict__ s_lut2, const uint32_t* wp,
+                                            uint32_t* __restrict__ erow) {
+  uint64_t buf = (uint64_t)wp[0] | ((uint64_t)wp[1] << 32);
+  int nbits = 64;
+  wp += 2;
+  uint8_t* eb8 = reinterpret_cast<uint8_t*>(erow);
+  for (int k = 0; k < kPerLane;) {
+    const uint32_t e = s_lut2[(uint32_t)buf & (kLutSize - 1)];
+    const int L = (int)(e >> 26), c = (int)((e >> 24) & 3u);
+    eb8[k] = (uint8_t)e;
+    eb8[k + 1] = (uint8_t)(e >> 8);
+    eb8[k + 2] = (uint8_t)(e >> 16);
+    k += c;
+    buf >>= L;
+    nbits -= L;
+    if (nbits < 32) {
+      buf |= (uint64_t)(*wp++) << nbits;
+      nbits += 32;
+    }
+  }
+}
+
 // grid.y = segment; each warp decodes whole blocks of its segment.
 __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -289,37 +317,10 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
         }
       }
       __syncwarp();
-      run = stage;
+      decode_lane(s_lut2, stage + (pre - words), erow);
+    } else {
+      decode_lane(s_lut2, run + (pre - words), erow);
     }
-    const uint32_t* wp = run + (pre - words);
-    uint64_t buf = (uint64_t)wp[0] | ((uint64_t)wp[1] << 32);
-    int nbits = 64;
-    wp += 2;
-    // up to three exponents per lookup; a row has 4 slack bytes past its
-    // 128 for the last lookup's extra symbols
-    // (exponents queue in a register and leave as whole words: one shared
-    // store per four symbols instead of three byte stores per lookup)
-    uint64_t q = 0;
-    int nq = 0, wi = 0;
-    for (int k = 0; k < kPerLane;) {
-      const uint32_t e = s_lut2[(uint32_t)buf & (kLutSize - 1)];
-      const int L = (int)(e >> 26), c = (int)((e >> 24) & 3u);
-      q |= (uint64_t)(e & 0xffffffu) << (8 * nq);  // bytes past c are zero
-      nq += c;
-      k += c;
-      if (nq >= 4) {
-        erow[wi++] = (uint32_t)q;
-        q >>= 32;
-        nq -= 4;
-      }
-      buf >>= L;
-      nbits -= L;
-      if (nbits < 32) {
-        buf |= (uint64_t)(*wp++) << nbits;
-        nbits += 32;
-      }
-    }
-    if (nq > 0) erow[wi] = (uint32_t)q;
     __syncwarp();
     // assembly: 16 rounds of 8 consecutive values per lane, 16-byte stores
     uint16_t* dst = S.dst + (uint64_t)blk * SPMOE_XC_BLOCK;
