@@ -209,36 +209,46 @@ constexpr int kPitch = kPerLane / 4 + 1;
 constexpr int kStageWords = 400;
 constexpr int kDecWarps = 16;
 constexpr int kDecThreads = 32 * kDecWarps;
-constexpr int kWarpSmemWords = kStageWords + 2 + kLanes * kPitch;
+constexpr int kWarpSmemWords = kStageWords + 3 + kLanes * kPitch;
 constexpr int kDecSmemBytes = 4 * kLutSize + kDecWarps * kWarpSmemWords * 4;
 static_assert(kDecWarps * kWarpSmemWords * 4 >= 2 * kLutSize, "lut1 is built in the warp buffers");
 
 // One lane's substream -> its 128 exponents (row `erow`).  Inlined twice:
 // on the staged copy (the compiler then emits plain shared loads for the
 // refills) and on the rare over-long block read from global memory.
-// Up to three exponents per lookup, stored as bytes (a row has a slack word
-// for the last lookup's extra symbols; queueing them in a register and
-// storing whole words measured the same).
+// Up to three exponents per lookup; they queue in a register and leave as
+// whole words (a row has a slack word for the last lookup's extra symbols):
+// the shared-memory pipe, not the ALUs, is the kernel's busiest unit.
 __device__ __forceinline__ void decode_lane(const uint32_t* __restrict__ s_lut2, const uint32_t* wp,
                                             uint32_t* __restrict__ erow) {
-  uint64_t buf = (uint64_t)wp[0] | ((uint64_t)wp[1] << 32);
-  int nbits = 64;
-  wp += 2;
-  uint8_t* eb8 = reinterpret_cast<uint8_t*>(erow);
+  // bit window = (nxt:cur) >> pos, pos < 32: at least 33 valid bits; the
+  // word after nxt is fetched one refill ahead, so a refill never waits on
+  // a load (the only load on the serial chain is the table lookup)
+  uint32_t cur = wp[0], nxt = wp[1], ahead = wp[2];
+  uint32_t pos = 0;
+  wp += 3;
+  uint64_t q = 0;
+  int nq = 0, wi = 0;
   for (int k = 0; k < kPerLane;) {
-    const uint32_t e = s_lut2[(uint32_t)buf & (kLutSize - 1)];
-    const int L = (int)(e >> 26), c = (int)((e >> 24) & 3u);
-    eb8[k] = (uint8_t)e;
-    eb8[k + 1] = (uint8_t)(e >> 8);
-    eb8[k + 2] = (uint8_t)(e >> 16);
+    const uint32_t e = s_lut2[__funnelshift_r(cur, nxt, pos) & (kLutSize - 1)];
+    const int c = (int)((e >> 24) & 3u);
+    q |= (uint64_t)(e & 0xffffffu) << (8 * nq);  // bytes past c are zero
+    nq += c;
     k += c;
-    buf >>= L;
-    nbits -= L;
-    if (nbits < 32) {
-      buf |= (uint64_t)(*wp++) << nbits;
-      nbits += 32;
+    if (nq >= 4) {
+      erow[wi++] = (uint32_t)q;
+      q >>= 32;
+      nq -= 4;
+    }
+    pos += e >> 26;
+    if (pos >= 32) {
+      pos -= 32;
+      cur = nxt;
+      nxt = ahead;
+      ahead = *wp++;
     }
   }
+  if (nq > 0) erow[wi] = (uint32_t)q;
 }
 
 // grid.y = segment; each warp decodes whole blocks of its segment.
@@ -278,7 +288,7 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* stage = reinterpret_cast<uint32_t*>(wbase) + warp * kWarpSmemWords;
-  uint32_t* ew = stage + kStageWords + 2;
+  uint32_t* ew = stage + kStageWords + 3;
   uint32_t* erow = ew + lane * kPitch;  // this lane's exponent row
   for (uint32_t blk = blockIdx.x * kDecWarps + warp; blk < S.nblk; blk += gridDim.x * kDecWarps) {
     // this lane's substream: block start + words of the lanes before it
@@ -300,20 +310,20 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
 #pragma unroll
     for (int it = 0; it < 4; ++it) sm2[it] = __ldg(reinterpret_cast<const uint2*>(smb) + (it + 4) * 32 + lane);
     if (nw <= (uint32_t)kStageWords) {
-      // coalesced copy of the block's code words (+2 words the last lane may
-      // peek past its run; the stream has 8 slack bytes), 12 loads in
+      // coalesced copy of the block's code words (+3 words the last lane may
+      // peek past its run; the stream has 12 slack bytes), 12 loads in
       // flight per lane before any store
-      for (uint32_t i0 = 0; i0 < nw + 2; i0 += 12 * 32) {
+      for (uint32_t i0 = 0; i0 < nw + 3; i0 += 12 * 32) {
         uint32_t t[12];
 #pragma unroll
         for (int k = 0; k < 12; ++k) {
           const uint32_t i = i0 + k * 32 + lane;
-          t[k] = i < nw + 2 ? __ldg(run + i) : 0u;
+          t[k] = i < nw + 3 ? __ldg(run + i) : 0u;
         }
 #pragma unroll
         for (int k = 0; k < 12; ++k) {
           const uint32_t i = i0 + k * 32 + lane;
-          if (i < nw + 2) stage[i] = t[k];
+          if (i < nw + 3) stage[i] = t[k];
         }
       }
       __syncwarp();
