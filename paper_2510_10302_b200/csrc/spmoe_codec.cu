@@ -209,9 +209,16 @@ constexpr int kPitch = kPerLane / 4 + 1;
 constexpr int kStageWords = 400;
 constexpr int kDecWarps = 16;
 constexpr int kDecThreads = 32 * kDecWarps;
-constexpr int kWarpSmemWords = kStageWords + 3 + kLanes * kPitch;
-constexpr int kDecSmemBytes = 4 * kLutSize + kDecWarps * kWarpSmemWords * 4;
+// staged run: up to 3 words of 16-byte alignment slack + the run + 3 peek
+// words, rounded up to 16 bytes (one bulk copy per block)
+constexpr int kStageAlloc = 412;
+static_assert(kStageAlloc * 4 >= ((12 + (kStageWords + 3) * 4 + 15) & ~15), "stage too small");
+constexpr int kWarpSmemWords = kStageAlloc + kLanes * kPitch;
+static_assert(kWarpSmemWords % 4 == 0, "warp buffers stay 16-byte aligned");
+constexpr int kDecSmemBytes = 4 * kLutSize + kDecWarps * kWarpSmemWords * 4 + kDecWarps * 8;
 static_assert(kDecWarps * kWarpSmemWords * 4 >= 2 * kLutSize, "lut1 is built in the warp buffers");
+
+__device__ __forceinline__ uint32_t sh_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // One lane's substream -> its 128 exponents (row `erow`).  Inlined twice:
 // on the staged copy (the compiler then emits plain shared loads for the
@@ -288,7 +295,16 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* stage = reinterpret_cast<uint32_t*>(wbase) + warp * kWarpSmemWords;
-  uint32_t* ew = stage + kStageWords + 3;
+  uint32_t* ew = stage + kStageAlloc;
+  // the block's code words arrive by one bulk copy (async proxy) per block,
+  // completing on this warp's mbarrier
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + kDecWarps * kWarpSmemWords * 4) + warp;
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sh_u32(mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t phase = 0;
   uint32_t* erow = ew + lane * kPitch;  // this lane's exponent row
   for (uint32_t blk = blockIdx.x * kDecWarps + warp; blk < S.nblk; blk += gridDim.x * kDecWarps) {
     // this lane's substream: block start + words of the lanes before it
@@ -310,24 +326,31 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
 #pragma unroll
     for (int it = 0; it < 4; ++it) sm2[it] = __ldg(reinterpret_cast<const uint2*>(smb) + (it + 4) * 32 + lane);
     if (nw <= (uint32_t)kStageWords) {
-      // coalesced copy of the block's code words (+3 words the last lane may
-      // peek past its run; the stream has 12 slack bytes), 12 loads in
-      // flight per lane before any store
-      for (uint32_t i0 = 0; i0 < nw + 3; i0 += 12 * 32) {
-        uint32_t t[12];
-#pragma unroll
-        for (int k = 0; k < 12; ++k) {
-          const uint32_t i = i0 + k * 32 + lane;
-          t[k] = i < nw + 3 ? __ldg(run + i) : 0u;
-        }
-#pragma unroll
-        for (int k = 0; k < 12; ++k) {
-          const uint32_t i = i0 + k * 32 + lane;
-          if (i < nw + 3) stage[i] = t[k];
-        }
+      const uint32_t delta = (uint32_t)((uintptr_t)run & 15);  // 0, 4, 8 or 12
+      if (lane == 0) {
+        // the run + 3 peek words (the stream has 12 readable slack bytes,
+        // then the segment's block offsets), from its 16-byte-aligned start
+        const uint32_t bytes = (delta + (nw + 3) * 4 + 15) & ~15u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after last block's reads
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sh_u32(mbar)), "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                sh_u32(stage)),
+            "l"(reinterpret_cast<const uint8_t*>(run) - delta), "r"(bytes), "r"(sh_u32(mbar))
+            : "memory");
       }
-      __syncwarp();
-      decode_lane(s_lut2, stage + (pre - words), erow);
+      asm volatile(
+          "{\n"
+          ".reg .pred p;\n"
+          "XCW_%=:\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+          "@!p bra XCW_%=;\n"
+          "}\n" ::"r"(sh_u32(mbar)),
+          "r"(phase)
+          : "memory");
+      phase ^= 1;
+      decode_lane(s_lut2, stage + (delta >> 2) + (pre - words), erow);
     } else {
       decode_lane(s_lut2, run + (pre - words), erow);
     }
