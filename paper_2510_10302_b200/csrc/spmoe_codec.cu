@@ -306,7 +306,9 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
   __syncwarp();
   uint32_t phase = 0;
   uint32_t* erow = ew + lane * kPitch;  // this lane's exponent row
-  for (uint32_t blk = blockIdx.x * kDecWarps + warp; blk < S.nblk; blk += gridDim.x * kDecWarps) {
+  // warp-major block order: the last, partial wave's blocks go to one warp
+  // of many CTAs (one per SM) instead of every warp of a few CTAs
+  for (uint32_t blk = warp * gridDim.x + blockIdx.x; blk < S.nblk; blk += gridDim.x * kDecWarps) {
     // this lane's substream: block start + words of the lanes before it
     const uint32_t words = __ldg(S.lanes + (uint64_t)blk * kLanes + lane);
     uint32_t pre = words;
