@@ -1,7 +1,8 @@
 """Host-link micro-benchmark of the runtime's copy tiers: demand batches of
 n Mixtral-8x7B experts through the native runtime, raw tier vs XC tier
 (staging ring + decode stream), no compute.  Prints per-batch device time,
-wire GB/s and the decode kernel's time alone."""
+wire GB/s, the decode kernel's time alone and its per-segment time inside
+the runtime (under the next segment's H2D copy)."""
 import json
 import sys
 import time
@@ -47,6 +48,7 @@ def main(n_rows=12, batch=6, reps=4):
         if tier == "xc":
             staging = torch.empty((3 * stride,), dtype=torch.uint8, device=dev)
             c.set_codec(stride, staging.data_ptr(), stride, 3, dec.cuda_stream)
+            c.decode_timing(True)
         cur = torch.cuda.current_stream()
         times = []
         for rep in range(reps + 1):
@@ -64,6 +66,10 @@ def main(n_rows=12, batch=6, reps=4):
             torch.cuda.synchronize()
             if rep:
                 times.append(e0.elapsed_time(e1))
+        if tier == "xc":
+            st = c.decode_stats()  # segment decodes inside the runtime, each under the next segment's H2D
+            res["decode_in_runtime_us_per_segment"] = st["ms"] * 1e3 / max(1, st["launches"])
+            res["decode_in_runtime_gbs"] = st["gbs"]
         wire = c.wire_bytes()["demand"]
         log = c.transfer_log()
         ms = float(np.median(times))
