@@ -268,7 +268,7 @@ int spmoe_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, uint64_t off
 /*   == x bit for bit.  Per-value coding only: no cross-value or         */
 /*   cross-expert modelling.                                             */
 /* --------------------------------------------------------------------- */
-#define SPMOE_XC_MAGIC 0x32435853u /* "SXC2" */
+#define SPMOE_XC_MAGIC 0x33435853u /* "SXC3" */
 #define SPMOE_XC_BLOCK 4096        /* values per coding block */
 #define SPMOE_XC_LANES 32          /* exponent substreams per block */
 #define SPMOE_XC_LMAX 12           /* longest exponent code, bits */
@@ -284,8 +284,12 @@ int spmoe_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, uint64_t off
  * then highest id first; codes assigned in (length, exponent) order).
  * Streams (byte offsets from the blob start, each 256-byte aligned, in this
  * order, so a segment's bytes are contiguous from its off_lut):
- *   lut   [4096]    u16  decode table: entry p (the next 12 code bits, LSB
- *                        first) = exponent | (code length << 8)
+ *   lut   [4096]    u32  multi-symbol decode table: entry p (the next 12
+ *                        code bits, LSB first) = up to three whole codes,
+ *                        sym0 | sym1 << 8 | sym2 << 16 | count << 24 |
+ *                        bits << 26 (count >= 1: an unused pattern of an
+ *                        incomplete code advances one bit); derived from
+ *                        len[] at encode time, so a decoder loads it
  *   sm    [n]       u8   (v >> 8 & 0x80) | (v & 0x7f)
  *   ex    [ex_words] u32 per block, SPMOE_XC_LANES lane substreams back to
  *                        back; lane l holds the bit-reversed codes of values

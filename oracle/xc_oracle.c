@@ -1,6 +1,6 @@
 /*
  * xc_oracle.c — CPU ORACLE of the XC expert-blob codec (include/spmoe.h,
- * "XC", format SXC2).  TEST INFRASTRUCTURE ONLY: tests/ compare the sm_100a
+ * "XC", format SXC3).  TEST INFRASTRUCTURE ONLY: tests/ compare the sm_100a
  * encoder's blob byte for byte against oracle_xc_encode and the decoder's
  * output against the original bits; the product path never links this file.
  *
@@ -18,7 +18,7 @@
  *   block  4096 values: sign|mantissa bytes; 32 lane substreams of the
  *          codes of values 128 l .. 128 l + 127, each padded to a word;
  *   layout header at 0, streams from 1280 on 256-byte boundaries in the
- *          order lut, sm, ex (+ 8 slack bytes), bofs, lanes per segment.
+ *          order lut (multi-symbol, u32), sm, ex (+ 8 slack bytes), bofs, lanes per segment.
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -122,6 +122,31 @@ void oracle_xc_lut(const uint8_t len[256], uint16_t lut[1 << LMAX]) {
   }
 }
 
+/* Multi-symbol table from the single-symbol one (restates the derivation
+ * in xc_lut2_of, paper_2510_10302_b200/csrc/spmoe_codec.cu): entry q = up to
+ * three whole codes that fit in the 12 peeked bits.  An unused pattern of
+ * an incomplete code (length 0) still advances by one bit. */
+void oracle_xc_lut2(const uint16_t lut[1 << LMAX], uint32_t lut2[1 << LMAX]) {
+  for (uint32_t q = 0; q < (1u << LMAX); ++q) {
+    const uint32_t e0 = lut[q];
+    uint32_t tot = e0 >> 8, cnt = 1, syms = e0 & 0xffu;
+    if (tot == 0) tot = 1;
+    const uint32_t e1 = lut[q >> tot], l1 = e1 >> 8;
+    if (l1 && tot + l1 <= LMAX) {
+      syms |= (e1 & 0xffu) << 8;
+      cnt = 2;
+      tot += l1;
+      const uint32_t e2 = lut[q >> tot], l2 = e2 >> 8;
+      if (l2 && tot + l2 <= LMAX) {
+        syms |= (e2 & 0xffu) << 16;
+        cnt = 3;
+        tot += l2;
+      }
+    }
+    lut2[q] = syms | (cnt << 24) | (tot << 26);
+  }
+}
+
 /* Encode nseg segments (back to back in src).  Returns the blob size; the
  * blob is written only if out != NULL and cap >= size.  0 on invalid
  * segment sizes. */
@@ -155,7 +180,7 @@ uint64_t oracle_xc_encode(const uint16_t* src, int nseg, const int64_t* seg_n, u
         words += (bits + 31) / 32;
       }
     g->ex_words = (uint32_t)words;
-    g->off_lut = pos; pos = a256(pos + (2u << LMAX));
+    g->off_lut = pos; pos = a256(pos + (4u << LMAX));
     g->off_sm = pos; pos = a256(pos + (uint64_t)n);
     g->off_ex = pos; pos = a256(pos + words * 4 + 8);
     g->off_bofs = pos; pos = a256(pos + (uint64_t)(nb + 1) * 4);
@@ -174,7 +199,9 @@ uint64_t oracle_xc_encode(const uint16_t* src, int nseg, const int64_t* seg_n, u
   for (int i = 0; i < nseg; ++i) {
     const spmoe_xc_segment* g = &hdr.seg[i];
     const int64_t n = (int64_t)g->n, nb = n / SPMOE_XC_BLOCK;
-    oracle_xc_lut(g->len, (uint16_t*)(out + g->off_lut));
+    uint16_t lut1[1 << LMAX];
+    oracle_xc_lut(g->len, lut1);
+    oracle_xc_lut2(lut1, (uint32_t*)(out + g->off_lut));
     uint8_t* sm = out + g->off_sm;
     uint32_t* ex = (uint32_t*)(out + g->off_ex);
     uint32_t* bofs = (uint32_t*)(out + g->off_bofs);
@@ -219,7 +246,8 @@ int oracle_xc_decode(const uint8_t* blob, uint16_t* dst) {
     const spmoe_xc_segment* g = &hdr.seg[i];
     const int64_t n = (int64_t)g->n, nb = n / SPMOE_XC_BLOCK;
     if (n <= 0 || n % SPMOE_XC_BLOCK) return 1;
-    const uint16_t* lut = (const uint16_t*)(blob + g->off_lut);
+    uint16_t lut[1 << LMAX];  /* the decoder walks the single-symbol table built from len[] */
+    oracle_xc_lut(g->len, lut);
     const uint8_t* sm = blob + g->off_sm;
     const uint32_t* ex = (const uint32_t*)(blob + g->off_ex);
     const uint32_t* bofs = (const uint32_t*)(blob + g->off_bofs);

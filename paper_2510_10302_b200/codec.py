@@ -2,7 +2,7 @@
 
 The offload tier's cost is bytes over PCIe (``IoChannel.transfer``,
 ``prefetch.py:45-74``; ``t_io = size / bw + overhead``, ``config.py:229-231``).
-XC (format SXC2 in ``include/spmoe.h``) stores each bf16 weight as its
+XC (format SXC3 in ``include/spmoe.h``) stores each bf16 weight as its
 sign|mantissa byte plus its exponent in the segment's canonical Huffman code
 (<= 12 bits, 32 lane substreams per 4096-value block), so a routed expert
 crosses the link as ~67.5 % of its raw bytes and is expanded bit-exactly
@@ -21,7 +21,7 @@ import torch
 
 from . import _native
 
-XC_MAGIC = 0x32435853  # "SXC2"
+XC_MAGIC = 0x33435853  # "SXC3"
 XC_BLOCK = 4096
 XC_MAX_SEG = 4
 

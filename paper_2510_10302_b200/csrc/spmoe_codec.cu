@@ -1,5 +1,5 @@
 // spmoe_codec.cu — XC, the lossless exponent coding of expert blobs that
-// cross the host link (format SXC2: include/spmoe.h, "XC").
+// cross the host link (format SXC3: include/spmoe.h, "XC").
 //
 // Why: with an offload budget the verify stage is bound by the pinned
 // host -> HBM copies of routed experts (IoChannel.transfer,
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kThreads) xc_write_kernel(const WriteParams p)
 
 // ----------------------------------------------------------------- decode
 struct DecSeg {
-  const uint16_t* lut;
+  const uint32_t* lut2;  // the blob's multi-symbol table
   const uint8_t* sm;
   const uint32_t* ex;
   const uint32_t* bofs;
@@ -216,7 +216,6 @@ static_assert(kStageAlloc * 4 >= ((12 + (kStageWords + 3) * 4 + 15) & ~15), "sta
 constexpr int kWarpSmemWords = kStageAlloc + kLanes * kPitch;
 static_assert(kWarpSmemWords % 4 == 0, "warp buffers stay 16-byte aligned");
 constexpr int kDecSmemBytes = 4 * kLutSize + kDecWarps * kWarpSmemWords * 4 + kDecWarps * 8;
-static_assert(kDecWarps * kWarpSmemWords * 4 >= 2 * kLutSize, "lut1 is built in the warp buffers");
 
 __device__ __forceinline__ uint32_t sh_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -266,33 +265,10 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
   uint32_t* s_lut2 = reinterpret_cast<uint32_t*>(dsm);
   uint8_t* wbase = dsm + 4 * kLutSize;
   const DecSeg& S = p.seg[blockIdx.y];
-  {
-    // the blob's single-symbol table (exponent | length << 8), parked in the
-    // warp buffers while the multi-symbol table is derived from it
-    uint16_t* s_lut = reinterpret_cast<uint16_t*>(wbase);
-    for (int i = threadIdx.x; i < kLutSize / 8; i += kDecThreads)
-      reinterpret_cast<uint4*>(s_lut)[i] = __ldg(reinterpret_cast<const uint4*>(S.lut) + i);
-    __syncthreads();
-    for (int q = threadIdx.x; q < kLutSize; q += kDecThreads) {
-      const uint32_t e0 = s_lut[q];
-      uint32_t tot = e0 >> 8, cnt = 1, syms = e0 & 0xffu;
-      if (tot == 0) tot = 1;  // unused pattern of an incomplete code: always progress
-      const uint32_t e1 = s_lut[(uint32_t)q >> tot], l1 = e1 >> 8;
-      if (l1 && tot + l1 <= (uint32_t)kLmax) {
-        syms |= (e1 & 0xffu) << 8;
-        cnt = 2;
-        tot += l1;
-        const uint32_t e2 = s_lut[(uint32_t)q >> tot], l2 = e2 >> 8;
-        if (l2 && tot + l2 <= (uint32_t)kLmax) {
-          syms |= (e2 & 0xffu) << 16;
-          cnt = 3;
-          tot += l2;
-        }
-      }
-      s_lut2[q] = syms | (cnt << 24) | (tot << 26);
-    }
-    __syncthreads();
-  }
+  // the segment's multi-symbol table, precomputed in the blob (lut2)
+  for (int i = threadIdx.x; i < kLutSize / 4; i += kDecThreads)
+    reinterpret_cast<uint4*>(s_lut2)[i] = __ldg(reinterpret_cast<const uint4*>(S.lut2) + i);
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* stage = reinterpret_cast<uint32_t*>(wbase) + warp * kWarpSmemWords;
   uint32_t* ew = stage + kStageAlloc;
@@ -467,6 +443,28 @@ void lut_of(const Codes& c, uint16_t* lut) {
   }
 }
 
+// Multi-symbol table (restated in oracle_xc_lut2, oracle/xc_oracle.c).
+void lut2_of(const uint16_t* lut, uint32_t* lut2) {
+  for (uint32_t q = 0; q < (uint32_t)kLutSize; ++q) {
+    const uint32_t e0 = lut[q];
+    uint32_t tot = e0 >> 8, cnt = 1, syms = e0 & 0xffu;
+    if (tot == 0) tot = 1;  // unused pattern of an incomplete code: always progress
+    const uint32_t e1 = lut[q >> tot], l1 = e1 >> 8;
+    if (l1 && tot + l1 <= (uint32_t)kLmax) {
+      syms |= (e1 & 0xffu) << 8;
+      cnt = 2;
+      tot += l1;
+      const uint32_t e2 = lut[q >> tot], l2 = e2 >> 8;
+      if (l2 && tot + l2 <= (uint32_t)kLmax) {
+        syms |= (e2 & 0xffu) << 16;
+        cnt = 3;
+        tot += l2;
+      }
+    }
+    lut2[q] = syms | (cnt << 24) | (tot << 26);
+  }
+}
+
 bool valid_segments(int nseg, const int64_t* seg_n) {
   if (nseg < 1 || nseg > SPMOE_XC_MAX_SEG || !seg_n) return false;
   for (int i = 0; i < nseg; ++i)
@@ -555,7 +553,7 @@ int spmoe_xc_plan(const uint16_t* src, int nseg, const int64_t* seg_n, void* wor
     spmoe_xc_segment& g = hdr->seg[i];
     const int64_t n = seg_n[i], nb = nblocks(n);
     g.ex_words = tot[i];
-    g.off_lut = pos; pos = align256(pos + 2 * (uint64_t)kLutSize);
+    g.off_lut = pos; pos = align256(pos + 4 * (uint64_t)kLutSize);
     g.off_sm = pos; pos = align256(pos + (uint64_t)n);
     g.off_ex = pos; pos = align256(pos + (uint64_t)g.ex_words * 4 + 8);
     g.off_bofs = pos; pos = align256(pos + (uint64_t)(nb + 1) * 4);
@@ -578,6 +576,7 @@ int spmoe_xc_encode(const uint16_t* src, const spmoe_xc_header* hdr, const void*
   if (e != cudaSuccess) return (int)e;
   const uint32_t* wk = (const uint32_t*)work;
   std::vector<uint16_t> luts((size_t)hdr->nseg * kLutSize);
+  std::vector<uint32_t> luts2((size_t)hdr->nseg * kLutSize);
   size_t off = 0;
   const uint16_t* s = src;
   for (uint32_t i = 0; i < hdr->nseg; ++i) {
@@ -595,13 +594,14 @@ int spmoe_xc_encode(const uint16_t* src, const spmoe_xc_header* hdr, const void*
     cudaMemcpyAsync(blob + g.off_bofs, p.bofs, (nb + 1) * 4, cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(blob + g.off_lanes, p.lanes, nb * kLanes, cudaMemcpyDeviceToDevice, st);
     lut_of(p.c, &luts[(size_t)i * kLutSize]);
-    cudaMemcpyAsync(blob + g.off_lut, &luts[(size_t)i * kLutSize], 2 * kLutSize, cudaMemcpyHostToDevice, st);
+    lut2_of(&luts[(size_t)i * kLutSize], &luts2[(size_t)i * kLutSize]);
+    cudaMemcpyAsync(blob + g.off_lut, &luts2[(size_t)i * kLutSize], 4 * kLutSize, cudaMemcpyHostToDevice, st);
     off += seg_work_words(n);
     s += n;
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
   if ((e = cudaMemcpyAsync(blob, hdr, sizeof(*hdr), cudaMemcpyHostToDevice, st)) != cudaSuccess) return (int)e;
-  return (int)cudaStreamSynchronize(st);  // luts / hdr are host memory
+  return (int)cudaStreamSynchronize(st);  // luts / luts2 / hdr are host memory
 }
 
 int spmoe_xc_decode_segments(const uint8_t* blob, const spmoe_xc_header* hdr, int first, int count,
@@ -618,7 +618,7 @@ int spmoe_xc_decode_segments(const uint8_t* blob, const spmoe_xc_header* hdr, in
     const spmoe_xc_segment& g = hdr->seg[first + j];
     if (g.n == 0 || g.n % SPMOE_XC_BLOCK) return (int)cudaErrorInvalidValue;
     DecSeg& S = p.seg[j];
-    S.lut = (const uint16_t*)(blob + g.off_lut);
+    S.lut2 = (const uint32_t*)(blob + g.off_lut);
     S.sm = blob + g.off_sm;
     S.ex = (const uint32_t*)(blob + g.off_ex);
     S.bofs = (const uint32_t*)(blob + g.off_bofs);
