@@ -306,8 +306,9 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
     if (nw <= (uint32_t)kStageWords) {
       const uint32_t delta = (uint32_t)((uintptr_t)run & 15);  // 0, 4, 8 or 12
       if (lane == 0) {
-        // the run + 3 peek words (the stream has 12 readable slack bytes,
-        // then the segment's block offsets), from its 16-byte-aligned start
+        // the run + 3 peek words from its 16-byte-aligned start, rounded up
+        // to 16 bytes: past the stream's 8 slack bytes come the segment's
+        // block offsets, so the copy never leaves the segment
         const uint32_t bytes = (delta + (nw + 3) * 4 + 15) & ~15u;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after last block's reads
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sh_u32(mbar)), "r"(bytes)
