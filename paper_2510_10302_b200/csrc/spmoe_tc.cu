@@ -50,6 +50,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+// Programmatic dependent launch: a kernel lets the next one in its stream
+// start launching (its CTAs then run their prologue on free SMs), and that
+// one waits for this grid's completion and memory before touching its
+// inputs.  Both are no-ops for kernels launched without the attribute.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -210,8 +217,9 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__
   const int kblocks = K / BK;
   const int mtiles = R / BM;
   const int split = p.split;
+  pdl_launch_dependents();
 
-  build_tiles(p, mtiles, split, &tl);
+  build_tiles(p, mtiles, split, &tl);  // offsets come from K2, two launches back
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -233,6 +241,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_sh;
   const int ntiles = tl.start[tl.n_active];
+  pdl_wait();  // the previous kernel's activations / partials are complete
 
   if (warp == 0) {
     if (lane == 0) {
@@ -554,6 +563,8 @@ ffn_tc_fused_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_con
 __global__ void reduce_split_kernel(const float* __restrict__ part, int split, int rows, int H,
                                     const int32_t* __restrict__ offsets, int E, uint64_t mask,
                                     float* __restrict__ y) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t n = (int64_t)rows * H;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(i / H);
@@ -570,6 +581,8 @@ __global__ void reduce_split_kernel(const float* __restrict__ part, int split, i
 __global__ void reduce_swiglu_kernel(const float* __restrict__ part, int split, int rows, int F,
                                      const int32_t* __restrict__ offsets, int E, uint64_t mask,
                                      uint16_t* __restrict__ h) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t n = (int64_t)rows * F;
   const float* up = part + (int64_t)split * n;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -589,6 +602,7 @@ __global__ void reduce_swiglu_kernel(const float* __restrict__ part, int split, 
 // x_perm[r] = x[perm[r]] (activation rows grouped by expert for TMA).
 __global__ void gather_rows_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ perm,
                                    const int32_t* __restrict__ offsets, int E, int H, uint16_t* __restrict__ out) {
+  pdl_launch_dependents();  // launched normally: its inputs are complete
   const int rows = offsets[E];
   const int nch = H >> 3;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)rows * nch;
@@ -632,6 +646,22 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, 
   return r == CUDA_SUCCESS;
 }
 
+// Launch with programmatic stream serialization (see pdl_wait).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <bool UP, int STAGES>
 int launch(const CUtensorMap& mw, const CUtensorMap& ma, const Params& p, int nsms, cudaStream_t s) {
   constexpr int NA = UP ? 2 : 1;
@@ -642,8 +672,7 @@ int launch(const CUtensorMap& mw, const CUtensorMap& ma, const Params& p, int ns
     cudaFuncSetAttribute(ffn_tc_kernel<UP, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  ffn_tc_kernel<UP, STAGES><<<nsms, kThreads, smem, s>>>(mw, ma, p);
-  return (int)cudaGetLastError();
+  return (int)launch_pdl(ffn_tc_kernel<UP, STAGES>, dim3(nsms), dim3(kThreads), smem, s, mw, ma, p);
 }
 
 }  // namespace tc
@@ -705,9 +734,8 @@ extern "C" int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, con
   st = launch<true, 5>(mw_up, ma_up, p, nsms, s);
   if (st) return st;
   if (split_up > 1) {
-    reduce_swiglu_kernel<<<nsms * 4, 256, 0, s>>>(workspace, split_up, rows, F, expert_offsets, E, expert_mask,
-                                                   h_scratch);
-    st = (int)cudaGetLastError();
+    st = (int)launch_pdl(reduce_swiglu_kernel, dim3(nsms * 4), dim3(256), 0, s, (const float*)workspace, split_up,
+                         rows, F, expert_offsets, E, expert_mask, h_scratch);
     if (st) return st;
   }
   p.split = split_dn;
@@ -715,8 +743,8 @@ extern "C" int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, con
   st = launch<false, 8>(mw_dn, ma_dn, p, nsms, s);
   if (st) return st;
   if (split_dn > 1) {
-    reduce_split_kernel<<<nsms * 4, 256, 0, s>>>(workspace, split_dn, rows, H, expert_offsets, E, expert_mask, y);
-    st = (int)cudaGetLastError();
+    st = (int)launch_pdl(reduce_split_kernel, dim3(nsms * 4), dim3(256), 0, s, (const float*)workspace, split_dn,
+                         rows, H, expert_offsets, E, expert_mask, y);
   }
   k3_timing_end(s);
   return st;
@@ -787,8 +815,8 @@ extern "C" int spmoe_expert_ffn_tc_fused(const uint16_t* pool, int64_t slot_elem
                                         smem, s);
   if (st) return st;
   if (split_dn > 1) {
-    reduce_split_kernel<<<nsms * 4, 256, 0, s>>>(workspace, split_dn, rows, H, expert_offsets, E, expert_mask, y);
-    st = (int)cudaGetLastError();
+    st = (int)launch_pdl(reduce_split_kernel, dim3(nsms * 4), dim3(256), 0, s, (const float*)workspace, split_dn,
+                         rows, H, expert_offsets, E, expert_mask, y);
   }
   k3_timing_end(s);
   return st;
