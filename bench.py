@@ -39,12 +39,14 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "TPOT ms and tokens/s, Mixtral-8x7B SD+offload; verify-MoE HBM GB/s; H2D GB/s"
 UNIT = "tokens/s"
+CPU_SAMPLE_LAYERS = 4
 
 CONFIGS = {
     # configs[1]: the headline
-    "mixtral": dict(arch="mixtral_8x7b", budget=0.25, N=4, batch=1, prompt=64),
-    "deepseek": dict(arch="deepseek_v2_lite", budget=0.25, N=4, batch=1, prompt=64),
-    "qwen": dict(arch="qwen15_moe_a27b", budget=0.25, N=4, batch=1, prompt=64),
+    # 128-token synthetic prompts
+    "mixtral": dict(arch="mixtral_8x7b", budget=0.25, N=4, batch=1, prompt=128),
+    "deepseek": dict(arch="deepseek_v2_lite", budget=0.25, N=4, batch=1, prompt=128),
+    "qwen": dict(arch="qwen15_moe_a27b", budget=0.25, N=4, batch=1, prompt=128),
     "tiny": dict(arch="tiny", budget=0.375, N=4, batch=1, prompt=16),
 }
 
@@ -127,117 +129,118 @@ def h2d_peak_gbs(torch, nbytes=1 << 30, reps=5) -> float:
 # CPU restatement (oracle port) of the same path: the reference arm and the
 # cpu_baseline leg.  Executes oracle/ only here, as the timed CPU baseline.
 # ---------------------------------------------------------------------------
-class CpuPath:
-    """The verify-time expert path of one SD iteration restated on the host
-    cores (oracle/spmoe_oracle.c, all threads): for ``sample_layers`` target
-    layers, K1 router + K2 permute + K3 SwiGLU experts + K4 combine at
-    T = B*(N+1) tokens, plus the drafting-stage predictor projections (K1,
-    k = prefetch_k) of the layers <= cutoff for N draft steps; scaled to all
-    layers; plus K6 acceptance.  Expert blobs are built once (setup), from
-    the GPU run's host pool when given, else regenerated with the same
-    counter-hash streams."""
-
-    def __init__(self, arch, seed, N, B, prefetch_k, cutoff, sample_layers, threads, blob_rows=None):
-        import numpy as np
-
-        from oracle import tensor_oracle as O
-        from paper_2510_10302_b200.model import K_EXPERT, K_ROUTER, _splitmix64, tensor_seed
-
-        self.O, self.arch, self.N, self.B = O, arch, N, B
-        self.prefetch_k, self.cutoff = prefetch_k, cutoff
-        O.set_threads(threads)
-        H, F, E = arch.hidden, arch.ffn, arch.num_experts
-        self.T = B * (N + 1)
-        rng = np.random.default_rng(seed)
-        self.x = O.f32_to_bf16_bits(rng.standard_normal((self.T, H)).astype(np.float32))
-        self.resid = O.f32_to_bf16_bits(rng.standard_normal((self.T, H)).astype(np.float32) * 0.1)
-        self.layers = list(range(sample_layers))
-        self.blobs = {}
-        n13 = F * H
-        for l in self.layers:
-            rw = O.fill_normal_bf16(E * H, tensor_seed(seed, K_ROUTER, l), 0, 1.0 / np.sqrt(H)).reshape(E, H)
-            eb = []
-            for e in range(E):
-                if blob_rows is not None:
-                    eb.append(blob_rows(l, e))
-                    continue
-                s0 = tensor_seed(seed, K_EXPERT, l * E + e)
-                b = np.empty(3 * n13, np.uint16)
-                b[:n13] = O.fill_normal_bf16(n13, _splitmix64(s0 ^ 1), 0, arch.init_std)
-                b[n13:2 * n13] = O.fill_normal_bf16(n13, _splitmix64(s0 ^ 3), 0, arch.init_std)
-                b[2 * n13:] = O.fill_normal_bf16(n13, _splitmix64(s0 ^ 2), 0, arch.init_std * arch.res_scale)
-                eb.append(b)
-            self.blobs[l] = (rw, eb)
-        self.logits = rng.standard_normal((B, N + 1, 4096)).astype(np.float32)
-        self.draft = rng.integers(0, 4096, (B, N)).astype(np.int32)
-
-    def iteration_seconds(self) -> float:
-        O, a = self.O, self.arch
-        E, k = a.num_experts, a.top_k
-        xd = self.x[: self.B]
-        t0 = time.perf_counter()
-        for l in self.layers:
-            rw, eb = self.blobs[l]
-            w, idx, _, _ = O.router_topk(self.x, rw, k, a.renorm)
-            off, perm, inv = O.moe_permute(idx, E)
-            used = set(int(v) for v in idx.ravel())
-            _, y = O.expert_ffn([eb[e] if e in used else None for e in range(E)], self.x, a.ffn, off, perm)
-            O.moe_combine(y, inv, w, self.T, a.hidden, k, residual=self.resid)
-            if self.cutoff is not None and l <= self.cutoff:
-                for _ in range(self.N):
-                    O.router_topk(xd, rw, self.prefetch_k, True)
-        t_layers = time.perf_counter() - t0
-        t1 = time.perf_counter()
-        O.greedy_accept(self.logits, self.draft)
-        t_acc = (time.perf_counter() - t1) * a.vocab / 4096
-        return t_layers * a.num_layers / len(self.layers) + t_acc
+def kv_max_seq(arch, cfg) -> int:
+    """The engine's KV capacity for this config (SpecMoEEngine max_seq)."""
+    N = cfg["N"]
+    return min(arch.max_seq, cfg["prompt"] + 64 * (N + 1) + N + 8)
 
 
-def calibration(cfg_name: str) -> dict:
-    p = ROOT / "profiles" / "bench_calibration.json"
-    if p.exists():
-        return json.loads(p.read_text()).get(cfg_name, {})
-    return {}
+def bench_prompts(arch, cfg, rank):
+    import torch
+
+    g = torch.Generator().manual_seed(1000 + rank)
+    return torch.randint(0, arch.vocab, (cfg["batch"], cfg["prompt"]), generator=g)
+
+
+def cpu_sd(arch, cfg, threads, layers=None, log_fn=None):
+    """The SD loop on the host cores (oracle/cpu_model.py: the CPU
+    restatement of the engine's draft forward, predictor, verify MoE and
+    greedy acceptance on the same determinism contract), on weights
+    regenerated on the CPU with the engine's counter-hash streams -- the
+    same model bit for bit (tests/test_e2e_gpu.py), no GPU involved.
+    ``layers``: keep only the first ``layers`` decoder layers (bounded
+    sample)."""
+    from dataclasses import replace
+
+    from oracle import cpu_model as CM
+    from oracle import tensor_oracle as O
+
+    O.set_threads(threads)
+    a = replace(arch, num_layers=layers) if layers else arch
+    t0 = time.perf_counter()
+    w = CM.CpuWeights.generate(a, 1234)
+    t_gen = time.perf_counter() - t0
+    pk = 1 if arch.num_experts <= 16 else arch.top_k
+    # the drafting-stage predictor runs at layer 0 (the cutoff the GPU arm's
+    # recalibration settles on at this config); it is a few router dots
+    sd = CM.CpuSD(w, batch=cfg["batch"], N=cfg["N"], kv_max_seq=kv_max_seq(arch, cfg), cutoff=0, prefetch_k=pk)
+    t0 = time.perf_counter()
+    sd.prefill(bench_prompts(arch, cfg, 0).numpy())
+    t_pre = time.perf_counter() - t0
+    if log_fn:
+        log_fn(f"[cpu] {a.num_layers}-layer model generated in {t_gen:.1f}s, prefill {t_pre:.1f}s, {threads} threads")
+    return sd, t_gen, t_pre
+
+
+def host_threads() -> int:
+    try:  # the CPU path may use every host core, not just the GPU's socket
+        os.sched_setaffinity(0, range(os.cpu_count() or 1))
+    except OSError:
+        pass
+    return len(os.sched_getaffinity(0))
 
 
 def run_reference(args, cfg, rank, world):
     """--impl reference: the CPU restatement of the path (oracle port; the
     reference package is a Python simulator with no tensor path and cannot
-    travel to the GPU box), all host threads, bounded samples."""
-    import numpy as np
-
+    travel to the GPU box) on all host threads.  Every step is one FULL SD
+    iteration of the configured model (all layers: N draft steps with the
+    draft-guided predictor, the N+1-token verify through every MoE layer,
+    lm_head, greedy acceptance); tokens come from this CPU loop itself."""
     from paper_2510_10302_b200.model import get_arch
 
     if rank != 0:
         return
     arch = get_arch(cfg["arch"])
-    threads = os.cpu_count() or 1
-    cal = calibration(args.config)
-    emitted = cal.get("emitted_per_iter", cfg["N"] + 1) * cfg["batch"]
-    sample_layers = 2 if arch.hidden >= 4096 else 4
-    pk = 1 if arch.num_experts <= 16 else arch.top_k
-    path = CpuPath(arch, 1234, cfg["N"], cfg["batch"], pk, cal.get("cutoff"), sample_layers, threads)
+    threads = host_threads()
+    sd, t_gen, t_pre = cpu_sd(arch, cfg, threads, log_fn=log)
+    for _ in range(args.warmup):
+        sd.step()
+    emitted = 0
     times = []
-    for i in range(args.warmup + args.steps):
-        t = path.iteration_seconds()
-        if i >= args.warmup:
-            times.append(t)
-    it_s = float(np.mean(times))
-    value = emitted / it_s
-    sample = (f"per step: {sample_layers} of {arch.num_layers} verify-MoE layers (K1 router, permute, SwiGLU "
-              f"experts, combine) at T={cfg['batch'] * (cfg['N'] + 1)} + drafting-stage predictor projections, "
-              f"scaled to {arch.num_layers} layers; {emitted:.3f} emitted tokens/iteration "
-              f"({'calibrated from our GPU run' if cal else 'upper bound N+1'})")
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        emitted += sum(sd.step())
+        times.append(time.perf_counter() - t)
+    total = sum(times)
+    value = emitted / total
+    it_ms = total / args.steps * 1e3
+    B, N = cfg["batch"], cfg["N"]
+    sample = (f"{args.steps} timed full SD iterations (after {args.warmup} warm-up) of {arch.name}: all "
+              f"{arch.num_layers} layers, N={N} draft steps + {N + 1}-token verify + lm_head + greedy acceptance, "
+              f"batch {B}, prompt {cfg['prompt']}; oracle/cpu_model.py on {threads} threads; "
+              f"{emitted / args.steps / B:.2f} tokens/iteration from this CPU loop")
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": it_s * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": it_ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16 weights, fp32 accumulate", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {arch.name} SD verify path, N={cfg['N']}, batch {cfg['batch']}"},
-        "tpot_ms": it_s * 1e3 / emitted,
+        "config": {"workload": f"{args.config}: {arch.name} SD verify path, N={N}, batch {B}",
+                   "prompt_len": cfg["prompt"]},
+        "tpot_ms": total * 1e3 / (emitted / B) if emitted else None,
+        "tokens_emitted": emitted,
+        "setup_s": {"generate_weights": t_gen, "prefill": t_pre},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
+
+
+def spawn_ranks(args) -> int:
+    """``--gpus N`` without a torchrun environment: launch N ranks of this
+    script through torch.distributed.run on 127.0.0.1 (one process per
+    GPU), forward its exit status.  Rank 0 prints the JSON line."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # rank/channel count visible in the log
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py")] + sys.argv[1:]
+    log(f"[bench] spawning {args.gpus} ranks: {' '.join(cmd)}")
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -258,7 +261,6 @@ def main():
                     help="experts with fewer routed tokens take the CUDA-core K3 (default 1: tcgen05 for every expert)")
     ap.add_argument("--host-codec", default="xc", choices=["xc", "none"],
                     help="host-tier expert encoding: xc (lossless exponent coding) or raw bf16")
-    ap.add_argument("--write-calibration", action="store_true")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.batch:
@@ -269,9 +271,14 @@ def main():
         cfg["budget"] = args.budget
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(spawn_ranks(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        log(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}")
+        sys.exit(2)
 
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
@@ -301,6 +308,8 @@ def main():
     arch = get_arch(cfg["arch"])
     E_all = arch.num_layers * arch.num_experts
     capacity = max(arch.num_experts, int(round(cfg["budget"] * E_all)))
+    if world > 1:
+        dist.barrier()  # every rank copies at once: the concurrent host-link peak
     peak_h2d = h2d_peak_gbs(torch)
     hw = HardwareSpec(gpu_memory=183_359 * 2**20, peak_non_expert_memory=24 * 10**9, pcie_bandwidth=peak_h2d * 1e9,
                       name="b200")
@@ -342,8 +351,7 @@ def main():
                         window_tokens=cfg["N"], host_share=share, host_leader=leader, host_distinct=distinct,
                         ffn_impl=args.ffn_impl, host_codec=None if args.host_codec == "none" else "xc",
                         tc_min_tokens=args.tc_min_tokens)
-    g = torch.Generator().manual_seed(1000 + rank)
-    prompts = torch.randint(0, arch.vocab, (cfg["batch"], cfg["prompt"]), generator=g)
+    prompts = bench_prompts(arch, cfg, rank)
     eng.prefill(prompts)
     log(f"[bench] setup {time.perf_counter() - t_setup:.1f}s capacity={capacity} cutoff={eng.cutoff} "
         f"h2d_peak={peak_h2d:.1f}GB/s timings={timings}")
@@ -393,12 +401,17 @@ def main():
     rep = eng.report(wall_s=wall)
     roof = eng.k3_roofline()
     dec = eng.cache.decode_stats() if eng.host_pool.codec else None
+    per_rank = None
     stats = torch.tensor([dev_ms, wall, float(emitted)], dtype=torch.float64, device="cpu" if share_gpu else "cuda")
     if world > 1:
         mx = stats.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm = stats.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, {"h2d_peak_gbs": peak_h2d, "h2d_gbs": rep.extras.get("h2d_wire_gbs"),
+                                          "link_busy_frac": rep.extras.get("link_busy_frac"),
+                                          "tokens": emitted, "device_ms": dev_ms})
         dev_ms, wall, emitted_all = float(mx[0]), float(mx[1]), float(sm[2])
     else:
         emitted_all = float(emitted)
@@ -454,6 +467,9 @@ def main():
         # decoded expert bytes per copy second are higher by 1 / wire_ratio
         "h2d_gbs": ex.get("h2d_wire_gbs"),
         "h2d_peak_gbs": peak_h2d,
+        # world > 1: each rank's pinned peak measured concurrently with all
+        # others (shared host DRAM / PCIe switches) and its timed-region link use
+        "per_rank": per_rank if world > 1 else None,
         "h2d_frac": (ex.get("h2d_wire_gbs") or 0.0) / peak_h2d if peak_h2d else None,
         "h2d_expert_gbs": ex.get("h2d_gbs"),
         "host_codec": {"codec": ex.get("host_codec") or "raw", "wire_ratio": ex.get("h2d_wire_ratio")},
@@ -506,41 +522,31 @@ def main():
     dom = max(cands, key=lambda r: r["ms_per_step"])
     out["roofline"] = dict(dom, dominant_by="GPU ms per step in the timed region, "
                            + ", ".join(f"{r['kernel'].split(' ')[0]} {r['ms_per_step']:.1f}" for r in cands))
-    if rank == 0 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        try:  # the CPU path may use every host core, not just the GPU's socket
-            os.sched_setaffinity(0, range(threads))
-        except OSError:
-            threads = len(os.sched_getaffinity(0))
+    eng.close()  # releases the pinned host pool before the CPU leg allocates its own weights
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # bounded sample (~10-30 s of CPU work): full SD iterations of the
+        # first CPU_SAMPLE_LAYERS decoder layers of the same model (identical
+        # per-layer shapes and arithmetic), time scaled by L / layers; the
+        # unscaled full-model loop is `bench.py --impl reference`
+        threads = host_threads()
+        nl = min(CPU_SAMPLE_LAYERS, arch.num_layers)
+        sd, _, _ = cpu_sd(arch, cfg, threads, layers=nl)
+        sd.step()  # warm-up
+        t0 = time.perf_counter()
+        for _ in range(2):
+            sd.step()
+        t_it = (time.perf_counter() - t0) / 2 * arch.num_layers / nl
         emitted_per_iter = emitted / args.steps
-        sample_layers = 2
-        hp = eng.host_pool
-        from oracle import tensor_oracle as O
-
-        def blob_rows(l, e):
-            # the CPU path computes on raw bf16 experts in host RAM
-            r = hp.row_of(l, e)
-            return hp.array[r] if hp.codec is None else O.xc_decode(hp.row_bytes(r))
-
-        path = CpuPath(arch, 1234, N, B, policy.prefetch_k, eng.cutoff, sample_layers, threads,
-                       blob_rows=blob_rows)
-        path.iteration_seconds()  # warm caches / page in
-        t_cpu = min(path.iteration_seconds() for _ in range(2))
         out["cpu_baseline"] = {
-            "value": emitted_per_iter / t_cpu, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{sample_layers} of {arch.num_layers} verify-MoE layers + predictor projections on the CPU "
-                      f"oracle (oracle/spmoe_oracle.c, {threads} threads), scaled to one SD iteration; "
-                      f"{emitted_per_iter:.2f} emitted tokens/iteration from this run",
-            "ms_per_iteration": t_cpu * 1e3,
+            "value": emitted_per_iter / t_it, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"2 full SD iterations (draft, predictor, verify MoE, lm_head, acceptance) of the first {nl} "
+                      f"of {arch.num_layers} layers on oracle/cpu_model.py ({threads} threads), per-layer time "
+                      f"scaled to {arch.num_layers} layers; {emitted_per_iter:.2f} tokens/iteration from this "
+                      f"GPU run (the unscaled full-model CPU loop is the --impl reference arm)",
+            "ms_per_iteration": t_it * 1e3,
         }
-    if rank == 0 and args.write_calibration:
-        p = ROOT / "profiles" / "bench_calibration.json"
-        d = json.loads(p.read_text()) if p.exists() else {}
-        d[args.config] = {"emitted_per_iter": emitted / args.steps / B, "cutoff": eng.cutoff}
-        p.write_text(json.dumps(d, indent=1))
     if rank == 0:
         print(json.dumps(out), flush=True)
-    eng.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -220,25 +220,52 @@ int spmoe_argmax_rows(const float* logits, int64_t ld, int rows, int V, int32_t*
 /* and the target verify pass outside the MoE; simcore.py:323-359).       */
 /* Latency-bound helpers that replace ~30 framework kernels per layer.    */
 /* --------------------------------------------------------------------- */
-/* out[r] = bf16(x[r] * rsqrt(mean(x[r]^2) + eps) * w), rows of H (H % 8 == 0). */
+/* out[r] = bf16((x[r] * s) * w), s = 1 / sqrt(dot_fixed(x[r], x[r]) / H + eps)
+ * (IEEE division and square root), rows of H (H % 8 == 0). */
 int spmoe_rms_norm(const uint16_t* x, const uint16_t* w, int rows, int H, float eps, uint16_t* out,
                    void* stream);
 /*
  * qkv     [B*T, (nh + 2*nkv)*hd] bf16  fused projection output
- * cos/sin [max_pos, hd] f32 rotate-half RoPE tables
+ * cos/sin [max_pos, hd] f32 rotate-half RoPE tables (host-computed, shared
+ *         bit for bit with the oracle)
  * start   [B] i64 device: position of each sequence's first new token
  * q_out   [B, nh, T, hd] bf16 out (rotated queries)
  * k_cache, v_cache [B, nkv, S, hd] bf16: rotated keys / values appended
  *         at positions start[b] .. start[b] + T - 1
+ * y = bf16(x*cos + rot*sin), each product and the sum IEEE-rounded.
+ * Rows whose position is >= S or >= max_pos write nothing (callers check
+ * lengths first; the guard keeps a bad position from corrupting memory).
  */
 int spmoe_rope_kv(const uint16_t* qkv, const float* cos_t, const float* sin_t, const int64_t* start,
-                  int B, int T, int nh, int nkv, int hd, int S, uint16_t* q_out, uint16_t* k_cache,
-                  uint16_t* v_cache, void* stream);
+                  int B, int T, int nh, int nkv, int hd, int S, int max_pos, uint16_t* q_out,
+                  uint16_t* k_cache, uint16_t* v_cache, void* stream);
 /* Causal GQA attention of the T new queries over keys 0 .. start[b] + t;
- * out [B, T, nh*hd] bf16; hd in {64, 128}; online softmax in fp32. */
+ * out [B, T, nh*hd] bf16; hd in {64, 128}; S * 32 + 33 KB of shared memory
+ * must fit 200 KB.  Fixed order: scores by lane-blocked dims + butterfly,
+ * det_exp(s - max), 8 key streams (key mod 8) summed ascending and merged in
+ * stream order, IEEE division (restated in oracle/forward_oracle.c). */
 int spmoe_attention(const uint16_t* q, const uint16_t* k_cache, const uint16_t* v_cache,
                     const int64_t* start, int B, int T, int nh, int nkv, int hd, int S, float scale,
                     uint16_t* out, void* stream);
+
+/* --------------------------------------------------------------------- */
+/* K9  linear: the projections around the MoE (fused qkv, W_o, lm_head)   */
+/*   of the draft and target forwards (SURVEY §8(f) rows 1-2,            */
+/*   simcore.py:323-359 compute slots; PAPER.md:352 draft model).         */
+/* --------------------------------------------------------------------- */
+/*
+ * y[t][n] = dot_fixed(w[n, 0:K], xin[t, 0:K]) with the determinism
+ * contract's order (K % 8 == 0).  xin = x, or RMSNorm(x; norm_w, eps) when
+ * norm_w != NULL (spmoe_rms_norm's arithmetic, fused into the staging).
+ *   y_f32  != NULL: y_f32[t*ldy + n] = y (fp32, e.g. lm_head logits)
+ *   y_bf16 != NULL: y_bf16[t*N + n] = bf16(y), or with resid != NULL
+ *                   bf16(resid[t*N + n] + bf16(y)) (resid may alias y_bf16)
+ * Weight-streaming, one warp per weight row, activations staged in shared
+ * memory 16 rows at a time.
+ */
+int spmoe_linear(const uint16_t* w, const uint16_t* x, int64_t ldx, int T, int K, int N,
+                 const uint16_t* norm_w, float eps, float* y_f32, int64_t ldy, uint16_t* y_bf16,
+                 const uint16_t* resid, void* stream);
 
 /* --------------------------------------------------------------------- */
 /* K5  h2d_batch                                                          */

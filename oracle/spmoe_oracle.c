@@ -24,7 +24,8 @@
  *   list); top-k tie-break is pinned to the reference's own known answers
  *   (test_trace.py:41-43, test_predictor.py:57-70) in tests/.
  *
- * Build: oracle/Makefile (gcc -O2 -ffp-contract=off, pthreads).  No
+ * Build: oracle/Makefile (gcc -O2 -ffp-contract=off, pthreads; parallel
+ * loops on the persistent pool of oracle/pool.c).  No
  * FMA contraction, no fast-math: every float operation is an IEEE
  * round-to-nearest single-precision op in the order written.
  */
@@ -33,51 +34,11 @@
 #include <stdlib.h>
 #include <string.h>
 
-#include <pthread.h>
+#include "pool.h"
 
-/* ------------------------------------------------------------------ */
-/* parallel-for over rows on plain pthreads (each row is computed       */
-/* independently in a fixed order, so results do not depend on the      */
-/* thread count)                                                        */
-/* ------------------------------------------------------------------ */
-static int g_threads = 1;
-
-void oracle_set_threads(int n) { g_threads = n > 0 ? n : 1; }
-int oracle_num_threads(void) { return g_threads; }
-
-typedef void (*row_fn)(void* ctx, int64_t i);
-typedef struct {
-  row_fn fn;
-  void* ctx;
-  int64_t lo, hi;
-} span_t;
-
-static void* span_main(void* a) {
-  span_t* s = (span_t*)a;
-  for (int64_t i = s->lo; i < s->hi; ++i) s->fn(s->ctx, i);
-  return NULL;
-}
-
-static void parallel_for(int64_t n, row_fn fn, void* ctx) {
-  int nt = g_threads;
-  if (nt > n) nt = (int)(n > 0 ? n : 1);
-  if (nt <= 1) {
-    for (int64_t i = 0; i < n; ++i) fn(ctx, i);
-    return;
-  }
-  pthread_t th[256];
-  span_t sp[256];
-  if (nt > 256) nt = 256;
-  for (int t = 0; t < nt; ++t) {
-    sp[t].fn = fn;
-    sp[t].ctx = ctx;
-    sp[t].lo = n * t / nt;
-    sp[t].hi = n * (t + 1) / nt;
-    if (t > 0) pthread_create(&th[t], NULL, span_main, &sp[t]);
-  }
-  span_main(&sp[0]);
-  for (int t = 1; t < nt; ++t) pthread_join(th[t], NULL);
-}
+/* parallel loops: oracle/pool.c (persistent workers, contiguous spans) */
+#define parallel_for oracle_parallel_for
+typedef oracle_row_fn row_fn;
 
 /* ------------------------------------------------------------------ */
 /* scalar helpers                                                       */
@@ -131,16 +92,18 @@ float oracle_det_silu(float g) { return g / (1.0f + oracle_det_exp(-g)); }
  * lane-0 value is the pairwise tree below.
  */
 float oracle_dot_fixed(const uint16_t* a, const uint16_t* b, int n) {
-  float lane[32];
+  float lane[32] = {0};
   const int nch = n / 8;
-  for (int j = 0; j < 32; ++j) {
-    float acc = 0.0f;
-    for (int c = j; c < nch; c += 32) {
-      const uint16_t* pa = a + 8 * c;
-      const uint16_t* pb = b + 8 * c;
+  /* chunk groups outer, lanes inner: each lane still sees its chunks in
+   * ascending order, but the 32 short chains overlap in the pipeline */
+  for (int c0 = 0; c0 < nch; c0 += 32) {
+    for (int j = 0; j < 32 && c0 + j < nch; ++j) {
+      const uint16_t* pa = a + 8 * (c0 + j);
+      const uint16_t* pb = b + 8 * (c0 + j);
+      float acc = lane[j];
       for (int v = 0; v < 8; ++v) acc = acc + bf2f(pa[v]) * bf2f(pb[v]);
+      lane[j] = acc;
     }
-    lane[j] = acc;
   }
   for (int w = 16; w >= 1; w >>= 1)
     for (int j = 0; j < w; ++j) lane[j] = lane[j] + lane[j + w];

@@ -36,13 +36,30 @@ _SIGS = {
     "oracle_fill_normal_bf16": (None, [_p, _i64, _u64, _u64, _f]),
     "oracle_set_threads": (None, [_i]),
     "oracle_num_threads": (_i, []),
+    "oracle_rms_scale": (_f, [_p, _i, _f]),
+    "oracle_rms_norm": (None, [_p, _p, _i, _i, _f, _p]),
+    "oracle_linear": (None, [_p, _p, _i64, _i, _i, _i, _p, _f, _p, _i64, _p, _p]),
+    "oracle_rope_kv": (None, [_p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _i, _p, _p, _p]),
+    "oracle_attention": (None, [_p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p]),
+    "cpu_lm_len": (_i, [_i]),
+    "cpu_pack_lm": (None, [_p, _i64, _i, _p]),
+    "cpu_pack_blob": (None, [_p, _i, _i, _p]),
+    "cpu_blob_lm_elems": (_i64, [_i, _i]),
+    "cpu_linear": (None, [_p, _p, _i64, _i, _i, _i, _p, _f, _p, _i64, _p, _p]),
+    "cpu_expert_ffn": (None, [_p, _i, _i, _p, _p, _i, _p, _p]),
+    "cpu_attn_block": (None, [_p, _i, _i, _i, _p, _p, _p, _f, _i, _i, _i, _p, _p, _i, _p, _p, _p, _i, _f]),
+    "cpu_upcycle": (None, [_p, _p, _i64, _f]),
+    "cpu_accum": (None, [_p, _p, _i64]),
+    "cpu_div_bf16": (None, [_p, _i64, _f, _p]),
+    "cpu_scale_bf16": (None, [_p, _i64, _f]),
     "oracle_xc_encode": (_u64, [_p, _i, _p, _p, _u64, _p]),
     "oracle_xc_decode": (_i, [_p, _p]),
 }
 
 
 def build() -> Path:
-    srcs = [HERE / "spmoe_oracle.c", HERE / "xc_oracle.c", HERE.parent / "include" / "spmoe.h"]
+    srcs = [HERE / n for n in ("spmoe_oracle.c", "forward_oracle.c", "cpu_path.c", "pool.c", "pool.h", "xc_oracle.c",
+                               "Makefile")] + [HERE.parent / "include" / "spmoe.h"]
     if not LIB.exists() or any(LIB.stat().st_mtime < s.stat().st_mtime for s in srcs):
         subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
     return LIB
@@ -165,6 +182,107 @@ def fill_normal_bf16(n, seed, offset=0, std=0.02):
     out = np.empty((n,), np.uint16)
     lib().oracle_fill_normal_bf16(_ptr(out), n, seed & 0xFFFFFFFFFFFFFFFF, offset & 0xFFFFFFFFFFFFFFFF, float(std))
     return out
+
+
+# ------------------------------------------------- layer block (forward_oracle.c)
+def rms_norm(x, w, eps):
+    x = _c(x, np.uint16)
+    H = x.shape[-1]
+    out = np.empty_like(x)
+    lib().oracle_rms_norm(_ptr(x), _ptr(_c(w, np.uint16)), x.size // H, H, float(eps), _ptr(out))
+    return out
+
+
+def linear(w, x, norm_w=None, eps=0.0, f32=False, residual=None):
+    """Scalar K9: x [T, K] bf16 bits, w [N, K] -> fp32 [T, N] (f32) or bf16
+    bits (bf16(residual + bf16(y)) with ``residual``)."""
+    w = _c(w, np.uint16)
+    x = _c(x, np.uint16)
+    N, K = w.shape
+    T = x.size // K
+    nw = None if norm_w is None else _c(norm_w, np.uint16)
+    if f32:
+        y = np.empty((T, N), np.float32)
+        lib().oracle_linear(_ptr(w), _ptr(x), K, T, K, N, _ptr(nw), float(eps), _ptr(y), N, None, None)
+        return y
+    out = np.empty((T, N), np.uint16)
+    r = None if residual is None else _c(residual, np.uint16).reshape(T, N)
+    lib().oracle_linear(_ptr(w), _ptr(x), K, T, K, N, _ptr(nw), float(eps), None, 0, _ptr(out), _ptr(r))
+    return out
+
+
+def rope_kv(qkv, cos, sin, start, nh, nkv, hd, k_cache, v_cache):
+    """qkv [B, T, (nh+2nkv)hd] bits; caches [B, nkv, S, hd] updated in place;
+    returns q [B, nh, T, hd]."""
+    qkv = _c(qkv, np.uint16)
+    B, T = qkv.shape[0], qkv.shape[1]
+    S = k_cache.shape[2]
+    q = np.zeros((B, nh, T, hd), np.uint16)
+    st = _c(start, np.int64)
+    lib().oracle_rope_kv(_ptr(qkv), _ptr(_c(cos, np.float32)), _ptr(_c(sin, np.float32)), _ptr(st), B, T, nh, nkv,
+                         hd, S, cos.shape[0], _ptr(q), _ptr(k_cache), _ptr(v_cache))
+    return q
+
+
+def attention(q, k_cache, v_cache, start, scale):
+    q = _c(q, np.uint16)
+    B, nh, T, hd = q.shape
+    nkv, S = k_cache.shape[1], k_cache.shape[2]
+    out = np.empty((B, T, nh * hd), np.uint16)
+    lib().oracle_attention(_ptr(q), _ptr(_c(k_cache, np.uint16)), _ptr(_c(v_cache, np.uint16)),
+                           _ptr(_c(start, np.int64)), B, T, nh, nkv, hd, S, float(scale), _ptr(out))
+    return out
+
+
+# ------------------------------------------------ lane-major CPU path (cpu_path.c)
+def lm_len(K: int) -> int:
+    return int(lib().cpu_lm_len(int(K)))
+
+
+def pack_lm(w):
+    """raw [N, K] bf16 bits -> lane-major [N, Kp]."""
+    w = _c(w, np.uint16)
+    N, K = w.shape
+    out = np.empty((N, lm_len(K)), np.uint16)
+    lib().cpu_pack_lm(_ptr(w), N, K, _ptr(out))
+    return out
+
+
+def pack_blob(blob, H, F):
+    blob = _c(blob, np.uint16).reshape(-1)
+    out = np.empty((int(lib().cpu_blob_lm_elems(H, F)),), np.uint16)
+    lib().cpu_pack_blob(_ptr(blob), H, F, _ptr(out))
+    return out
+
+
+def lm_linear(w_lm, K, x, norm_w=None, eps=0.0, f32=False, residual=None):
+    w_lm = _c(w_lm, np.uint16)
+    N = w_lm.shape[0]
+    x = _c(x, np.uint16)
+    T = x.size // K
+    nw = None if norm_w is None else _c(norm_w, np.uint16)
+    if f32:
+        y = np.empty((T, N), np.float32)
+        lib().cpu_linear(_ptr(w_lm), _ptr(x), K, T, K, N, _ptr(nw), float(eps), _ptr(y), N, None, None)
+        return y
+    out = np.empty((T, N), np.uint16)
+    r = None if residual is None else _c(residual, np.uint16).reshape(T, N)
+    lib().cpu_linear(_ptr(w_lm), _ptr(x), K, T, K, N, _ptr(nw), float(eps), None, 0, _ptr(out), _ptr(r))
+    return out
+
+
+def lm_expert_ffn(blob_lm, H, F, x, perm=None, n=None):
+    """One expert (LM blob) on rows x[perm[q]] -> (h [n, F] bits, y [n, H] f32)."""
+    x = _c(x, np.uint16)
+    if perm is not None:
+        perm = _c(perm, np.int32)
+        n = perm.size if n is None else n
+    elif n is None:
+        n = x.shape[0]
+    h = np.empty((max(n, 1), F), np.uint16)
+    y = np.empty((max(n, 1), H), np.float32)
+    lib().cpu_expert_ffn(_ptr(_c(blob_lm, np.uint16)), H, F, _ptr(x), _ptr(perm), n, _ptr(h), _ptr(y))
+    return h[:n], y[:n]
 
 
 # ---------------------------------------------------------------- bf16 utils

@@ -51,7 +51,8 @@ SIGNATURES: dict[str, tuple] = {
     "spmoe_argmax_rows": (_i, [_p, _i64, _i, _i, _p, _p]),
     "spmoe_h2d_batch": (_i, [_p, _p, _p, _i, _p]),
     "spmoe_rms_norm": (_i, [_p, _p, _i, _i, _f, _p, _p]),
-    "spmoe_rope_kv": (_i, [_p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p]),
+    "spmoe_rope_kv": (_i, [_p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p]),
+    "spmoe_linear": (_i, [_p, _p, _i64, _i, _i, _i, _p, _f, _p, _i64, _p, _p, _p]),
     "spmoe_attention": (_i, [_p, _p, _p, _p, _i, _i, _i, _i, _i, _i, _f, _p, _p]),
     "spmoe_fill_normal_bf16": (_i, [_p, _i64, _u64, _u64, _f, _p]),
     "spmoe_rt_create": (_p, [_i, _i, _i, _p, _p, _p, _sz, _p, _i]),

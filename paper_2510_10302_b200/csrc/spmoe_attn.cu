@@ -1,23 +1,22 @@
 // spmoe_attn.cu — the target/draft layer block around the MoE (SURVEY.md
 // §8(f) rows 1-2: draft forward and the verify pass outside the MoE) as
-// three fused sm_100a kernels instead of ~30 small framework kernels per
-// layer:
+// fused sm_100a kernels instead of ~30 small framework kernels per layer:
 //
-//   rms_norm_kernel   y = bf16(x * rsqrt(mean(x^2) + eps) * w), one warp per
-//                     row, fp32 (HF Mixtral/Qwen/DeepSeek RMSNorm)
+//   rms_norm_kernel   y = bf16((x * r) * w), r = 1/sqrt(mean(x^2) + eps), one
+//                     warp per row (HF Mixtral/Qwen/DeepSeek RMSNorm)
 //   rope_kv_kernel    split the fused qkv projection, rotate q and k
-//                     (rotate-half RoPE, fp32 math, bf16 out), write q in
-//                     [B, nh, T, hd] and append k, v to the layer's KV cache
-//                     [B, nkv, S, hd] at each sequence's own positions
+//                     (rotate-half RoPE), write q in [B, nh, T, hd] and append
+//                     k, v to the layer's KV cache [B, nkv, S, hd] at each
+//                     sequence's own positions
 //   attn_kernel       causal GQA attention of T new queries over the cached
-//                     keys 0..pos, online softmax in fp32, output
+//                     keys 0..pos, two-pass softmax in fp32, output
 //                     [B, T, nh*hd] bf16 ready for the W_o projection
 //
-// These are latency-bound (a few KB to a few MB per launch); the projections
-// around them are cuBLAS GEMMs (weight-bandwidth bound).  Numerics follow
-// the PyTorch reference within bf16 rounding of the attention output;
-// routing parity is unaffected because the oracle checks each MoE layer on
-// the GPU's own layer input.
+// Every operation follows the determinism contract of include/spmoe.h, so
+// the CPU oracle (oracle/forward_oracle.c) reproduces each output bit for
+// bit: fixed-order reductions, IEEE mul/add/div/sqrt written out with
+// __f*_rn (never contracted), det_exp instead of the SFU exp.  The
+// projections around them are K9 linear launches (spmoe_kernels.cu).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -28,14 +27,9 @@ using namespace spmoe;
 
 namespace {
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 // ------------------------------------------------------------------ RMSNorm
-// One warp per row; H % 8 == 0; 16-byte loads.
+// One warp per row; H % 8 == 0.  ss = dot_fixed(x, x) (lane-strided 8-value
+// chunks, butterfly), r = 1 / sqrt(ss / H + eps), y = bf16((x * r) * w).
 __global__ void __launch_bounds__(256) rms_norm_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w,
                                                        int rows, int H, float eps, uint16_t* __restrict__ out) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -44,17 +38,14 @@ __global__ void __launch_bounds__(256) rms_norm_kernel(const uint16_t* __restric
   const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)warp * H);
   const int n8 = H / 8;
   float ss = 0.0f;
-  for (int i = lane; i < n8; i += 32) {
-    const uint4 v = xr[i];
-    const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+  for (int c = lane; c < n8; c += 32) {
+    float a[8];
+    unpack8(xr[c], a);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float a = bf16_lo(u[j]), b = bf16_hi(u[j]);
-      ss += a * a + b * b;
-    }
+    for (int v = 0; v < 8; ++v) ss = fmaf(a[v], a[v], ss);  // bf16 squares are exact
   }
-  ss = warp_sum(ss);
-  const float r = rsqrtf(ss / (float)H + eps);
+  ss = warp_sum_fixed(ss);
+  const float r = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)H), eps)));
   const uint4* wr = reinterpret_cast<const uint4*>(w);
   uint4* orow = reinterpret_cast<uint4*>(out + (int64_t)warp * H);
   for (int i = lane; i < n8; i += 32) {
@@ -63,9 +54,8 @@ __global__ void __launch_bounds__(256) rms_norm_kernel(const uint16_t* __restric
     uint32_t o[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      // fp32 (x * r) * w, one rounding to bf16 (as the PyTorch reference)
-      const float lo = (bf16_lo(u[j]) * r) * bf16_lo(gw[j]);
-      const float hi = (bf16_hi(u[j]) * r) * bf16_hi(gw[j]);
+      const float lo = __fmul_rn(__fmul_rn(bf16_lo(u[j]), r), bf16_lo(gw[j]));
+      const float hi = __fmul_rn(__fmul_rn(bf16_hi(u[j]), r), bf16_hi(gw[j]));
       o[j] = (uint32_t)f32_to_bf16(lo) | ((uint32_t)f32_to_bf16(hi) << 16);
     }
     orow[i] = make_uint4(o[0], o[1], o[2], o[3]);
@@ -74,14 +64,20 @@ __global__ void __launch_bounds__(256) rms_norm_kernel(const uint16_t* __restric
 
 // ------------------------------------------------------------- RoPE + KV
 // One CTA per (token row); threads walk the nh + 2 nkv heads' dims.
+// y[d] = bf16(x[d] * cos[pos][d] + rot[d] * sin[pos][d]), rot = [-x2, x1],
+// the two products and the sum each IEEE-rounded.  Positions at or beyond
+// the cache (S) or the RoPE table (max_pos) write nothing (the host checks
+// lengths before launching; this keeps a bad position from corrupting
+// memory).
 __global__ void __launch_bounds__(256) rope_kv_kernel(const uint16_t* __restrict__ qkv, const float* __restrict__ cos_t,
                                                       const float* __restrict__ sin_t, const int64_t* __restrict__ start,
-                                                      int T, int nh, int nkv, int hd, int S,
+                                                      int T, int nh, int nkv, int hd, int S, int max_pos,
                                                       uint16_t* __restrict__ q_out, uint16_t* __restrict__ kc,
                                                       uint16_t* __restrict__ vc) {
   const int row = blockIdx.x;  // b * T + t
   const int b = row / T, t = row % T;
   const int64_t pos = start[b] + t;
+  if (pos < 0 || pos >= S || pos >= max_pos) return;
   const uint16_t* src = qkv + (int64_t)row * (nh + 2 * nkv) * hd;
   const float* cs = cos_t + pos * hd;
   const float* sn = sin_t + pos * hd;
@@ -91,11 +87,10 @@ __global__ void __launch_bounds__(256) rope_kv_kernel(const uint16_t* __restrict
     const int head = i / hd, d = i % hd;
     const float x = bf16_to_f32(src[i]);
     if (head < nh + nkv) {
-      // rotate_half: [-x2, x1]
       const int pd = d < half ? d + half : d - half;
       const float xp = bf16_to_f32(src[head * hd + pd]);
       const float rot = d < half ? -xp : xp;
-      const uint16_t y = f32_to_bf16(x * cs[d] + rot * sn[d]);
+      const uint16_t y = f32_to_bf16(__fadd_rn(__fmul_rn(x, cs[d]), __fmul_rn(rot, sn[d])));
       if (head < nh) {
         q_out[(((int64_t)b * nh + head) * T + t) * hd + d] = y;
       } else {
@@ -110,15 +105,33 @@ __global__ void __launch_bounds__(256) rope_kv_kernel(const uint16_t* __restrict
 }
 
 // ------------------------------------------------------------ attention
-// One CTA (NW warps) per (b, head, chunk of QC queries).  Each warp owns a
-// strided subset of the keys and keeps, per query, an online-softmax state
-// (max, sum, acc[hd/32 per lane]); the warps merge through shared memory.
-template <int HD, int QC, int NW>
-__global__ void __launch_bounds__(32 * NW) attn_kernel(const uint16_t* __restrict__ q, const uint16_t* __restrict__ kc,
-                                                   const uint16_t* __restrict__ vc, const int64_t* __restrict__ start,
-                                                   int T, int nh, int nkv, int S, float scale,
-                                                   uint16_t* __restrict__ out) {
+// One CTA (NW = 8 warps) per (b, head, chunk of QC = 8 queries).  The fixed
+// order, restated by oracle_attention:
+//   qs[d]  = q[d] * scale
+//   s_j    = sum_d qs[d] * k_j[d]: lane l sums its PL = hd/32 consecutive
+//            dims in order, then the xor butterfly 16,8,4,2,1
+//   m      = max_j s_j over the causal keys j <= pos
+//   p_j    = det_exp(s_j - m)
+//   stream w (= warp w) sums its keys j = w, w+8, w+16, ... ascending:
+//            l_w = sum p_j,  acc_w[d] = sum p_j * v_j[d]
+//   l = l_0 + l_1 + ... + l_7 (in w order), acc[d] likewise,
+//   out[d] = bf16(acc[d] / l).
+// Pass 1 keeps the scores of the chunk in shared memory ([QC][S] fp32).
+constexpr int kAttnQC = 8;
+constexpr int kAttnNW = 8;
+
+template <int HD>
+__global__ void __launch_bounds__(32 * kAttnNW) attn_kernel(const uint16_t* __restrict__ q,
+                                                         const uint16_t* __restrict__ kc,
+                                                         const uint16_t* __restrict__ vc,
+                                                         const int64_t* __restrict__ start, int T, int nh, int nkv,
+                                                         int S, float scale, uint16_t* __restrict__ out) {
+  constexpr int QC = kAttnQC, NW = kAttnNW;
   constexpr int PL = HD / 32;  // dims per lane
+  extern __shared__ __align__(16) float sm[];
+  float* s_p = sm;                        // [QC][S] scores, then probabilities
+  float* s_acc = s_p + (int64_t)QC * S;   // [NW][QC][HD]
+  float* s_l = s_acc + NW * QC * HD;      // [NW][QC]
   const int nqc = (T + QC - 1) / QC;
   const int qc = blockIdx.x % nqc;
   const int h = (blockIdx.x / nqc) % nh;
@@ -127,76 +140,89 @@ __global__ void __launch_bounds__(32 * NW) attn_kernel(const uint16_t* __restric
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = qc * QC;
   const int nq = min(QC, T - t0);
-  const int64_t p0 = start[b];
-  const int klen = (int)(p0 + t0 + nq);  // keys 0 .. last query's position
+  const int64_t p0 = start[b] + t0;  // position of the chunk's first query
+  const int klen = (int)min((int64_t)S, p0 + nq);  // keys 0 .. last query's position
   float qv[QC][PL];
 #pragma unroll
   for (int i = 0; i < QC; ++i)
 #pragma unroll
     for (int j = 0; j < PL; ++j)
-      qv[i][j] = i < nq ? bf16_to_f32(q[(((int64_t)b * nh + h) * T + t0 + i) * HD + lane * PL + j]) * scale : 0.0f;
-  float m[QC], l[QC], acc[QC][PL];
+      qv[i][j] = i < nq ? __fmul_rn(bf16_to_f32(q[(((int64_t)b * nh + h) * T + t0 + i) * HD + lane * PL + j]), scale)
+                        : 0.0f;
+  const uint16_t* kb = kc + ((int64_t)b * nkv + kh) * S * HD;
+  const uint16_t* vb = vc + ((int64_t)b * nkv + kh) * S * HD;
+  // pass 1: scores
+  for (int key = warp; key < klen; key += NW) {
+    float kv[PL];
+#pragma unroll
+    for (int j = 0; j < PL; ++j) kv[j] = bf16_to_f32(kb[(int64_t)key * HD + lane * PL + j]);
+#pragma unroll
+    for (int i = 0; i < QC; ++i) {
+      if (i >= nq || key > p0 + i) continue;  // causal (warp-uniform)
+      float s = 0.0f;
+#pragma unroll
+      for (int j = 0; j < PL; ++j) s = __fadd_rn(s, __fmul_rn(qv[i][j], kv[j]));
+      s = warp_sum_fixed(s);
+      if (lane == 0) s_p[i * S + key] = s;
+    }
+  }
+  __syncthreads();
+  // max and probabilities: warp i owns query i
+  if (warp < nq) {
+    const int kl = (int)min((int64_t)S, p0 + warp + 1);
+    float* row = s_p + warp * S;
+    float m = -INFINITY;
+    for (int j = lane; j < kl; j += 32) m = fmaxf(m, row[j]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(SPMOE_FULL_MASK, m, o));
+    for (int j = lane; j < kl; j += 32) row[j] = det_exp(__fsub_rn(row[j], m));
+  }
+  __syncthreads();
+  // pass 2: stream w = warp w, keys ascending
+  float l[QC], acc[QC][PL];
 #pragma unroll
   for (int i = 0; i < QC; ++i) {
-    m[i] = -INFINITY;
     l[i] = 0.0f;
 #pragma unroll
     for (int j = 0; j < PL; ++j) acc[i][j] = 0.0f;
   }
-  const uint16_t* kb = kc + ((int64_t)b * nkv + kh) * S * HD;
-  const uint16_t* vb = vc + ((int64_t)b * nkv + kh) * S * HD;
   for (int key = warp; key < klen; key += NW) {
-    float kv[PL], vv[PL];
+    float vv[PL];
 #pragma unroll
-    for (int j = 0; j < PL; ++j) {
-      kv[j] = bf16_to_f32(kb[(int64_t)key * HD + lane * PL + j]);
-      vv[j] = bf16_to_f32(vb[(int64_t)key * HD + lane * PL + j]);
-    }
+    for (int j = 0; j < PL; ++j) vv[j] = bf16_to_f32(vb[(int64_t)key * HD + lane * PL + j]);
 #pragma unroll
     for (int i = 0; i < QC; ++i) {
-      if (i >= nq || key > p0 + t0 + i) continue;  // causal (warp-uniform)
-      float s = 0.0f;
+      if (i >= nq || key > p0 + i) continue;
+      const float pj = s_p[i * S + key];
+      l[i] = __fadd_rn(l[i], pj);
 #pragma unroll
-      for (int j = 0; j < PL; ++j) s += qv[i][j] * kv[j];
-      s = warp_sum(s);
-      const float mn = fmaxf(m[i], s);
-      const float c = __expf(m[i] - mn), pexp = __expf(s - mn);
-      l[i] = l[i] * c + pexp;
-#pragma unroll
-      for (int j = 0; j < PL; ++j) acc[i][j] = acc[i][j] * c + pexp * vv[j];
-      m[i] = mn;
+      for (int j = 0; j < PL; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(pj, vv[j]));
     }
   }
-  // merge the 4 warps' states
-  __shared__ float sm_m[NW][QC], sm_l[NW][QC];
-  __shared__ float sm_acc[NW][QC][HD];
-  if (lane == 0)
 #pragma unroll
-    for (int i = 0; i < QC; ++i) {
-      sm_m[warp][i] = m[i];
-      sm_l[warp][i] = l[i];
-    }
+  for (int i = 0; i < QC; ++i) {
 #pragma unroll
-  for (int i = 0; i < QC; ++i)
-#pragma unroll
-    for (int j = 0; j < PL; ++j) sm_acc[warp][i][lane * PL + j] = acc[i][j];
+    for (int j = 0; j < PL; ++j) s_acc[(warp * QC + i) * HD + lane * PL + j] = acc[i][j];
+    if (lane == 0) s_l[warp * QC + i] = l[i];
+  }
   __syncthreads();
   for (int idx = threadIdx.x; idx < nq * HD; idx += blockDim.x) {
     const int i = idx / HD, d = idx % HD;
-    float mx = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) mx = fmaxf(mx, sm_m[w][i]);
     float den = 0.0f, num = 0.0f;
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
-      if (sm_m[w][i] == -INFINITY) continue;
-      const float c = __expf(sm_m[w][i] - mx);
-      den += sm_l[w][i] * c;
-      num += sm_acc[w][i][d] * c;
+      den = __fadd_rn(den, s_l[w * QC + i]);
+      num = __fadd_rn(num, s_acc[(w * QC + i) * HD + d]);
     }
-    out[(((int64_t)b * T + t0 + i) * nh + h) * HD + d] = f32_to_bf16(num / den);
+    out[(((int64_t)b * T + t0 + i) * nh + h) * HD + d] = f32_to_bf16(__fdiv_rn(num, den));
   }
 }
+
+size_t attn_smem(int S, int hd) {
+  return ((size_t)kAttnQC * S + (size_t)kAttnNW * kAttnQC * hd + kAttnNW * kAttnQC) * sizeof(float);
+}
+
+constexpr size_t kAttnSmemCap = 200 * 1024;
 
 }  // namespace
 
@@ -211,29 +237,38 @@ int spmoe_rms_norm(const uint16_t* x, const uint16_t* w, int rows, int H, float 
 }
 
 int spmoe_rope_kv(const uint16_t* qkv, const float* cos_t, const float* sin_t, const int64_t* start, int B, int T,
-                  int nh, int nkv, int hd, int S, uint16_t* q_out, uint16_t* k_cache, uint16_t* v_cache,
-                  void* stream) {
-  if (B < 0 || T < 0 || nh < 1 || nkv < 1 || nh % nkv || hd % 2 || !qkv || !q_out || !k_cache || !v_cache)
+                  int nh, int nkv, int hd, int S, int max_pos, uint16_t* q_out, uint16_t* k_cache,
+                  uint16_t* v_cache, void* stream) {
+  if (B < 0 || T < 0 || nh < 1 || nkv < 1 || nh % nkv || hd % 2 || S < 1 || max_pos < 1 || !qkv || !q_out ||
+      !k_cache || !v_cache || !cos_t || !sin_t || !start)
     return (int)cudaErrorInvalidValue;
   if (B * T == 0) return 0;
-  rope_kv_kernel<<<B * T, 256, 0, (cudaStream_t)stream>>>(qkv, cos_t, sin_t, start, T, nh, nkv, hd, S, q_out,
-                                                          k_cache, v_cache);
+  rope_kv_kernel<<<B * T, 256, 0, (cudaStream_t)stream>>>(qkv, cos_t, sin_t, start, T, nh, nkv, hd, S, max_pos,
+                                                          q_out, k_cache, v_cache);
   return (int)cudaGetLastError();
 }
 
 int spmoe_attention(const uint16_t* q, const uint16_t* k_cache, const uint16_t* v_cache, const int64_t* start,
                     int B, int T, int nh, int nkv, int hd, int S, float scale, uint16_t* out, void* stream) {
-  if (B < 0 || T < 0 || nh < 1 || nkv < 1 || nh % nkv || (hd != 64 && hd != 128) || !q || !out)
+  if (B < 0 || T < 0 || nh < 1 || nkv < 1 || nh % nkv || (hd != 64 && hd != 128) || S < 1 || !q || !out ||
+      !k_cache || !v_cache || !start)
     return (int)cudaErrorInvalidValue;
   if (B * T == 0) return 0;
-  constexpr int QC = 8;  // T = N + 1 <= 9 verify tokens: one or two chunks
-  const int nqc = (T + QC - 1) / QC;
+  const size_t smem = attn_smem(S, hd);
+  if (smem > kAttnSmemCap) return (int)cudaErrorInvalidValue;
+  const int nqc = (T + kAttnQC - 1) / kAttnQC;
   const dim3 grid(B * nh * nqc);
   cudaStream_t st = (cudaStream_t)stream;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmemCap);
+    cudaFuncSetAttribute(attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmemCap);
+    configured = true;
+  }
   if (hd == 128)
-    attn_kernel<128, QC, 8><<<grid, 256, 0, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale, out);
+    attn_kernel<128><<<grid, 32 * kAttnNW, smem, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale, out);
   else
-    attn_kernel<64, QC, 8><<<grid, 256, 0, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale, out);
+    attn_kernel<64><<<grid, 32 * kAttnNW, smem, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale, out);
   return (int)cudaGetLastError();
 }
 

@@ -328,6 +328,132 @@ __global__ void __launch_bounds__(kFfnThreads, 1) ffn_kernel(const FfnParams p) 
 
 constexpr int kActSmemCap = 200 * 1024;
 
+// ---------------------------------------------------------------------------
+// K9 linear: y[t][n] = dot_fixed(W[n,:], x[t,:]) for the projections around
+// the MoE (fused qkv, W_o, lm_head) -- the same weight-streaming warp-per-row
+// scheme and fixed reduction order as K3's down phase, so the whole forward
+// (not just the MoE) is reproducible on the CPU oracle bit for bit.  Rows are
+// dealt in 16-row tiles, one contiguous tile range per CTA; the T activation
+// rows are staged in shared memory TT at a time (prefill re-streams the
+// weights once per TT-token group).
+//
+// Optional fused pieces, each with the arithmetic of its standalone kernel:
+//   norm_w != null : stage RMSNorm(x) (rms_norm_kernel's exact arithmetic)
+//                    instead of x -- norm -> projection in one launch;
+//   resid  != null : out = bf16(resid + bf16(y)) (the residual add of the
+//                    torch graph `x = x + proj(o)`), else out = bf16(y);
+//   y_f32  != null : raw fp32 dot products (lm_head logits).
+// ---------------------------------------------------------------------------
+struct LinParams {
+  const uint16_t* w;     // [N, K]
+  const uint16_t* x;     // [T, K] (row stride ldx elements)
+  const uint16_t* norm_w;
+  float eps;
+  int64_t ldx;
+  int T, K, N;
+  float* y_f32;          // [T, ldy]
+  int64_t ldy;
+  uint16_t* y_bf16;      // [T, N]
+  const uint16_t* resid; // [T, N] (may alias y_bf16)
+};
+
+// Fixed-order RMSNorm scale of one row (one warp): ss = dot_fixed(x, x),
+// r = 1 / sqrt(ss / H + eps) with IEEE division and square root.
+__device__ __forceinline__ float rms_scale_row(const uint4* xr, int nchunks, int H, float eps, int lane) {
+  float acc = 0.0f;
+  for (int c = lane; c < nchunks; c += 32) {
+    float a[8];
+    unpack8(__ldg(xr + c), a);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) acc = fmaf(a[v], a[v], acc);  // exact squares
+  }
+  acc = warp_sum_fixed(acc);
+  const float mean = __fdiv_rn(acc, (float)H);
+  return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(mean, eps)));
+}
+
+// y = bf16((x * r) * w), two IEEE products.
+__device__ __forceinline__ uint32_t rms_apply2(uint32_t xw, uint32_t gw, float r) {
+  const float lo = __fmul_rn(__fmul_rn(bf16_lo(xw), r), bf16_lo(gw));
+  const float hi = __fmul_rn(__fmul_rn(bf16_hi(xw), r), bf16_hi(gw));
+  return (uint32_t)f32_to_bf16(lo) | ((uint32_t)f32_to_bf16(hi) << 16);
+}
+
+template <int TT>
+__global__ void __launch_bounds__(kFfnThreads, 1) linear_kernel(const LinParams p) {
+  extern __shared__ __align__(16) uint4 s_act[];
+  __shared__ float s_r[TT];
+  constexpr int kRowsPerTile = kFfnThreads / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nchunks = p.K >> 3;
+  const int tiles = (p.N + kRowsPerTile - 1) / kRowsPerTile;
+  const int t_begin = (int)((int64_t)tiles * blockIdx.x / gridDim.x);
+  const int t_end = (int)((int64_t)tiles * (blockIdx.x + 1) / gridDim.x);
+  if (t_begin >= t_end) return;
+  for (int t0 = 0; t0 < p.T; t0 += TT) {
+    const int nt = min(TT, p.T - t0);
+    __syncthreads();  // previous group's readers are done
+    if (p.norm_w != nullptr) {
+      for (int t = warp; t < nt; t += kFfnThreads / 32)
+        s_r[t] = rms_scale_row(reinterpret_cast<const uint4*>(p.x + (int64_t)(t0 + t) * p.ldx), nchunks, p.K,
+                               p.eps, lane);
+      __syncthreads();
+    }
+    for (int q = threadIdx.x; q < nt * nchunks; q += kFfnThreads) {
+      const int t = q / nchunks, c = q - t * nchunks;
+      uint4 v = __ldg(reinterpret_cast<const uint4*>(p.x + (int64_t)(t0 + t) * p.ldx) + c);
+      if (p.norm_w != nullptr) {
+        const uint4 g = __ldg(reinterpret_cast<const uint4*>(p.norm_w) + c);
+        const float r = s_r[t];
+        v = make_uint4(rms_apply2(v.x, g.x, r), rms_apply2(v.y, g.y, r), rms_apply2(v.z, g.z, r),
+                       rms_apply2(v.w, g.w, r));
+      }
+      s_act[t * nchunks + c] = v;
+    }
+    __syncthreads();
+    for (int tile = t_begin; tile < t_end; ++tile) {
+      const int row = tile * kRowsPerTile + warp;
+      if (row >= p.N) continue;
+      const uint4* wr[1] = {reinterpret_cast<const uint4*>(p.w + (int64_t)row * p.K)};
+      float acc[1][TT];
+#pragma unroll
+      for (int t = 0; t < TT; ++t) acc[0][t] = 0.0f;
+      stream_rows<TT, 1, 16>(wr, s_act, nchunks, nt, nchunks, lane, acc);
+#pragma unroll
+      for (int t = 0; t < TT; ++t) {
+        if (t < nt) {
+          const float s = warp_sum_fixed(acc[0][t]);
+          if (lane == t) {
+            const int64_t tt = t0 + t;
+            if (p.y_f32 != nullptr) p.y_f32[tt * p.ldy + row] = s;
+            if (p.y_bf16 != nullptr) {
+              uint16_t o = f32_to_bf16(s);
+              if (p.resid != nullptr)
+                o = f32_to_bf16(__fadd_rn(bf16_to_f32(p.resid[tt * p.N + row]), bf16_to_f32(o)));
+              p.y_bf16[tt * p.N + row] = o;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int TT>
+int launch_linear(const LinParams& p, cudaStream_t s) {
+  const size_t smem = (size_t)TT * p.K * 2;
+  if (smem > (size_t)kActSmemCap) return (int)cudaErrorInvalidValue;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(linear_kernel<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kActSmemCap);
+    configured = true;
+  }
+  const int tiles = (p.N + 15) / 16;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  linear_kernel<TT><<<grid, kFfnThreads, smem, s>>>(p);
+  return launch_status();
+}
+
 // Register tile: the smallest of 1/2/4/8 covering the hint that also fits
 // the activation stage (TT x K bf16) in shared memory.
 int pick_tile(int hint, int K) {
@@ -604,6 +730,29 @@ int spmoe_expert_ffn(const uint16_t* pool, int64_t slot_elems, const int32_t* sl
                              expert_offsets, h_scratch, y, max_tokens_per_expert, stream);
   if (tm.end) cudaEventRecord(tm.end, (cudaStream_t)stream);
   return st;
+}
+
+int spmoe_linear(const uint16_t* w, const uint16_t* x, int64_t ldx, int T, int K, int N,
+                 const uint16_t* norm_w, float eps, float* y_f32, int64_t ldy, uint16_t* y_bf16,
+                 const uint16_t* resid, void* stream) {
+  if (T < 0 || K <= 0 || (K & 7) || N <= 0 || ldx < K || (ldx & 7)) return (int)cudaErrorInvalidValue;
+  if (T == 0) return 0;
+  if (!w || !x || (!y_f32 && !y_bf16) || (y_f32 && ldy < N) || (resid && !y_bf16))
+    return (int)cudaErrorInvalidValue;
+  LinParams p{};
+  p.w = w; p.x = x; p.norm_w = norm_w; p.eps = eps; p.ldx = ldx;
+  p.T = T; p.K = K; p.N = N;
+  p.y_f32 = y_f32; p.ldy = ldy; p.y_bf16 = y_bf16; p.resid = resid;
+  int tt = T <= 1 ? 1 : T <= 2 ? 2 : T <= 4 ? 4 : T <= 8 ? 8 : 16;
+  while (tt > 1 && (size_t)tt * K * 2 > (size_t)kActSmemCap) tt >>= 1;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (tt) {
+    case 1: return launch_linear<1>(p, s);
+    case 2: return launch_linear<2>(p, s);
+    case 4: return launch_linear<4>(p, s);
+    case 8: return launch_linear<8>(p, s);
+    default: return launch_linear<16>(p, s);
+  }
 }
 
 int spmoe_gather_rows(const void* src, const int32_t* idx, int n, int div, int64_t row_bytes,

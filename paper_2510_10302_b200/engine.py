@@ -46,7 +46,7 @@ from . import kernels as K
 from .cache import ExpertId, NativeExpertCache
 from .config import HardwareSpec, Policy, PolicySpec, ProfiledTimings, ValidationError, cache_capacity_slots
 from .cutoff import cutoff_input_from_specs, solve_cutoff
-from .model import ArchSpec, HostExpertPool, KVCache, attention, build_weights, model_spec_for, rms_norm
+from .model import ArchSpec, HostExpertPool, KVCache, attention_block, build_weights, lm_logits, model_spec_for, rms_norm
 from .predictor import DraftGuidedPredictor, HistoryCounter, top_k_indices
 from .report import ComputeSlot, IterationRecord, SimReport, TransferKind, TransferRecord
 
@@ -486,16 +486,21 @@ class SpecMoEEngine:
         T, H = xn.shape
         k, E = a.top_k, a.num_experts
         w, idx, sg = routed if routed is not None else self._route(l, xn, s)
-        if self.policy.policy is Policy.GATING_NEXT_LAYER and l + 1 < a.num_layers:
-            self._gating_predict(l + 1, xn)
+        gating = self.policy.policy is Policy.GATING_NEXT_LAYER and l + 1 < a.num_layers
+        if gating:
+            # K1 for layer l+1 runs on the GPU now; its task is pushed after
+            # layer l's lookups and demand load (simcore.py:360-418 order)
+            g_ring = self._gating_launch(l + 1, xn)
         self._lib.spmoe_event_synchronize(self._route_ev)
         ids = self.route_ring.view[0, : T * k].copy()
         counts = np.bincount(ids, minlength=E)
         # copies first: the host-side bookkeeping below overlaps the link
         plan = self._cache_issue(l, counts) if self.ep is None else None
-        self.history.record_many(l, ids)
         if self.record:
             self.decisions.append(("verify", l, [int(v) for v in ids]))
+        if gating:
+            self._gating_push(l + 1, g_ring)
+        self.history.record_many(l, ids)
         if self.record_routing:
             self._iter_logits.append(s.logits[:T].clone())
         if self.ep is not None:
@@ -608,17 +613,25 @@ class SpecMoEEngine:
         y_back = self.ep.combine(y_recv)
         return self._shared_and_combine(l, xn, resid, s, w, idx, sg, y_back, inv, slots)
 
-    def _gating_predict(self, layer: int, xn: torch.Tensor) -> None:
-        """gating_next_layer baseline: predict layer+1 from this layer's MLP
-        input, blocking prefetch (``vanilla_prefetch_step``, prefetch.py:241-273)."""
+    def _gating_launch(self, layer: int, xn: torch.Tensor) -> tuple:
+        """gating_next_layer baseline, GPU half: K1 predicts layer+1 from this
+        layer's MLP input (one token per sequence: the verify position, as
+        simcore.py:407 uses ``position`` -- the first of each sequence's
+        verify tokens)."""
         pk = self.policy.prefetch_k
         B = self.batch
-        # one token per sequence (the verify position, as simcore.py:407 uses
-        # ``position``): the first of each sequence's verify tokens
         x_pos = xn.view(B, -1, xn.shape[-1])[:, 0, :].contiguous()
-        i, hptr, ev = self.predictor.predict(
+        return self.predictor.predict(
             x_pos, self.weights.layers[layer].router, pk, True, self.scratch.pw[:B, :pk], self.scratch.pidx[:B, :pk]
         )
+
+    def _gating_push(self, layer: int, launched: tuple) -> None:
+        """gating_next_layer baseline, host half: blocking prefetch of the
+        predicted layer+1 experts (``vanilla_prefetch_step``,
+        prefetch.py:241-273), issued after this layer's demand load."""
+        pk = self.policy.prefetch_k
+        B = self.batch
+        i, hptr, ev = launched
         self.cache.push_task(layer, hptr, B * pk, ev)
         self._pushed.append((layer, i))
         self._drain()
@@ -647,8 +660,7 @@ class SpecMoEEngine:
         pk = self.policy.prefetch_k
         for l in range(a.num_layers):
             lw = w.layers[l]
-            h = rms_norm(x, lw.attn_norm, a.rms_eps)
-            x = x + attention(w, l, h, self.draft_kv, start, kv_len_max)
+            x = attention_block(w, l, x, self.draft_kv, start)
             hn = rms_norm(x, lw.ffn_norm, a.rms_eps)
             if spmoe and l <= self.cutoff:
                 if ring_base is None:
@@ -657,8 +669,7 @@ class SpecMoEEngine:
                     self.predictor.predict_at(ring_base + l, hn[:, -1, :].contiguous(), lw.router, pk, True,
                                               self.pred_w, self.pred_idx)
             x = self._dense_ffn(lw.draft_ffn, a.d_ffn, hn.reshape(B * T, -1), x.reshape(B * T, -1), s).view(B, T, -1)
-        hn = rms_norm(x[:, -1, :], w.final_norm, a.rms_eps)
-        return torch.matmul(hn, w.lm_head.t()).float()
+        return lm_logits(w, x[:, -1, :])
 
     # ------------------------------------------------------------ CUDA graphs
     def _capture(self, fn) -> torch.cuda.CUDAGraph:
@@ -696,10 +707,16 @@ class SpecMoEEngine:
         self._vxn = torch.zeros((B * T, H), dtype=torch.bfloat16, device=dev)
         self._vstart = torch.zeros((B,), dtype=torch.int64, device=dev)
         self._h_vstart = torch.zeros((B,), dtype=torch.int64).pin_memory()
-        # plausible positions for the warm-up/capture runs (overwritten later)
-        P0 = min(len(sq) for sq in self.seqs)
-        self._g_base.fill_(P0 - 2)
-        self._vstart.fill_(P0 - 1)
+        # each sequence's own next positions for the warm-up run outside
+        # capture: it writes KV only at positions the next real step rewrites
+        # before reading them (draft P-2.., verify P-1..), never over
+        # committed entries of a longer sequence (re-capture mid-run with
+        # diverged lengths, see recalibrate)
+        for b, sq in enumerate(self.seqs):
+            self._h_base[b] = len(sq) - 2
+            self._h_vstart[b] = len(sq) - 1
+        self._g_base.copy_(self._h_base)
+        self._vstart.copy_(self._h_vstart)
         dkv, tkv = self.draft_kv.max_seq, self.target_kv.max_seq
 
         def draft_fn(d):
@@ -718,9 +735,8 @@ class SpecMoEEngine:
             def fn():
                 lw = self.weights.layers[l]
                 x = self._vx.view(B, T, H)
-                h = rms_norm(x, lw.attn_norm, a.rms_eps)
-                x.add_(attention(self.weights, l, h, self.target_kv, self._vstart, tkv))
-                self._vxn.copy_(rms_norm(x, lw.ffn_norm, a.rms_eps).view(B * T, H))
+                attention_block(self.weights, l, x, self.target_kv, self._vstart, out=x)
+                rms_norm(x, lw.ffn_norm, a.rms_eps, out=self._vxn.view(B, T, H))
                 self._vroute[l] = self._route(l, self._vxn, self.scratch)
             return fn
 
@@ -748,19 +764,18 @@ class SpecMoEEngine:
                     eb.record()
                     self.stalls.append(_Stall("prefetch", l, ea, eb))
 
-    def _target_forward(self, tokens: torch.Tensor, start: torch.Tensor, kv_len_max: int, s: _Scratch) -> torch.Tensor:
+    def _target_forward(self, tokens: torch.Tensor, start: torch.Tensor, kv_len_max: int, s: _Scratch,
+                        logits: bool = True) -> torch.Tensor | None:
         a, w = self.arch, self.weights
         B, T = tokens.shape
         x = self._embed(tokens)
         for l in range(a.num_layers):
             self._gating_waits(l)
             lw = w.layers[l]
-            h = rms_norm(x, lw.attn_norm, a.rms_eps)
-            x = x + attention(w, l, h, self.target_kv, start, kv_len_max)
+            x = attention_block(w, l, x, self.target_kv, start)
             hn = rms_norm(x, lw.ffn_norm, a.rms_eps)
             x = self._moe_verify(l, hn.reshape(B * T, -1).contiguous(), x.reshape(B * T, -1).contiguous(), s).view(B, T, -1)
-        hn = rms_norm(x, w.final_norm, a.rms_eps)
-        return torch.matmul(hn, w.lm_head.t()).float()
+        return lm_logits(w, x) if logits else None
 
     def _step_graphed(self, P: list[int], N: int, ev1):
         """Drafting + verification with the captured graphs; the per-layer
@@ -806,8 +821,7 @@ class SpecMoEEngine:
                 self.route_events.append((len(self.iter_records), l, ev))
             self._moe_verify(l, self._vxn, self._vx, self.scratch, routed=self._vroute[l])
             self._slot_end("verify", P[0] - 1, l)
-        hn = rms_norm(self._vx.view(B, T, H), self.weights.final_norm, a.rms_eps)
-        logits = torch.matmul(hn, self.weights.lm_head.t()).float()
+        logits = lm_logits(self.weights, self._vx.view(B, T, H))
         return logits, draft_tok
 
     def _slot_begin(self) -> None:
@@ -852,13 +866,14 @@ class SpecMoEEngine:
         B, P = prompts.shape
         if B != self.batch or P < 2:
             raise ValueError("prompts must be [batch, >=2]")
+        self._check_room(P)
         self.seqs = [list(map(int, row)) for row in prompts.tolist()]
         self.draft_len = [P - 1] * B  # positions held by the draft KV
         ctx = prompts[:, :-1].to(self.device)
         start = torch.zeros((B,), dtype=torch.int64, device=self.device)
         s = self._prefill_scratch(B * (P - 1))
         self._draft_forward(ctx, start, P - 1, None)
-        self._target_forward(ctx, start, P - 1, s)
+        self._target_forward(ctx, start, P - 1, s, logits=False)
         self.cache.drain()
         torch.cuda.synchronize(self.device)
         self._ensure_graphs()
@@ -866,6 +881,15 @@ class SpecMoEEngine:
         self.cache.clear_log()
         self.history = HistoryCounter(self.arch.num_layers, self.arch.num_experts)
         self._reset_run_state()
+
+    def _check_room(self, positions: int) -> None:
+        """Raise before any KV write past the caches: an SD iteration writes
+        positions up to len(seq) + N - 1 (verify), prefill up to P - 2."""
+        cap = min(self.draft_kv.max_seq, self.target_kv.max_seq)
+        if positions > cap:
+            raise ValueError(
+                f"sequence would need {positions} KV positions but the caches hold {cap} "
+                f"(max_tokens={self.max_tokens}, arch.max_seq={self.arch.max_seq})")
 
     def _coarse_history_enqueue(self) -> None:
         pk = self.policy.prefetch_k
@@ -892,6 +916,7 @@ class SpecMoEEngine:
         if pol.policy is Policy.COARSE_HISTORY:
             self._coarse_history_enqueue()
         P = [len(sq) for sq in self.seqs]
+        self._check_room(max(P) + N)
         graphs = self.use_graphs and N == pol.draft_length
         if graphs:
             self._ensure_graphs()

@@ -436,8 +436,47 @@ def rope_kv(qkv: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor, start: torc
     q = torch.empty((B, nh, T, hd), dtype=BF16, device=qkv.device)
     LAUNCHES["count"] += 1
     _native.call("spmoe_rope_kv", qkv.data_ptr(), cos.data_ptr(), sin.data_ptr(), start.data_ptr(), B, T, nh, nkv,
-                 hd, k_cache.shape[2], q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), _stream(stream))
+                 hd, k_cache.shape[2], cos.shape[0], q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
+                 _stream(stream))
     return q
+
+
+def linear(x: torch.Tensor, w: torch.Tensor, *, norm_w: torch.Tensor | None = None, eps: float = 0.0,
+           out_f32: torch.Tensor | None = None, out: torch.Tensor | None = None,
+           residual: torch.Tensor | None = None, f32: bool = False, stream=None) -> torch.Tensor:
+    """K9: ``x [..., K] @ w[N, K]^T`` with the fixed-order dot product.
+
+    ``norm_w``: RMSNorm x first (fused).  ``f32`` / ``out_f32``: fp32 output
+    (logits); else bf16, or ``bf16(residual + bf16(y))`` with ``residual``
+    (``out`` may be ``residual`` itself: in place)."""
+    _need(w, BF16, "w", 2)
+    if x.dtype != BF16 or not x.is_cuda:
+        raise ValueError("x must be a CUDA bf16 tensor (no CPU fallback)")
+    N, K = w.shape
+    if x.shape[-1] != K:
+        raise ValueError("linear: x and w disagree on K")
+    x2 = x.reshape(-1, K)
+    if x2.stride(-1) != 1:
+        x2 = x2.contiguous()
+    T = x2.shape[0]
+    lead = tuple(x.shape[:-1])
+    y32 = yb = None
+    if f32 or out_f32 is not None:
+        y32 = out_f32 if out_f32 is not None else torch.empty(lead + (N,), dtype=F32, device=x.device)
+        res = y32
+    else:
+        yb = out if out is not None else torch.empty(lead + (N,), dtype=BF16, device=x.device)
+        res = yb
+    if residual is not None:
+        _need(residual, BF16, "residual")
+        if residual.numel() != T * N:
+            raise ValueError("residual shape mismatch")
+    if norm_w is not None:
+        _need(norm_w, BF16, "norm_w", 1)
+    LAUNCHES["count"] += 1
+    _native.call("spmoe_linear", w.data_ptr(), x2.data_ptr(), x2.stride(0), T, K, N, _ptr(norm_w), float(eps),
+                 _ptr(y32), N if y32 is not None else 0, _ptr(yb), _ptr(residual), _stream(stream))
+    return res
 
 
 def attention_cached(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, start: torch.Tensor,

@@ -18,8 +18,10 @@ hidden states.  Everything here is plumbing around the hot path:
   shared experts, lm_head, and the draft's dense FFN.  The draft shares the
   target's embedding, attention and lm_head (SURVEY.md §7 hard part 2) and
   uses the mean of the layer's experts as its FFN, optionally perturbed.
-* attention / RoPE / RMSNorm in torch (cuBLAS GEMMs + SDPA): not on the hot
-  path.
+* the attention block and lm_head around the MoE: K9 fixed-order
+  projections, RoPE + KV append and attention kernels (csrc/spmoe_attn.cu),
+  all inside the determinism contract so the whole forward is reproducible
+  on the CPU oracle.
 """
 
 from __future__ import annotations
@@ -475,6 +477,20 @@ def build_weights(
     )
 
 
+def gate_mass(router: np.ndarray, top_k: int, renorm: bool) -> float:
+    """Expected routed gate mass of a router ``[E, H]``: 1 with top-k
+    renormalisation, else E[sum of the top-k softmax probabilities] over 512
+    seeded N(0, 1) inputs -- host float64 (numpy), so the CPU reference arm
+    (oracle/cpu_model.py) derives the identical draft FFN."""
+    if renorm:
+        return 1.0
+    xs = np.random.default_rng(0).standard_normal((512, router.shape[1]))
+    lg = xs @ router.astype(np.float64).T
+    p = np.exp(lg - lg.max(-1, keepdims=True))
+    p /= p.sum(-1, keepdims=True)
+    return float(np.sort(p, axis=-1)[:, -top_k:].sum(-1).mean())
+
+
 def _draft_proxy(arch: ArchSpec, mean: torch.Tensor, shared: torch.Tensor | None, router: torch.Tensor) -> torch.Tensor:
     """Dense draft FFN approximating the layer's MoE: the mean routed expert
     with W2 scaled by the expected routed gate mass (1 with top-k renorm,
@@ -482,13 +498,7 @@ def _draft_proxy(arch: ArchSpec, mean: torch.Tensor, shared: torch.Tensor | None
     RMS inputs), concatenated along F with the shared expert (W2 scaled by
     the expected sigmoid gate, 0.5, for Qwen)."""
     H, F = arch.hidden, arch.ffn
-    if arch.renorm:
-        mass = 1.0
-    else:
-        g = torch.Generator(device=router.device).manual_seed(0)
-        xs = torch.randn((512, H), generator=g, device=router.device, dtype=torch.float32)
-        p = torch.softmax(xs @ router.float().t(), dim=-1)
-        mass = float(p.topk(arch.top_k, dim=-1).values.sum(-1).mean())
+    mass = gate_mass(router.float().cpu().numpy(), arch.top_k, arch.renorm)
     w1 = mean[: F * H].view(F, H)
     w3 = mean[F * H : 2 * F * H].view(F, H)
     w2 = (mean[2 * F * H :].view(H, F).float() * mass).to(mean.dtype)
@@ -527,20 +537,33 @@ def fill_expert_blob(blob: torch.Tensor, arch: ArchSpec, seed: int, row: int) ->
 # ---------------------------------------------------------------------------
 # transformer pieces (torch; off the hot path)
 # ---------------------------------------------------------------------------
-def rope_tables(arch: ArchSpec, device) -> tuple[torch.Tensor, torch.Tensor]:
+def rope_tables_host(arch: ArchSpec) -> tuple[np.ndarray, np.ndarray]:
+    """Rotate-half RoPE tables ``[max_seq, head_dim]`` f32, computed on the
+    host with libm (``math``: correctly rounded double cos/sin, independent
+    of the CPU's SIMD extensions) so the device and the CPU oracle use the
+    same bits.  inv_freq_i = 1 / theta^(2i/d); angle = pos * inv_freq."""
     d = arch.head_dim
-    inv = 1.0 / (arch.rope_theta ** (torch.arange(0, d, 2, dtype=torch.float64, device=device) / d))
-    pos = torch.arange(arch.max_seq, dtype=torch.float64, device=device)
-    ang = torch.outer(pos, inv)
-    ang = torch.cat([ang, ang], dim=-1)
-    return ang.cos().float(), ang.sin().float()
+    inv = [1.0 / (arch.rope_theta ** (i / d)) for i in range(0, d, 2)]
+    cos = np.empty((arch.max_seq, d), np.float32)
+    sin = np.empty((arch.max_seq, d), np.float32)
+    for p in range(arch.max_seq):
+        c = [math.cos(p * f) for f in inv]
+        s_ = [math.sin(p * f) for f in inv]
+        cos[p] = c + c
+        sin[p] = s_ + s_
+    return cos, sin
 
 
-def rms_norm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
-    """bf16 RMSNorm (csrc/spmoe_attn.cu; fp32 math, one rounding)."""
+def rope_tables(arch: ArchSpec, device) -> tuple[torch.Tensor, torch.Tensor]:
+    cos, sin = rope_tables_host(arch)
+    return torch.from_numpy(cos).to(device), torch.from_numpy(sin).to(device)
+
+
+def rms_norm(x: torch.Tensor, w: torch.Tensor, eps: float, out: torch.Tensor | None = None) -> torch.Tensor:
+    """bf16 RMSNorm (csrc/spmoe_attn.cu; fixed-order fp32 math, IEEE sqrt/div)."""
     from .kernels import rms_norm as _rms
 
-    return _rms(x, w, eps)
+    return _rms(x, w, eps, out=out)
 
 
 class KVCache:
@@ -555,22 +578,31 @@ class KVCache:
         self.max_seq = S
 
 
-def attention(
+def attention_block(
     w: ModelWeights,
     layer: int,
-    x_norm: torch.Tensor,  # [B, T, H]
+    x: torch.Tensor,  # [B, T, H] residual stream
     kv: KVCache,
     start: torch.Tensor,  # [B] int64 position of the first of the T tokens
-    kv_len_max: int,  # max over b of start[b] + T (the kernel masks per sequence)
+    out: torch.Tensor | None = None,
 ) -> torch.Tensor:
-    """qkv projection (cuBLAS) -> fused RoPE + KV append -> causal GQA
-    attention over the cache -> W_o projection (cuBLAS)."""
+    """The attention half of a decoder layer: RMSNorm fused into the qkv
+    projection (K9) -> RoPE + KV append -> causal GQA attention over the
+    cache -> W_o projection fused with the residual add (K9):
+    ``bf16(x + bf16(attn(norm(x)) W_o^T))``; ``out=x`` updates in place."""
     from . import kernels as K
 
     a = w.arch
     lw = w.layers[layer]
-    qkv = torch.matmul(x_norm, lw.wqkv.t())
+    qkv = K.linear(x, lw.wqkv, norm_w=lw.attn_norm, eps=a.rms_eps)
     q = K.rope_kv(qkv, w.rope_cos, w.rope_sin, start, a.num_heads, a.num_kv_heads, a.head_dim, kv.k[layer],
                   kv.v[layer])
     o = K.attention_cached(q, kv.k[layer], kv.v[layer], start)
-    return torch.matmul(o, lw.wo.t())
+    return K.linear(o, lw.wo, residual=x, out=out)
+
+
+def lm_logits(w: ModelWeights, x: torch.Tensor) -> torch.Tensor:
+    """Final RMSNorm fused into the lm_head projection, fp32 logits."""
+    from . import kernels as K
+
+    return K.linear(x, w.lm_head, norm_w=w.final_norm, eps=w.arch.rms_eps, f32=True)

@@ -40,3 +40,20 @@ def test_two_rank_replicas_share_one_pool():
     assert line["tokens_emitted"] >= 2 * 2  # both ranks' streams are summed
     assert line["host_codec"]["codec"] == "xc"
     assert "too small" not in r.stderr  # the tiny pool always fits: the shared path ran
+
+
+def test_bench_gpus_flag_self_spawns_ranks():
+    """`python bench.py --gpus 2` with no torchrun environment launches two
+    ranks itself (the driver's SCALE run needs no harness changes) and
+    reports n_gpus 2 with both streams' tokens and per-rank link figures."""
+    env = dict(os.environ, SPMOE_BENCH_SHARE_GPU="1")
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "tiny", "--steps", "2",
+           "--warmup", "3", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["tokens_emitted"] >= 4
+    assert len(line["per_rank"]) == 2 and all(p["h2d_peak_gbs"] > 0 for p in line["per_rank"])
+
