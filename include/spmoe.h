@@ -409,8 +409,10 @@ void spmoe_rt_unpin(spmoe_rt* rt, const int32_t* layers, const int32_t* experts,
 int spmoe_rt_lru_order(spmoe_rt* rt, int32_t* layers, int32_t* experts, int cap);
 /* counters: hits, misses, evictions, prefetch_evictions,
  * prefetch_insertions, demand_insertions, tasks_completed, tasks_aborted,
- * prefetch_bytes, demand_bytes, n_resident, evictions_of_queued_targets */
-void spmoe_rt_counters(spmoe_rt* rt, int64_t* out12);
+ * prefetch_bytes, demand_bytes, n_resident, evictions_of_queued_targets,
+ * handoff_timeouts (tasks dropped after the bounded 5 s index hand-off wait,
+ * prefetch.py:353-355) */
+void spmoe_rt_counters(spmoe_rt* rt, int64_t* out13);
 void spmoe_rt_reset_stats(spmoe_rt* rt);
 
 /*
@@ -453,8 +455,16 @@ int spmoe_rt_push_task_flag(spmoe_rt* rt, int layer, const int32_t* host_idx, in
 /* Device-side increment of a host-visible counter in mapped memory
  * (stream-ordered; system-scope fenced). */
 int spmoe_signal_bump(int32_t* flag, void* stream);
-/* Block until every pushed task has been popped and its copies issued. */
+/* Block until every pushed task has been popped and its copies issued.
+ * Returns (and clears) the first error since the last drain: a failed H2D
+ * copy / event record (the experts whose copies were not issued are
+ * uninstalled, never left resident over stale bytes), a failed ready-event
+ * wait, or cudaErrorTimeout when a task's indices were not published within
+ * 5 s (the task is dropped and counted in handoff_timeouts). */
 int spmoe_rt_drain(spmoe_rt* rt);
+/* Fault injection for tests: the next n expert copies fail with
+ * cudaErrorInvalidValue before anything is enqueued. */
+int spmoe_rt_debug_fail_copies(spmoe_rt* rt, int n);
 /* Drop queued-but-unpopped tasks (end of inference); returns count. */
 int spmoe_rt_abort_pending(spmoe_rt* rt);
 int spmoe_rt_worker_stop(spmoe_rt* rt);

@@ -55,7 +55,8 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # engine / model pull in torch CUDA state; import lazily
-    if name in ("SpecMoEEngine", "simulate", "effective_cutoff", "compare_policies", "sweep"):
+    if name in ("SpecMoEEngine", "simulate", "effective_cutoff", "compare_policies", "sweep",
+                "SWEEP_PARAMETERS"):
         from . import engine
 
         return getattr(engine, name)

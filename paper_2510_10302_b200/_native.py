@@ -74,6 +74,7 @@ SIGNATURES: dict[str, tuple] = {
     "spmoe_rt_push_task_flag": (_i, [_p, _i, _p, _i, _p, _i, _i]),
     "spmoe_signal_bump": (_i, [_p, _p]),
     "spmoe_rt_drain": (_i, [_p]),
+    "spmoe_rt_debug_fail_copies": (_i, [_p, _i]),
     "spmoe_rt_abort_pending": (_i, [_p]),
     "spmoe_rt_worker_stop": (_i, [_p]),
     "spmoe_rt_transfer_log": (_i, [_p, _p, _p, _i]),

@@ -152,6 +152,7 @@ class NativeExpertCache:
         "demand_bytes",
         "n_resident",
         "evictions_of_queued_targets",
+        "handoff_timeouts",
     )
 
     def __init__(
@@ -250,7 +251,7 @@ class NativeExpertCache:
         return [ExpertId(L[i], X[i]) for i in range(n)]
 
     def counters(self) -> dict[str, int]:
-        buf = (C.c_int64 * 12)()
+        buf = (C.c_int64 * len(self.COUNTER_NAMES))()
         self._lib.spmoe_rt_counters(self._h, buf)
         return dict(zip(self.COUNTER_NAMES, list(buf)))
 
@@ -317,7 +318,12 @@ class NativeExpertCache:
         )
 
     def drain(self) -> None:
-        self._lib.spmoe_rt_drain(self._h)
+        """Wait for every pushed task; raises if a copy, event wait or flag
+        hand-off failed since the last drain (the failed task's experts are
+        not left resident)."""
+        from . import _native
+
+        _native.check("spmoe_rt_drain", self._lib.spmoe_rt_drain(self._h))
 
     def abort_pending(self) -> int:
         return self._lib.spmoe_rt_abort_pending(self._h)

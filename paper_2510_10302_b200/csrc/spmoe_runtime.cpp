@@ -49,7 +49,19 @@ struct Transfer {
   cudaEvent_t start, end;
   cudaEvent_t copy_end;  // after the last H2D (XC tier: before its decode)
   int64_t wire_bytes;  // bytes that crossed the host link
+  // once the copies are done the three events are turned into times (ms
+  // since the runtime epoch) and recycled, so a long run holds a bounded
+  // number of live events (spmoe_rt::resolve_log)
+  bool resolved = false;
+  float t_start = -1.0f, t_end = -1.0f, t_copy_end = -1.0f;
 };
+
+// Bound on the consumer's flag / event wait for one prefetch task, as the
+// reference bounds the live worker's checkpoint wait (prefetch.py:353-355).
+constexpr double kHandoffTimeoutS = 5.0;
+// Live timing events kept before finished ones are resolved and recycled.
+constexpr size_t kLiveTransfers = 512;
+constexpr size_t kLiveDecodeTimings = 1024;
 
 }  // namespace
 
@@ -92,11 +104,22 @@ struct spmoe_rt {
     int64_t bytes;
   };
   std::vector<DecodeTiming> dec_times;
+  double dec_ms_acc = 0.0;  // resolved decode timings not yet reported
+  int64_t dec_bytes_acc = 0, dec_n_acc = 0;
 
   // counters
   int64_t hits = 0, misses = 0, evictions = 0, prefetch_evictions = 0, prefetch_insertions = 0,
           demand_insertions = 0, tasks_completed = 0, tasks_aborted = 0, prefetch_bytes = 0,
-          demand_bytes = 0, evictions_of_queued = 0, prefetch_wire = 0, demand_wire = 0;
+          demand_bytes = 0, evictions_of_queued = 0, prefetch_wire = 0, demand_wire = 0,
+          handoff_timeouts = 0;
+
+  // first CUDA error seen by a copy / event / hand-off since the last
+  // spmoe_rt_drain (which returns and clears it); guarded by mu_
+  int err_ = 0;
+  int fail_copies_ = 0;  // fault injection (spmoe_rt_debug_fail_copies)
+  void note_error(int st) {
+    if (st != 0 && err_ == 0) err_ = st;
+  }
 
   // worker
   std::mutex mu_;
@@ -112,8 +135,10 @@ struct spmoe_rt {
 
   // transfer log
   std::vector<Transfer> log_;
+  size_t first_live_ = 0;  // log_[i] for i < first_live_ are resolved
   cudaEvent_t epoch_ = nullptr;
   int seq_ = 0;
+  std::vector<cudaEvent_t> free_ev_;  // recycled timing events
 
   // ---------------------------------------------------------------- LRU
   void unlink(int key) {
@@ -199,9 +224,70 @@ struct spmoe_rt {
 
   // ------------------------------------------------------------- copies
   cudaEvent_t new_timing_event() {
+    if (!free_ev_.empty()) {
+      cudaEvent_t e = free_ev_.back();
+      free_ev_.pop_back();
+      return e;
+    }
     cudaEvent_t e = nullptr;
     cudaEventCreate(&e);
     return e;
+  }
+  void recycle(cudaEvent_t& e) {
+    if (e) free_ev_.push_back(e);
+    e = nullptr;
+  }
+
+  // Turn a finished transfer's events into times and recycle them.
+  bool resolve(Transfer& tr) {
+    if (tr.resolved) return true;
+    if (cudaEventQuery(tr.end) != cudaSuccess || cudaEventQuery(tr.copy_end) != cudaSuccess) return false;
+    cudaEventElapsedTime(&tr.t_start, epoch_, tr.start);
+    cudaEventElapsedTime(&tr.t_end, epoch_, tr.end);
+    cudaEventElapsedTime(&tr.t_copy_end, epoch_, tr.copy_end);
+    recycle(tr.start);
+    recycle(tr.end);
+    recycle(tr.copy_end);
+    tr.resolved = true;
+    return true;
+  }
+  // Keep at most kLiveTransfers transfers holding events: resolve the oldest
+  // ones that have finished (in order; stops at the first still in flight).
+  void resolve_log() {
+    while (log_.size() - first_live_ > kLiveTransfers && resolve(log_[first_live_])) ++first_live_;
+  }
+  void resolve_decode_timings() {
+    if (dec_times.size() <= kLiveDecodeTimings) return;
+    size_t i = 0;
+    for (; i < dec_times.size(); ++i) {
+      auto& t = dec_times[i];
+      if (cudaEventQuery(t.b) != cudaSuccess) break;
+      float x = 0.0f;
+      if (cudaEventElapsedTime(&x, t.a, t.b) == cudaSuccess) {
+        dec_ms_acc += x;
+        dec_bytes_acc += t.bytes;
+        ++dec_n_acc;
+      }
+      recycle(t.a);
+      recycle(t.b);
+    }
+    dec_times.erase(dec_times.begin(), dec_times.begin() + i);
+  }
+  // Undo the installation of keys whose copies were never issued (a failed
+  // copy must not leave an expert marked resident over stale slot bytes).
+  void uninstall(const std::vector<int>& keys) {
+    for (int k : keys) {
+      if (!resident(k)) continue;
+      if (pinned_flag[k]) {
+        pinned_flag[k] = 0;
+        --n_pinned;
+      }
+      unlink(k);
+      free_slots.push_back(slot_of[k]);
+      slot_of[k] = -1;
+      --n_resident;
+    }
+    std::sort(free_slots.begin(), free_slots.end(), std::greater<int>());
   }
 
   const char* host_row(int key) const {
@@ -247,8 +333,8 @@ struct spmoe_rt {
       if (st == cudaSuccess) st = cudaStreamWaitEvent(decode_stream, full, 0);
       DecodeTiming dt{nullptr, nullptr, 0};
       if (st == cudaSuccess && time_decode) {
-        cudaEventCreate(&dt.a);
-        cudaEventCreate(&dt.b);
+        dt.a = new_timing_event();
+        dt.b = new_timing_event();
         dt.bytes = (int64_t)(hi - lo) + 2 * (int64_t)h->seg[g].n;
         st = cudaEventRecord(dt.a, decode_stream);
       }
@@ -279,17 +365,26 @@ struct spmoe_rt {
     tr.end = new_timing_event();
     tr.copy_end = new_timing_event();
     cudaError_t st = cudaEventRecord(tr.start, copy_stream);
+    size_t done = 0;  // keys whose copy (and ready event) was issued
     for (size_t i = 0; i < keys.size() && st == cudaSuccess; ++i) {
       const int k = keys[i];
       const int s = slot_of[k];
+      if (fail_copies_ > 0) {
+        --fail_copies_;
+        st = cudaErrorInvalidValue;
+        break;
+      }
       st = codec ? copy_xc(s, host_row(k), tr.wire_bytes) : copy_raw(s, host_row(k), tr.wire_bytes);
+      if (st != cudaSuccess) break;
       ready_rec[s] = 1;
-      if (st == cudaSuccess && !batched && kind == 0 && i + 1 < keys.size()) {
+      ++done;
+      if (!batched && kind == 0 && i + 1 < keys.size()) {
         // unbatched I/O (PolicySpec.batched_io = false): one copy launch at
         // a time, each completed before the next is issued
         st = cudaStreamSynchronize(copy_stream);
       }
     }
+    if (done < keys.size()) uninstall(std::vector<int>(keys.begin() + done, keys.end()));
     // the transfer ends when its last expert is usable (after its decode)
     if (st == cudaSuccess) st = cudaEventRecord(tr.copy_end, copy_stream);
     if (st == cudaSuccess) st = cudaEventRecord(tr.end, codec ? decode_stream : copy_stream);
@@ -302,22 +397,44 @@ struct spmoe_rt {
       demand_wire += tr.wire_bytes;
     }
     log_.push_back(std::move(tr));
+    resolve_log();
+    if (time_decode) resolve_decode_timings();
+    note_error((int)st);
     return (int)st;
   }
 
   // -------------------------------------------------------------- worker
   void run_task(const Task& t) {
+    int wait_st = 0;
     if (t.flag) {
       // graph-safe hand-off: the predictor's completion counter in mapped
-      // memory reaches `expected` once this replay's indices are visible
+      // memory reaches `expected` once this replay's indices are visible;
+      // bounded like the reference's checkpoint wait (prefetch.py:353-355)
+      const auto t0 = std::chrono::steady_clock::now();
       int spins = 0;
       while (*t.flag < t.expected) {
-        if (++spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(2));
+        if (++spins > 64) {
+          std::this_thread::sleep_for(std::chrono::microseconds(2));
+          if ((spins & 1023) == 0 &&
+              std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > kHandoffTimeoutS) {
+            wait_st = (int)cudaErrorTimeout;
+            break;
+          }
+        }
       }
     } else if (t.ready) {
-      cudaEventSynchronize(t.ready);
+      wait_st = (int)cudaEventSynchronize(t.ready);
     }
     std::lock_guard<std::mutex> g(mu_);
+    if (wait_st != 0) {
+      // the task's indices never became valid: drop it, count it, and
+      // surface the error at the next drain
+      if (wait_st == (int)cudaErrorTimeout) ++handoff_timeouts;
+      ++tasks_aborted;
+      note_error(wait_st);
+      window_.push_back(WindowEntry{});
+      return;
+    }
     // pop-time residency filter (enqueue_critical prefetch.py:131-135 and the
     // worker re-check prefetch.py:186-189 collapse into one probe here,
     // because the predicted ids live on the device until the kernel is done)
@@ -335,8 +452,8 @@ struct spmoe_rt {
       std::vector<int> victims;
       if (insert_batch(load, 0, victims)) {
         we.victims = victims;
-        issue_copies(load, t.layer, 0);
-        ++tasks_completed;
+        if (issue_copies(load, t.layer, 0) == 0) ++tasks_completed;
+        else ++tasks_aborted;
       }
     }
     window_.push_back(std::move(we));
@@ -424,10 +541,16 @@ void spmoe_rt_destroy(spmoe_rt* rt) {
   for (auto e : rt->ready_ev) cudaEventDestroy(e);
   for (auto e : rt->read_ev) cudaEventDestroy(e);
   for (auto& t : rt->log_) {
+    if (t.resolved) continue;
     cudaEventDestroy(t.start);
     cudaEventDestroy(t.end);
     cudaEventDestroy(t.copy_end);
   }
+  for (auto& t : rt->dec_times) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (auto e : rt->free_ev_) cudaEventDestroy(e);
   if (rt->epoch_) cudaEventDestroy(rt->epoch_);
   delete rt;
 }
@@ -512,7 +635,7 @@ void spmoe_rt_counters(spmoe_rt* rt, int64_t* o) {
   o[0] = rt->hits; o[1] = rt->misses; o[2] = rt->evictions; o[3] = rt->prefetch_evictions;
   o[4] = rt->prefetch_insertions; o[5] = rt->demand_insertions; o[6] = rt->tasks_completed;
   o[7] = rt->tasks_aborted; o[8] = rt->prefetch_bytes; o[9] = rt->demand_bytes;
-  o[10] = rt->n_resident; o[11] = rt->evictions_of_queued;
+  o[10] = rt->n_resident; o[11] = rt->evictions_of_queued; o[12] = rt->handoff_timeouts;
 }
 
 void spmoe_rt_reset_stats(spmoe_rt* rt) {
@@ -523,6 +646,7 @@ void spmoe_rt_reset_stats(spmoe_rt* rt) {
   rt->tasks_completed = rt->tasks_aborted = 0;
   rt->prefetch_bytes = rt->demand_bytes = rt->evictions_of_queued = 0;
   rt->prefetch_wire = rt->demand_wire = 0;
+  rt->handoff_timeouts = 0;
 }
 
 int spmoe_rt_set_codec(spmoe_rt* rt, size_t row_stride, void* staging, size_t staging_bytes, int n_staging,
@@ -569,8 +693,10 @@ int spmoe_rt_decode_timing(spmoe_rt* rt, int enable) {
 int spmoe_rt_decode_stats(spmoe_rt* rt, double* ms_out, int64_t* bytes_out, int64_t* launches_out) {
   if (!rt) return (int)cudaErrorInvalidValue;
   std::lock_guard<std::mutex> g(rt->mu_);
-  double ms = 0.0;
-  int64_t bytes = 0, n = 0;
+  double ms = rt->dec_ms_acc;
+  int64_t bytes = rt->dec_bytes_acc, n = rt->dec_n_acc;
+  rt->dec_ms_acc = 0.0;
+  rt->dec_bytes_acc = rt->dec_n_acc = 0;
   for (auto& t : rt->dec_times) {
     cudaEventSynchronize(t.b);
     float x = 0.0f;
@@ -579,8 +705,8 @@ int spmoe_rt_decode_stats(spmoe_rt* rt, double* ms_out, int64_t* bytes_out, int6
       bytes += t.bytes;
       ++n;
     }
-    cudaEventDestroy(t.a);
-    cudaEventDestroy(t.b);
+    rt->recycle(t.a);
+    rt->recycle(t.b);
   }
   rt->dec_times.clear();
   if (ms_out) *ms_out = ms;
@@ -612,11 +738,20 @@ int spmoe_rt_demand_load(spmoe_rt* rt, const int32_t* layers, const int32_t* exp
   if (!missing.empty()) {
     std::vector<int> victims;
     if (!rt->insert_batch(missing, 1, victims)) return -1;
+    const int err_before = rt->err_;
     st = rt->issue_copies(missing, missing[0] / rt->E, 1);
+    rt->err_ = err_before;  // returned to the caller here, not at the next drain
   }
   if (slots_out)
     for (int i = 0; i < n; ++i) slots_out[i] = rt->slot_of[ids[i]];
   return st;
+}
+
+int spmoe_rt_debug_fail_copies(spmoe_rt* rt, int n) {
+  if (!rt || n < 0) return (int)cudaErrorInvalidValue;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  rt->fail_copies_ = n;
+  return 0;
 }
 
 int spmoe_rt_wait_slot(spmoe_rt* rt, int slot, void* stream) {
@@ -693,7 +828,10 @@ int spmoe_rt_drain(spmoe_rt* rt) {
     }
   }
   rt->close_window();
-  return 0;
+  std::lock_guard<std::mutex> g(rt->mu_);
+  const int err = rt->err_;
+  rt->err_ = 0;
+  return err;
 }
 
 int spmoe_rt_abort_pending(spmoe_rt* rt) {
@@ -717,12 +855,14 @@ void spmoe_rt_clear_log(spmoe_rt* rt) {
   if (!rt) return;
   std::lock_guard<std::mutex> g(rt->mu_);
   for (auto& t : rt->log_) {
+    if (t.resolved) continue;
     cudaEventSynchronize(t.end);
-    cudaEventDestroy(t.start);
-    cudaEventDestroy(t.end);
-    cudaEventDestroy(t.copy_end);
+    rt->recycle(t.start);
+    rt->recycle(t.end);
+    rt->recycle(t.copy_end);
   }
   rt->log_.clear();
+  rt->first_live_ = 0;
 }
 
 int spmoe_rt_worker_stop(spmoe_rt* rt) {
@@ -743,19 +883,15 @@ int spmoe_rt_transfer_log(spmoe_rt* rt, int32_t* rec4, double* t2, int cap) {
   if (!rt) return 0;
   std::lock_guard<std::mutex> g(rt->mu_);
   int n = 0;
-  for (const auto& tr : rt->log_) {
+  for (auto& tr : rt->log_) {
     if (n >= cap) break;
     rec4[4 * n + 0] = tr.layer;
     rec4[4 * n + 1] = (int32_t)tr.experts.size();
     rec4[4 * n + 2] = tr.kind;
     rec4[4 * n + 3] = tr.seq;
-    float a = -1.0f, b = -1.0f;
-    if (cudaEventQuery(tr.end) == cudaSuccess) {
-      cudaEventElapsedTime(&a, rt->epoch_, tr.start);
-      cudaEventElapsedTime(&b, rt->epoch_, tr.end);
-    }
-    t2[2 * n + 0] = a;
-    t2[2 * n + 1] = b;
+    const bool ok = rt->resolve(tr);
+    t2[2 * n + 0] = ok ? tr.t_start : -1.0f;
+    t2[2 * n + 1] = ok ? tr.t_end : -1.0f;
     ++n;
   }
   return n;
@@ -765,10 +901,8 @@ double spmoe_rt_transfer_copy_end_ms(spmoe_rt* rt, int i) {
   if (!rt) return -1.0;
   std::lock_guard<std::mutex> g(rt->mu_);
   if (i < 0 || i >= (int)rt->log_.size()) return -1.0;
-  float ms = -1.0f;
-  if (cudaEventQuery(rt->log_[i].copy_end) != cudaSuccess) return -1.0;
-  if (cudaEventElapsedTime(&ms, rt->epoch_, rt->log_[i].copy_end) != cudaSuccess) return -1.0;
-  return ms;
+  auto& tr = rt->log_[i];
+  return rt->resolve(tr) ? (double)tr.t_copy_end : -1.0;
 }
 
 int64_t spmoe_rt_transfer_wire_bytes(spmoe_rt* rt, int i) {

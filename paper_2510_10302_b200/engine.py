@@ -292,6 +292,13 @@ class SpecMoEEngine:
         # layer, routed ids) at each verify layer
         self.decisions: list[tuple[str, int, list[int]]] = []
         self.captures: list[dict] = []
+        # finished timing events folded into plain numbers (_fold_events), so
+        # a long generate() holds a bounded number of live CUDA events
+        self._stall_done = {"prefetch": 0.0, "demand": 0.0}
+        self._iters_done: list[tuple[float, float]] = []  # (draft ms, verify ms)
+        self._k3_done: list[tuple[float, int, int, int]] = []  # (ms, bytes, experts, rows)
+        self.k3_events = []
+        self._slots_done: list[ComputeSlot] = []
 
     @property
     def stream(self):
@@ -431,28 +438,29 @@ class SpecMoEEngine:
 
     def k3_roofline(self) -> dict:
         """Average algorithmic bytes / launch-pair duration of the timed K3 calls."""
-        torch.cuda.synchronize(self.device)
-        if not self.k3_events:
+        self._fold_events(force=True)
+        done = self._k3_done
+        if not done:
             return {}
-        ms = [a_.elapsed_time(b_) for a_, b_, *_ in self.k3_events]
-        byts = [x[2] for x in self.k3_events]
+        ms = [x[0] for x in done]
+        byts = [x[1] for x in done]
         tot_ms = sum(ms)
         return {
             "launches": len(ms),
             "bytes_per_launch": sum(byts) / len(byts),
             "ms_per_launch": tot_ms / len(ms),
             "achieved_gbs": sum(byts) / (tot_ms / 1e3) / 1e9,
-            "experts_per_launch": sum(x[3] for x in self.k3_events) / len(ms),
-            "rows_per_launch": sum(x[4] for x in self.k3_events) / len(ms),
+            "experts_per_launch": sum(x[2] for x in done) / len(ms),
+            "rows_per_launch": sum(x[3] for x in done) / len(ms),
             "total_ms": tot_ms,
-            "by_shape": self._k3_by_shape(ms),
+            "by_shape": self._k3_by_shape(done),
         }
 
-    def _k3_by_shape(self, ms) -> dict:
+    def _k3_by_shape(self, done) -> dict:
         """Timed K3 launches grouped by (experts, routed rows): count, mean
         microseconds and achieved GB/s of algorithmic bytes."""
         groups: dict = {}
-        for (_, _, byts, ne, rows), t in zip(self.k3_events, ms):
+        for t, byts, ne, rows in done:
             g = groups.setdefault(f"{ne}x{rows}", [0, 0.0, 0])
             g[0] += 1
             g[1] += t
@@ -900,9 +908,35 @@ class SpecMoEEngine:
             self.cache.push_task(l, buf.ctypes.data, pk, 0)
             self._pushed.append((l, buf))
 
+    _LIVE_EVENTS = 2048
+
+    def _fold_events(self, force: bool = False) -> None:
+        """Turn completed timing-event pairs into numbers and drop the events
+        once more than _LIVE_EVENTS are held (or always with ``force``).  The
+        lists are appended in stream order and step() ends with a host sync,
+        so everything recorded by earlier iterations has completed."""
+        n = len(self.stalls) + len(self.k3_events) + len(self.iter_events) + len(self._slot_events)
+        if not force and n <= self._LIVE_EVENTS:
+            return
+        torch.cuda.synchronize(self.device)
+        for s_ in self.stalls:
+            self._stall_done[s_.kind] += s_.a.elapsed_time(s_.b)
+        self.stalls = []
+        for ea, eb, byts, ne, rows in self.k3_events:
+            self._k3_done.append((ea.elapsed_time(eb), byts, ne, rows))
+        self.k3_events = []
+        for e0, e1, e2 in self.iter_events:
+            self._iters_done.append((e0.elapsed_time(e1), e1.elapsed_time(e2)))
+        self.iter_events = []
+        for kind, it, tok, layer, ea, eb in self._slot_events:
+            self._slots_done.append(ComputeSlot(kind, it, tok, layer, self.cache.since_epoch_ms(ea) / 1e3,
+                                                self.cache.since_epoch_ms(eb) / 1e3))
+        self._slot_events = []
+
     def step(self, remaining: list[int] | None = None) -> list[int]:
         """One SD iteration for every sequence; returns tokens emitted per
         sequence (the accepted drafts plus one correction/bonus token)."""
+        self._fold_events()
         a, pol = self.arch, self.policy
         B = self.batch
         N = pol.draft_length
@@ -996,20 +1030,16 @@ class SpecMoEEngine:
 
     # -------------------------------------------------------------- report
     def timing_summary(self) -> dict:
-        torch.cuda.synchronize(self.device)
+        self._fold_events(force=True)
         draft = verify = 0.0
         iters = []
         t = 0.0
-        for i, (e0, e1, e2) in enumerate(self.iter_events):
-            d = e0.elapsed_time(e1)
-            v = e1.elapsed_time(e2)
+        for d, v in self._iters_done:
             draft += d
             verify += v
             iters.append((t, t + d, t + d + v))
             t += d + v
-        stall = {"prefetch": 0.0, "demand": 0.0}
-        for s_ in self.stalls:
-            stall[s_.kind] += s_.a.elapsed_time(s_.b)
+        stall = dict(self._stall_done)
         return {"draft_ms": draft, "verify_ms": verify, "stall_ms": stall, "iters": iters}
 
     def export_trace(self, path, seq: int = 0) -> int:
@@ -1081,10 +1111,8 @@ class SpecMoEEngine:
             for r, it in zip(self.iter_records, ts["iters"])
         ]
         # compute slots on the same clock as the transfer log (runtime epoch)
-        slots = [
-            ComputeSlot(kind, it, tok, layer, self.cache.since_epoch_ms(ea) / 1e3, self.cache.since_epoch_ms(eb) / 1e3)
-            for kind, it, tok, layer, ea, eb in self._slot_events
-        ]
+        self._fold_events(force=True)
+        slots = list(self._slots_done)
         n_emit = self.emitted_total
         extras = {
             "batch": self.batch,
@@ -1154,3 +1182,85 @@ def simulate(model, hw, timings, policy, trace=None, predictor=None, warm_start=
         return eng.generate(prompts, max_new_tokens)
     finally:
         eng.close()
+
+
+def _run_points(model, hw, timings, policies, *, arch=None, prompts=None, max_new_tokens: int = 32, batch: int = 1,
+                **engine_kw) -> list[SimReport]:
+    """One engine per policy over ONE model build (pinned host pool and
+    device weights shared through ``model_state``) and identical prompts."""
+    from .model import ARCH_PRESETS
+
+    if arch is None:
+        arch = ARCH_PRESETS.get(getattr(model, "name", ""), ARCH_PRESETS["tiny"])
+    owner = None
+    out = []
+    try:
+        for p in policies:
+            if prompts is None:
+                g = torch.Generator().manual_seed(p.seed)
+                prompts = torch.randint(0, arch.vocab, (batch, 16), generator=g)
+            state = owner.model_state if owner is not None else None
+            kw = dict(engine_kw)
+            kw.setdefault("max_tokens", max(prompts.shape[1] + max_new_tokens + 8, 64))
+            eng = SpecMoEEngine(arch, hw, timings, p, batch=batch, model_state=state, **kw)
+            try:
+                out.append(eng.generate(prompts, max_new_tokens))
+            finally:
+                if owner is None:
+                    owner = eng  # keeps the shared model alive until the last point
+                else:
+                    eng.close()
+    finally:
+        if owner is not None:
+            owner.close()
+    return out
+
+
+def compare_policies(model, hw, timings, policies, trace=None, warm_start=False, *, arch=None, prompts=None,
+                     max_new_tokens: int = 32, batch: int = 1, **engine_kw) -> list[SimReport]:
+    """``moesim.compare_policies`` (``simcore.py:518-527``) on the real
+    engine: one report per policy over the identical model, prompts and seed.
+
+    ``trace`` must be None (routing comes from the hidden states).  The
+    engine's prefill always leaves the prompt's experts resident, which is
+    the real-run counterpart of the reference's ``warm_start`` fill
+    (``simcore.py:299-307``); ``warm_start`` is accepted for signature
+    compatibility."""
+    if trace is not None:
+        raise ValidationError("the B200 engine computes routing from hidden states; pass trace=None")
+    if not policies:
+        return []
+    return _run_points(model, hw, timings, list(policies), arch=arch, prompts=prompts,
+                       max_new_tokens=max_new_tokens, batch=batch, **engine_kw)
+
+
+SWEEP_PARAMETERS = {
+    "cutoff_layer": "cutoff_layer",
+    "draft_length": "draft_length",
+    "cache_capacity": "cache_capacity_experts",
+    "prefetch_k": "prefetch_k",
+}
+
+
+def sweep(parameter: str, values: list, model, hw, timings, policy, trace=None, warm_start=False, *, arch=None,
+          prompts=None, max_new_tokens: int = 32, batch: int = 1, **engine_kw) -> list[tuple[object, SimReport]]:
+    """``moesim.sweep`` (``simcore.py:530-564``) on the real engine: one run
+    per parameter value, same model build, prompts and seed; same parameter
+    names and the same ValidationError rules as the reference."""
+    from dataclasses import replace
+
+    if parameter not in SWEEP_PARAMETERS:
+        raise ValidationError(f"unknown sweep parameter {parameter!r}; choose from {sorted(SWEEP_PARAMETERS)}")
+    if not values:
+        raise ValidationError("sweep range is empty")
+    if parameter == "cutoff_layer" and policy.policy is not Policy.DRAFT_PREFETCH:
+        raise ValidationError("cutoff_layer sweeps require the draft_prefetch policy")
+    if parameter == "prefetch_k" and policy.policy is Policy.ON_DEMAND:
+        raise ValidationError("prefetch_k does not apply to the on_demand policy")
+    if trace is not None:
+        raise ValidationError("the B200 engine computes routing from hidden states; pass trace=None")
+    field_name = SWEEP_PARAMETERS[parameter]
+    pols = [replace(policy, **{field_name: int(v)}) for v in values]
+    reps = _run_points(model, hw, timings, pols, arch=arch, prompts=prompts, max_new_tokens=max_new_tokens,
+                       batch=batch, **engine_kw)
+    return list(zip(values, reps))

@@ -346,3 +346,43 @@ def test_engine_timeline_csvs(tmp_path):
         assert rows[0] == SimReport.csv_header() and len(rows) == 2
     finally:
         eng.close()
+
+
+def test_failed_copy_is_reported_and_rolled_back():
+    """A copy that cannot be issued (fault injection: the runtime's next
+    copies fail as a rejected cudaMemcpyAsync would) surfaces as an error from the demand load and from the
+    worker's drain, and never leaves the expert marked resident (SURVEY §5:
+    copy errors surface as status codes)."""
+    import numpy as np
+
+    from paper_2510_10302_b200 import _native
+    from paper_2510_10302_b200._native import SpmoeError
+    from paper_2510_10302_b200.cache import ExpertId, NativeExpertCache
+
+    lib = _native.load()
+    pool = torch.empty((4, 64), dtype=torch.bfloat16, device="cuda")
+    hostpool = torch.zeros((16, 64), dtype=torch.bfloat16).pin_memory()
+    cs = torch.cuda.Stream()
+    cache = NativeExpertCache(4, 2, 8, dev_pool_ptr=pool.data_ptr(), host_pool_ptr=hostpool.data_ptr(),
+                              slot_bytes=128, copy_stream_ptr=cs.cuda_stream)
+    try:
+        _native.check("inject", lib.spmoe_rt_debug_fail_copies(cache._h, 1))
+        with pytest.raises(SpmoeError):
+            cache.demand_load([(0, 1), (0, 2)])
+        assert ExpertId(0, 1) not in cache and ExpertId(0, 2) not in cache and len(cache) == 0
+        cache.drain()  # the demand error was already returned
+        cache.demand_load([(0, 1)])  # the runtime keeps working
+        cache.drain()
+        assert ExpertId(0, 1) in cache
+        _native.check("inject", lib.spmoe_rt_debug_fail_copies(cache._h, 1))
+        cache.start_worker()
+        idx = np.array([4], np.int32)
+        ev = torch.cuda.Event()
+        ev.record()
+        _native.check("push", lib.spmoe_rt_push_task(cache._h, 1, idx.ctypes.data, 1, ev.cuda_event, 0))
+        with pytest.raises(SpmoeError):
+            cache.drain()
+        assert ExpertId(1, 4) not in cache
+        assert cache.counters()["tasks_aborted"] == 1
+    finally:
+        cache.close()

@@ -118,3 +118,35 @@ def test_native_slot_assignment_matches_policy_oracle(native):
                 assert nat.slot_of(*e) == ora.slot[e]
     finally:
         nat.close()
+
+
+def test_worker_handoff_wait_is_bounded(native):
+    """A prefetch task whose indices are never published (its completion flag
+    never reaches the expected count) is dropped after the bounded wait of
+    the reference's live worker (prefetch.py:353-355): drain raises the
+    timeout instead of hanging, the task counts as aborted, nothing is
+    installed.  Host-only: the flag spin needs no GPU."""
+    import numpy as np
+
+    from paper_2510_10302_b200._native import SpmoeError
+    from paper_2510_10302_b200.cache import ExpertId, NativeExpertCache
+
+    nat = NativeExpertCache(4, 2, 8)
+    try:
+        nat.start_worker()
+        flag = np.zeros(1, np.int32)
+        idx = np.array([3], np.int32)
+        assert native.spmoe_rt_push_task_flag(nat._h, 0, idx.ctypes.data, 1, flag.ctypes.data, 1, -1) == 0
+        with pytest.raises(SpmoeError) as ei:
+            nat.drain()
+        assert "timeout" in str(ei.value).lower() or "timed out" in str(ei.value).lower()
+        c = nat.counters()
+        assert c["handoff_timeouts"] == 1 and c["tasks_aborted"] == 1 and c["tasks_completed"] == 0
+        assert ExpertId(0, 3) not in nat and len(nat) == 0
+        # the error is reported once; the runtime keeps working
+        nat.drain()
+        nat.insert_batch([ExpertId(1, 2)])
+        assert ExpertId(1, 2) in nat
+    finally:
+        nat.stop_worker()
+        nat.close()
