@@ -1193,20 +1193,21 @@ def _run_points(model, hw, timings, policies, *, arch=None, prompts=None, max_ne
     if arch is None:
         arch = ARCH_PRESETS.get(getattr(model, "name", ""), ARCH_PRESETS["tiny"])
     owner = None
+    shared = engine_kw.pop("model_state", None)  # a caller-owned model build
     out = []
     try:
         for p in policies:
             if prompts is None:
                 g = torch.Generator().manual_seed(p.seed)
                 prompts = torch.randint(0, arch.vocab, (batch, 16), generator=g)
-            state = owner.model_state if owner is not None else None
+            state = shared if shared is not None else (owner.model_state if owner is not None else None)
             kw = dict(engine_kw)
             kw.setdefault("max_tokens", max(prompts.shape[1] + max_new_tokens + 8, 64))
             eng = SpecMoEEngine(arch, hw, timings, p, batch=batch, model_state=state, **kw)
             try:
                 out.append(eng.generate(prompts, max_new_tokens))
             finally:
-                if owner is None:
+                if owner is None and shared is None:
                     owner = eng  # keeps the shared model alive until the last point
                 else:
                     eng.close()

@@ -67,9 +67,40 @@ def point(arch, hw, state, *, N=4, batch=1, budget=0.25, cutoff=None, policy="dr
         eng.close()
 
 
+def facade(arch, hw, state, a):
+    import paper_2510_10302_b200 as m
+    from paper_2510_10302_b200.model import model_spec_for
+
+    cap = max(arch.num_experts, int(round(0.25 * arch.num_layers * arch.num_experts)))
+    pol = PolicySpec(policy=Policy.DRAFT_PREFETCH, prefetch_k=arch.top_k, draft_length=4, acceptance_rate=1.0,
+                     seed=1234, cutoff_layer=0, cache_capacity_experts=cap)
+    g = torch.Generator().manual_seed(1000)
+    prompts = torch.randint(0, arch.vocab, (1, 64), generator=g)
+    kw = dict(arch=arch, prompts=prompts, max_new_tokens=5 * a.steps, model_state=state, window_tokens=4)
+    spec, t = model_spec_for(arch), b200_timings(arch, hw)
+
+    def row(label, v, rep):
+        r = {"sweep": "facade", "arch": arch.name, label: v, "tpot_ms": rep.tpot * 1e3, "hit_rate": rep.hit_rate,
+             "cutoff": rep.cutoff_effective, "acceptance": rep.extras["acceptance_rate"],
+             "hidden_prefetch_fraction": rep.extras["hidden_prefetch_fraction"],
+             "prefetch_insertions": rep.counters["prefetch_insertions"]}
+        print(json.dumps(r), flush=True)
+        with open(a.out, "a") as f:
+            f.write(json.dumps(r) + "\n")
+
+    for v, rep in m.sweep("cutoff_layer", [0, 3, 6, 13, 20, 26], spec, hw, t, pol, **kw):
+        row("cutoff_layer", v, rep)
+    from dataclasses import replace
+
+    pols = [replace(pol, policy=Policy(p), cutoff_layer=None if p != "draft_prefetch" else pol.cutoff_layer)
+            for p in ("on_demand", "draft_prefetch", "gating_next_layer", "coarse_history")]
+    for p, rep in zip(pols, m.compare_policies(spec, hw, t, pols, **kw)):
+        row("policy", p.policy.value, rep)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["deepseek", "qwen", "mixtral", "mixtral_grid"])
+    ap.add_argument("which", choices=["deepseek", "qwen", "mixtral", "mixtral_grid", "facade"])
     ap.add_argument("--out", default="profiles/sweeps_r1.jsonl")
     ap.add_argument("--steps", type=int, default=6)
     # the bit-exact CUDA-core K3 gives every policy point the same token
@@ -77,7 +108,7 @@ def main():
     # into launches); tcgen05 split choices do, which perturbs acceptance
     ap.add_argument("--ffn-impl", default="cuda_core")
     a = ap.parse_args()
-    name = {"deepseek": "deepseek_v2_lite", "qwen": "qwen15_moe_a27b", "mixtral": "mixtral_8x7b",
+    name = {"facade": "deepseek_v2_lite", "deepseek": "deepseek_v2_lite", "qwen": "qwen15_moe_a27b", "mixtral": "mixtral_8x7b",
             "mixtral_grid": "mixtral_8x7b"}[a.which]
     arch = get_arch(name)
     hw = HardwareSpec(gpu_memory=183_359 * 2**20, peak_non_expert_memory=24 * 10**9, pcie_bandwidth=55.5e9,
@@ -91,6 +122,12 @@ def main():
     state = seed_eng.model_state
     print(f"# model built in {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
     pts = []
+    if a.which == "facade":
+        # the reference's own sweep / compare_policies entry points
+        # (moesim simcore.py:518-564) over the real engine, one model build
+        facade(arch, hw, state, a)
+        seed_eng.close()
+        return
     if a.which == "deepseek":
         pts.append(dict(policy="on_demand"))
         pts.append(dict())  # solver's cutoff (N-token window)
