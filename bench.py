@@ -256,6 +256,8 @@ def main():
     ap.add_argument("--policy", default="draft_prefetch")
     ap.add_argument("--cutoff", type=int, default=None, help="explicit cutoff layer (default: solver)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-event-pass", dest="event_pass", action="store_false",
+                    help="skip the 2 extra steps that time the roofline kernels with CUDA events")
     ap.add_argument("--ffn-impl", default="auto", choices=["auto", "tcgen05", "cuda_core"])
     ap.add_argument("--tc-min-tokens", type=int, default=None,
                     help="experts with fewer routed tokens take the CUDA-core K3 (default 1: tcgen05 for every expert)")
@@ -368,10 +370,14 @@ def main():
     eng._reset_run_state()
     eng.cache.reset_stats()
     eng.cache.clear_log()
+    # per-launch kernel durations for the rooflines: device-clock spans
+    # (globaltimer, first CTA start -> last CTA end) -- CUDA events around
+    # launches are skewed by ~30 us per pair while the host link is saturated
+    # (profiles/r2_event_skew_probe.txt); an event-timed pass follows below
     eng.time_k3 = True
     if eng.host_pool.codec:
         eng.cache.decode_stats()  # drop warm-up records
-        eng.cache.decode_timing(True)
+        eng.cache.decode_timing("device")
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -401,6 +407,27 @@ def main():
     rep = eng.report(wall_s=wall)
     roof = eng.k3_roofline()
     dec = eng.cache.decode_stats() if eng.host_pool.codec else None
+    # the same kernels timed with CUDA events on their streams (2 untimed
+    # extra steps, outside the timed region): the event-based figures
+    ev_k3, ev_dec = None, None
+    if args.event_pass:
+        eng._reset_run_state()
+        eng.time_k3 = "events"
+        if eng.host_pool.codec:
+            eng.cache.decode_timing("events")
+        for _ in range(2):
+            eng.step()
+        torch.cuda.synchronize()
+        r2 = eng.k3_roofline()
+        ev_k3 = r2.get("events_ms_per_launch")
+        if ev_k3:
+            ev_k3 = {"ms_per_launch": ev_k3, "achieved": r2["bytes_per_launch"] / (ev_k3 / 1e3) / 1e9}
+        if eng.host_pool.codec:
+            d2 = eng.cache.decode_stats()
+            eng.cache.decode_timing(False)
+            if d2["launches"]:
+                ev_dec = {"ms_per_launch": d2["ms"] / d2["launches"], "achieved": d2["gbs"]}
+        eng.time_k3 = False
     per_rank = None
     stats = torch.tensor([dev_ms, wall, float(emitted)], dtype=torch.float64, device="cpu" if share_gpu else "cuda")
     if world > 1:
@@ -479,7 +506,7 @@ def main():
         "stall_ms_per_step": {"prefetch": ex.get("stall_prefetch_ms", 0) / args.steps,
                               "demand": ex.get("stall_demand_ms", 0) / args.steps},
         "roofline_k3": {
-            "kernel": "spmoe_expert_ffn (K3 grouped SwiGLU, up+down launch pair)",
+            "kernel": "spmoe_expert_ffn_tc_units (K3: unit-fused tcgen05 SwiGLU, both phases per (expert, 128-feature block) + fixed-order partial sum)",
             "bound": "hbm",
             "achieved": roof.get("achieved_gbs"),
             "peak": peaks["hbm_gbs"],
@@ -492,6 +519,8 @@ def main():
             "bytes_per_launch": roof.get("bytes_per_launch"),
             "ms_per_launch": roof.get("ms_per_launch"),
             "by_shape": roof.get("by_shape"),
+            "timing": "device globaltimer span per K3 call (first kernel's first CTA start -> last kernel's last CTA end)",
+            "cuda_events": None if not ev_k3 else dict(ev_k3, frac=ev_k3["achieved"] / peaks["hbm_gbs"]),
         },
         # the copy path's XC decode kernel (runs under the copies of later
         # segments; only the last segment of a layer is on the critical path)
@@ -504,6 +533,8 @@ def main():
             "ms_per_step": dec["ms"] / args.steps,
             "bytes_per_launch": dec["bytes"] / dec["launches"],
             "ms_per_launch": dec["ms"] / dec["launches"],
+            "timing": "device globaltimer span per launch (first CTA start -> last CTA end)",
+            "cuda_events": None if not ev_dec else dict(ev_dec, frac=ev_dec["achieved"] / peaks["hbm_gbs"]),
         },
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": d2h_step},
         # Python-issued kernels (K.LAUNCHES) + the runtime's XC decodes

@@ -161,11 +161,37 @@ int spmoe_expert_ffn_tc_fused(const uint16_t* pool, int64_t slot_elems, const in
                               uint16_t* h_scratch, float* y, float* workspace, int split_dn,
                               uint32_t* grid_sync, void* stream);
 
+/*
+ * Unit-fused variant for verify-sized calls (<= 16 routed tokens per
+ * expert): each work unit (expert, 128-feature block m) runs
+ * W1/W3 rows of block m -> h block in shared memory -> the matching W2
+ * column block -> partial y_m; a PDL-chained second launch sums the F/128
+ * partials per element in a fixed order into y.  x_perm: [T*k, H] scratch
+ * for the expert-grouped rows of x (as spmoe_expert_ffn_tc).  workspace:
+ * spmoe_expert_ffn_tc_units_workspace_floats(T*k, H, F) floats.
+ * h_scratch (nullable) receives h.  Same
+ * tolerance contract as spmoe_expert_ffn_tc; an expert's result never
+ * depends on which experts share the launch.  Returns
+ * cudaErrorInvalidValue when max_tokens_per_expert > 16.
+ */
+int spmoe_expert_ffn_tc_units(const uint16_t* pool, int64_t slot_elems, const int32_t* slot_of_expert,
+                              uint64_t expert_mask, const uint16_t* x, int T, int H, int F, int E, int k,
+                              const int32_t* expert_offsets, const int32_t* perm_token,
+                              int max_tokens_per_expert, uint16_t* x_perm, uint16_t* h_scratch, float* y,
+                              float* workspace, void* stream);
+int64_t spmoe_expert_ffn_tc_units_workspace_floats(int rows, int H, int F);
+
 /* Profiling hook: CUDA events (cudaEvent_t, timing-enabled) recorded on the
  * stream right before the first kernel and after the last kernel of the
  * NEXT spmoe_expert_ffn / _tc / _tc_fused call made by this host thread, so
  * the measured span excludes host-side launch preparation.  NULLs clear. */
 int spmoe_k3_timing(void* start, void* end);
+/* Device-clock variant for the NEXT spmoe_expert_ffn_tc / _tc_units call on
+ * this host thread: span points at a zeroed device {uint64 t0, t1}; t0 =
+ * globaltimer (ns) when the call's first kernel starts its first CTA, t1 =
+ * when its last kernel ends its last CTA.  Unlike events it is not skewed
+ * by a saturated host link (tools/probes/tma_stream.cu h2d).  NULL clears. */
+int spmoe_k3_devtiming(void* span);
 
 /* --------------------------------------------------------------------- */
 /* K4  moe_combine                                                        */
@@ -367,6 +393,11 @@ int spmoe_xc_decode(const uint8_t* blob, const spmoe_xc_header* hdr, uint16_t* d
  * copy path decode a segment as soon as its bytes have landed. */
 int spmoe_xc_decode_segments(const uint8_t* blob, const spmoe_xc_header* hdr, int first, int count,
                              uint16_t* dst, void* stream);
+/* Same, with device-clock timing: span (nullable) points at a zeroed device
+ * {uint64 t0, t1}; the launch sets t0 = globaltimer (ns) when its first CTA
+ * starts and t1 = when its last CTA ends. */
+int spmoe_xc_decode_segments_timed(const uint8_t* blob, const spmoe_xc_header* hdr, int first, int count,
+                                   uint16_t* dst, void* stream, void* span);
 
 /* --------------------------------------------------------------------- */
 /* Native runtime: LRU slot cache + prefetch worker (prefetch.py,        */
@@ -501,12 +532,14 @@ double spmoe_rt_transfer_copy_end_ms(spmoe_rt* rt, int i);
  */
 int spmoe_rt_set_codec(spmoe_rt* rt, size_t row_stride, void* staging, size_t staging_bytes,
                        int n_staging, void* decode_stream);
-/* Profiling hook: with enable != 0, every XC segment decode issued from now
- * on is bracketed by timing events on the decode stream. */
+/* Profiling hook for every XC segment decode issued from now on:
+ * enable = 1 brackets each launch with timing events on the decode stream,
+ * enable = 2 records its device-clock span (globaltimer, first CTA start ->
+ * last CTA end), 0 stops. */
 int spmoe_rt_decode_timing(spmoe_rt* rt, int enable);
 /* Sum of the timed decode durations (ms), the bytes they read (blob) plus
  * wrote (raw), and their count since the last call; clears the record
- * (synchronizes on the recorded events). */
+ * (synchronizes on the decode stream). */
 int spmoe_rt_decode_stats(spmoe_rt* rt, double* ms, int64_t* bytes, int64_t* launches);
 /* Host-link bytes since the last reset: {prefetch, demand}. */
 void spmoe_rt_wire_bytes(spmoe_rt* rt, int64_t* out2);

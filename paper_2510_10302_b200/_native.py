@@ -44,6 +44,8 @@ SIGNATURES: dict[str, tuple] = {
     "spmoe_expert_ffn_down": (_i, [_p, _i64, _p, _u64, _i, _i, _i, _i, _i, _p, _p, _p, _i, _p]),
     "spmoe_expert_ffn_tc": (_i, [_p, _i64, _p, _u64, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _i, _i, _p]),
     "spmoe_expert_ffn_tc_fused": (_i, [_p, _i64, _p, _u64, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _i, _p, _p]),
+    "spmoe_expert_ffn_tc_units": (_i, [_p, _i64, _p, _u64, _p, _i, _i, _i, _i, _i, _p, _p, _i, _p, _p, _p, _p, _p]),
+    "spmoe_expert_ffn_tc_units_workspace_floats": (_i64, [_i, _i, _i]),
     "spmoe_k3_timing": (_i, [_p, _p]),
     "spmoe_moe_combine": (_i, [_p, _p, _p, _i, _i, _i, _p, _p, _p, _p, _p]),
     "spmoe_gather_rows": (_i, [_p, _p, _i, _i, _i64, _p, _p]),
@@ -74,6 +76,8 @@ SIGNATURES: dict[str, tuple] = {
     "spmoe_rt_push_task_flag": (_i, [_p, _i, _p, _i, _p, _i, _i]),
     "spmoe_signal_bump": (_i, [_p, _p]),
     "spmoe_rt_drain": (_i, [_p]),
+    "spmoe_k3_devtiming": (_i, [_p]),
+    "spmoe_xc_decode_segments_timed": (_i, [_p, _p, _i, _i, _p, _p, _p]),
     "spmoe_rt_debug_fail_copies": (_i, [_p, _i]),
     "spmoe_rt_abort_pending": (_i, [_p]),
     "spmoe_rt_worker_stop": (_i, [_p]),

@@ -359,9 +359,15 @@ class NativeExpertCache:
         _native.check("spmoe_rt_set_codec", self._lib.spmoe_rt_set_codec(
             self._h, row_stride, staging_ptr, staging_bytes, n_staging, decode_stream_ptr))
 
-    def decode_timing(self, enable: bool) -> None:
-        """Bracket every XC segment decode with timing events (profiling)."""
-        self._lib.spmoe_rt_decode_timing(self._h, 1 if enable else 0)
+    def decode_timing(self, enable) -> None:
+        """Time every XC segment decode from now on (profiling): ``"device"``
+        (or 2) records each launch's device-clock span (globaltimer, first
+        CTA start -> last CTA end), ``True`` / ``"events"`` (or 1) brackets it
+        with CUDA events on the decode stream, falsy stops."""
+        from . import _native
+
+        mode = {"device": 2, "events": 1}.get(enable, 1 if enable is True else int(enable or 0))
+        _native.check("spmoe_rt_decode_timing", self._lib.spmoe_rt_decode_timing(self._h, mode))
 
     def decode_stats(self) -> dict:
         """Timed decodes since the last call: total ms, bytes read + written,

@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "../../include/spmoe.h"
+#include "spmoe_common.cuh"
 
 namespace {
 
@@ -198,6 +199,7 @@ struct DecSeg {
 
 struct DecParams {
   DecSeg seg[SPMOE_XC_MAX_SEG];
+  spmoe::DevSpan* span;  // optional device-clock timing of this launch
 };
 
 // Exponents of one block, lane-major with a 33-word pitch (conflict-free
@@ -264,6 +266,7 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
   // sym0 | sym1 << 8 | sym2 << 16 | count << 24 | bits << 26
   uint32_t* s_lut2 = reinterpret_cast<uint32_t*>(dsm);
   uint8_t* wbase = dsm + 4 * kLutSize;
+  spmoe::span_begin(p.span);
   const DecSeg& S = p.seg[blockIdx.y];
   // the segment's multi-symbol table, precomputed in the blob (lut2)
   for (int i = threadIdx.x; i < kLutSize / 4; i += kDecThreads)
@@ -356,6 +359,7 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
     }
     __syncwarp();
   }
+  spmoe::span_end(p.span);
 }
 
 inline uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
@@ -605,13 +609,14 @@ int spmoe_xc_encode(const uint16_t* src, const spmoe_xc_header* hdr, const void*
   return (int)cudaStreamSynchronize(st);  // luts / luts2 / hdr are host memory
 }
 
-int spmoe_xc_decode_segments(const uint8_t* blob, const spmoe_xc_header* hdr, int first, int count,
-                             uint16_t* dst, void* stream) {
+int spmoe_xc_decode_segments_timed(const uint8_t* blob, const spmoe_xc_header* hdr, int first, int count,
+                                   uint16_t* dst, void* stream, void* span) {
   if (!blob || !hdr || !dst || hdr->magic != SPMOE_XC_MAGIC || hdr->nseg < 1 || hdr->nseg > SPMOE_XC_MAX_SEG ||
       first < 0 || count < 1 || first + count > (int)hdr->nseg)
     return (int)cudaErrorInvalidValue;
   DecParams p;
   std::memset(&p, 0, sizeof(p));
+  p.span = (spmoe::DevSpan*)span;
   uint16_t* d = dst;
   for (int i = 0; i < first; ++i) d += hdr->seg[i].n;
   uint32_t maxblk = 0;
@@ -639,6 +644,11 @@ int spmoe_xc_decode_segments(const uint8_t* blob, const spmoe_xc_header* hdr, in
   const uint32_t gx = std::max(1u, std::min(want, (maxblk + kDecWarps - 1) / kDecWarps));
   xc_decode_kernel<<<dim3(gx, count), kDecThreads, kDecSmemBytes, (cudaStream_t)stream>>>(p);
   return (int)cudaGetLastError();
+}
+
+int spmoe_xc_decode_segments(const uint8_t* blob, const spmoe_xc_header* hdr, int first, int count,
+                             uint16_t* dst, void* stream) {
+  return spmoe_xc_decode_segments_timed(blob, hdr, first, count, dst, stream, nullptr);
 }
 
 int spmoe_xc_decode(const uint8_t* blob, const spmoe_xc_header* hdr, uint16_t* dst, void* stream) {

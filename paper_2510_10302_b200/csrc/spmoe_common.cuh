@@ -17,7 +17,33 @@ namespace spmoe {
 // measured duration excludes host-side launch preparation.
 struct K3Timing {
   cudaEvent_t start = nullptr, end = nullptr;
+  void* dspan = nullptr;  // DevSpan* (spmoe_k3_devtiming)
 };
+
+// Device-clock span of one launch (or one chain of launches): t0 = the
+// globaltimer (ns) when the first CTA of the first kernel starts, t1 = when
+// the last CTA of the last kernel ends.  Zero-initialised by the host; CUDA
+// events around launches are skewed by tens of microseconds while the host
+// link is saturated (tools/probes/tma_stream.cu h2d), the device clock is
+// not.
+struct DevSpan {
+  unsigned long long t0, t1;
+};
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// thread 0 of every CTA; the earliest CTA wins
+__device__ __forceinline__ void span_begin(DevSpan* s) {
+  if (s && threadIdx.x == 0) atomicCAS(&s->t0, 0ull, globaltimer_ns());
+}
+// every thread of the CTA (contains a __syncthreads)
+__device__ __forceinline__ void span_end(DevSpan* s) {
+  if (!s) return;
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&s->t1, globaltimer_ns());
+}
 K3Timing& k3_timing();
 inline void k3_timing_begin(cudaStream_t s) {
   if (k3_timing().start) cudaEventRecord(k3_timing().start, s);

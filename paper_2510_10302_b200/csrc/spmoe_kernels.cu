@@ -772,6 +772,11 @@ int spmoe_gather_rows(const void* src, const int32_t* idx, int n, int div, int64
   return launch_status();
 }
 
+int spmoe_k3_devtiming(void* span) {
+  k3_timing().dspan = span;
+  return 0;
+}
+
 int spmoe_k3_timing(void* start, void* end) {
   k3_timing().start = (cudaEvent_t)start;
   k3_timing().end = (cudaEvent_t)end;

@@ -98,12 +98,17 @@ struct spmoe_rt {
   cudaStream_t decode_stream = nullptr;
   // optional decode-kernel timing (spmoe_rt_decode_timing): event pairs
   // around each segment decode, with the bytes it read (blob) and wrote
-  bool time_decode = false;
+  int time_decode = 0;  // 1: event pairs, 2: device-clock spans
   struct DecodeTiming {
     cudaEvent_t a, b;
     int64_t bytes;
   };
   std::vector<DecodeTiming> dec_times;
+  // device-clock spans: a zeroed device ring of {t0, t1} (ns), one per
+  // timed launch, with the bytes each launch read + wrote
+  static constexpr int kSpanCap = 1 << 17;
+  unsigned long long* dspans = nullptr;
+  std::vector<int64_t> dspan_bytes;
   double dec_ms_acc = 0.0;  // resolved decode timings not yet reported
   int64_t dec_bytes_acc = 0, dec_n_acc = 0;
 
@@ -332,15 +337,22 @@ struct spmoe_rt {
       if (st == cudaSuccess) st = cudaEventRecord(full, copy_stream);
       if (st == cudaSuccess) st = cudaStreamWaitEvent(decode_stream, full, 0);
       DecodeTiming dt{nullptr, nullptr, 0};
-      if (st == cudaSuccess && time_decode) {
+      const int64_t dbytes = (int64_t)(hi - lo) + 2 * (int64_t)h->seg[g].n;
+      if (st == cudaSuccess && time_decode == 1) {
         dt.a = new_timing_event();
         dt.b = new_timing_event();
-        dt.bytes = (int64_t)(hi - lo) + 2 * (int64_t)h->seg[g].n;
+        dt.bytes = dbytes;
         st = cudaEventRecord(dt.a, decode_stream);
       }
+      void* span = nullptr;
+      if (time_decode == 2 && dspans && (int)dspan_bytes.size() < kSpanCap) {
+        span = dspans + 2 * dspan_bytes.size();
+        dspan_bytes.push_back(dbytes);
+      }
       if (st == cudaSuccess)
-        st = (cudaError_t)spmoe_xc_decode_segments((const uint8_t*)staging[i], h, g, 1, dst, decode_stream);
-      if (st == cudaSuccess && time_decode) {
+        st = (cudaError_t)spmoe_xc_decode_segments_timed((const uint8_t*)staging[i], h, g, 1, dst, decode_stream,
+                                                         span);
+      if (st == cudaSuccess && time_decode == 1) {
         st = cudaEventRecord(dt.b, decode_stream);
         dec_times.push_back(dt);
       }
@@ -398,7 +410,7 @@ struct spmoe_rt {
     }
     log_.push_back(std::move(tr));
     resolve_log();
-    if (time_decode) resolve_decode_timings();
+    if (time_decode == 1) resolve_decode_timings();
     note_error((int)st);
     return (int)st;
   }
@@ -551,6 +563,7 @@ void spmoe_rt_destroy(spmoe_rt* rt) {
     cudaEventDestroy(t.b);
   }
   for (auto e : rt->free_ev_) cudaEventDestroy(e);
+  if (rt->dspans) cudaFree(rt->dspans);
   if (rt->epoch_) cudaEventDestroy(rt->epoch_);
   delete rt;
 }
@@ -686,7 +699,14 @@ int spmoe_rt_set_codec(spmoe_rt* rt, size_t row_stride, void* staging, size_t st
 int spmoe_rt_decode_timing(spmoe_rt* rt, int enable) {
   if (!rt) return (int)cudaErrorInvalidValue;
   std::lock_guard<std::mutex> g(rt->mu_);
-  rt->time_decode = enable != 0;
+  if (enable < 0 || enable > 2) return (int)cudaErrorInvalidValue;
+  if (enable == 2 && !rt->dspans) {
+    const size_t bytes = sizeof(unsigned long long) * 2 * spmoe_rt::kSpanCap;
+    cudaError_t st = cudaMalloc((void**)&rt->dspans, bytes);
+    if (st == cudaSuccess) st = cudaMemset(rt->dspans, 0, bytes);
+    if (st != cudaSuccess) return (int)st;
+  }
+  rt->time_decode = enable;
   return 0;
 }
 
@@ -709,6 +729,20 @@ int spmoe_rt_decode_stats(spmoe_rt* rt, double* ms_out, int64_t* bytes_out, int6
     rt->recycle(t.b);
   }
   rt->dec_times.clear();
+  if (!rt->dspan_bytes.empty()) {
+    const size_t n2 = rt->dspan_bytes.size();
+    std::vector<unsigned long long> t(2 * n2);
+    if (rt->decode_stream) cudaStreamSynchronize(rt->decode_stream);
+    cudaMemcpy(t.data(), rt->dspans, sizeof(unsigned long long) * 2 * n2, cudaMemcpyDeviceToHost);
+    for (size_t i = 0; i < n2; ++i) {
+      if (t[2 * i] == 0 || t[2 * i + 1] < t[2 * i]) continue;
+      ms += (double)(t[2 * i + 1] - t[2 * i]) * 1e-6;
+      bytes += rt->dspan_bytes[i];
+      ++n;
+    }
+    cudaMemset(rt->dspans, 0, sizeof(unsigned long long) * 2 * n2);
+    rt->dspan_bytes.clear();
+  }
   if (ms_out) *ms_out = ms;
   if (bytes_out) *bytes_out = bytes;
   if (launches_out) *launches_out = n;

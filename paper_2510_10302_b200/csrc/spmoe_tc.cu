@@ -41,6 +41,7 @@ struct Params {
   uint16_t* h_out;  // up, split 1: [rows, F] bf16
   float* g_part;    // up, split > 1: [split][rows, F] fp32 (gate), then up
   float* y_part;    // down: [split][rows, H] fp32 (split 1: y itself)
+  DevSpan* span_end;  // optional device-clock span closed by this launch
   int E, H, F, rows, split;
   int slot[kMaxExperts];
 };
@@ -346,6 +347,7 @@ ffn_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
   }
+  span_end(p.span_end);
 }
 
 // ------------------------------------------------------------------ fused
@@ -558,11 +560,282 @@ ffn_tc_fused_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_con
   }
 }
 
+// ------------------------------------------------------------ unit-fused
+// ONE launch per K3 call, no grid-wide dependency: a work UNIT is (expert e,
+// 128-feature block m).  Its up part streams W1/W3 rows [128m, 128m+128)
+// over all of H and yields h[:, 128m:128m+128]; that h block is exactly
+// the K-slice of the down phase that W2[:, 128m:128m+128] multiplies, so
+// the same CTA runs the down part straight from shared memory (h never
+// round-trips through HBM or waits for other CTAs) and writes a partial y_m
+// per 128-row output tile; a PDL-chained second launch sums the F/128
+// partials of every element in a fixed order (its CTAs are resident and
+// waiting before this kernel ends).  (Letting the last unit of each tile
+// reduce it inside this kernel was measured 5-50x slower: the slowest CTA
+// ends up last on every tile and serialises all the reductions.)  An
+// expert's bits depend only on its own units, never on which experts share
+// the launch.
+// Tokens per expert <= 16 (one N=16 MMA): the SD verify regime.
+constexpr int UN = 16;  // tokens per unit (MMA N)
+
+struct UnitParams {
+  const int32_t* offsets;
+  uint16_t* h_out;      // [rows, F] bf16 (optional copy of h for callers/tests)
+  float* y_part;        // [F/128][rows, H] fp32 partials
+  int H, F, rows, n_active;
+  int active[kMaxExperts];
+  int slot[kMaxExperts];
+};
+
+template <int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_constant__ CUtensorMap map_x,
+                   const __grid_constant__ CUtensorMap map_wd, const UnitParams p) {
+  constexpr int A_BYTES = BM * BK * 2;                // 16 KB weight box
+  constexpr int X_BYTES = UN * BK * 2;                // 2 KB: 16 rows of x_perm x 64 features
+  constexpr int STAGE_BYTES = 2 * A_BYTES + X_BYTES;  // up: W1 + W3 + x; down: two W2 k-blocks
+  constexpr int HB_BYTES = UN * BK * 2;               // one 64-feature k-block of h (K-major, SW128)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* hb = smem + STAGES * STAGE_BYTES;  // h block as the down MMA's B operand: 2 x [16 x 64]
+  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], gu_full, h_ready, y_full[2], y_empty[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb_up = p.H / BK;
+  const int mt_up = p.F / BM;  // units per expert
+  const int mt_dn = p.H / BM;  // down M-tiles per unit
+  const int n_units = p.n_active * mt_up;
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&gu_full, 1);
+    mbar_init(&h_ready, 128);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&y_full[s], 1);
+      mbar_init(&y_empty[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_wu) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_wd) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+  }
+  if (warp == 1) {
+    // columns: g [0,16) | u [16,32) | y0 [32,48) | y1 [48,64)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(64));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer: per unit, the up stream then the
+      // W2 column block (weights never depend on h, so the down loads run
+      // ahead while the epilogue turns the up accumulators into h).  x_perm
+      // comes from the gather kernel this launch is PDL-chained to: the
+      // weight boxes of the first STAGES stages go out before waiting for it.
+      int stage = 0;
+      uint32_t phase = 0;
+      bool waited = false;
+      int pend_stage[STAGES], pend_kb[STAGES], pend_row[STAGES], npend = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int a = u / mt_up, m = u - a * mt_up;
+        const int e = p.active[a], slot = p.slot[a];
+        const int arow = p.offsets[e];
+        for (int kb = 0; kb < kb_up; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* st = smem + stage * STAGE_BYTES;
+          mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
+          tma_load_3d(st, &map_wu, &full_bar[stage], kb * BK, m * BM, slot);
+          tma_load_3d(st + A_BYTES, &map_wu, &full_bar[stage], kb * BK, p.F + m * BM, slot);
+          if (waited) {
+            tma_load_2d(st + 2 * A_BYTES, &map_x, &full_bar[stage], kb * BK, arow);
+          } else {
+            pend_stage[npend] = stage;
+            pend_kb[npend] = kb;
+            pend_row[npend] = arow;
+            if (++npend == STAGES || kb + 1 == kb_up) {
+              pdl_wait();
+              for (int i = 0; i < npend; ++i)
+                tma_load_2d(smem + pend_stage[i] * STAGE_BYTES + 2 * A_BYTES, &map_x, &full_bar[pend_stage[i]],
+                            pend_kb[i] * BK, pend_row[i]);
+              npend = 0;
+              waited = true;
+            }
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        for (int j = 0; j < mt_dn; ++j) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* st = smem + stage * STAGE_BYTES;
+          mbar_expect_tx(&full_bar[stage], 2 * A_BYTES);
+          tma_load_3d(st, &map_wd, &full_bar[stage], m * BM, j * BM, slot);
+          tma_load_3d(st + A_BYTES, &map_wd, &full_bar[stage], m * BM + BK, j * BM, slot);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+      if (!waited) pdl_wait();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      const uint32_t idesc = instr_desc(UN);
+      const uint32_t d_g = tmem_base, d_u = tmem_base + 16;
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, hphase = 0, aphase = 0;
+      const uint64_t hb0 = smem_desc_sw128(hb), hb1 = smem_desc_sw128(hb + HB_BYTES);
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        // up: g, u accumulators (free: the previous unit's down MMAs, issued
+        // after its h_ready, imply its epilogue has drained them)
+        for (int kb = 0; kb < kb_up; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          uint8_t* st = smem + stage * STAGE_BYTES;
+          const uint64_t a0 = smem_desc_sw128(st), a1 = smem_desc_sw128(st + A_BYTES);
+          const uint64_t b0 = smem_desc_sw128(st + 2 * A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+            umma(d_g, a0 + 2 * k, b0 + 2 * k, idesc, accum);
+            umma(d_u, a1 + 2 * k, b0 + 2 * k, idesc, accum);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&gu_full);
+        // down: B = this unit's h block from shared memory
+        mbar_wait(&h_ready, hphase);
+        hphase ^= 1;
+        tc_fence_after();
+        for (int j = 0; j < mt_dn; ++j) {
+          mbar_wait(&y_empty[acc], aphase ^ 1);
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          uint8_t* st = smem + stage * STAGE_BYTES;
+          const uint64_t a0 = smem_desc_sw128(st), a1 = smem_desc_sw128(st + A_BYTES);
+          const uint32_t d = tmem_base + 32 + 16 * acc;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) umma(d, a0 + 2 * k, hb0 + 2 * k, idesc, k > 0 ? 1u : 0u);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) umma(d, a1 + 2 * k, hb1 + 2 * k, idesc, 1u);
+          umma_commit(&empty_bar[stage]);
+          umma_commit(&y_full[acc]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++acc == 2) { acc = 0; aphase ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2..5, TMEM lane quarter q = warp % 4
+    const int q = warp & 3;
+    const int fl = 32 * q + lane;  // feature row within the unit (up), h row within the tile (down)
+    int acc = 0;
+    uint32_t gphase = 0, aphase = 0;
+    const int64_t plane = (int64_t)p.rows * p.H;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const int a = u / mt_up, m = u - a * mt_up;
+      const int e = p.active[a];
+      const int r0 = p.offsets[e];
+      const int ntok = min(UN, p.offsets[e + 1] - r0);
+      mbar_wait(&gu_full, gphase);
+      gphase ^= 1;
+      tc_fence_after();
+      float g[16], v[16];
+      const uint32_t lq = (uint32_t)(32 * q) << 16;
+      tmem_ld16(tmem_base + lq, g);
+      tmem_ld16(tmem_base + lq + 16, v);
+      tmem_wait_ld();
+      // h -> shared memory in the K-major 128B-swizzled layout the down
+      // MMA reads: k-block fl / 64, row = token, 16-byte chunk XOR row % 8
+      uint8_t* hk = hb + (fl >> 6) * HB_BYTES;
+      const int k = fl & 63;
+#pragma unroll
+      for (int n = 0; n < UN; ++n) {
+        const uint16_t hv = n < ntok ? f32_to_bf16(__fmul_rn(det_silu(g[n]), v[n])) : (uint16_t)0;
+        const uint32_t off = (uint32_t)((n >> 3) * 1024 + (n & 7) * 128 + ((((k >> 3) ^ (n & 7)) << 4)) + (k & 7) * 2);
+        *reinterpret_cast<uint16_t*>(hk + off) = hv;
+        if (p.h_out && n < ntok) p.h_out[(int64_t)(r0 + n) * p.F + m * BM + fl] = hv;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+      tc_fence_before();
+      mbar_arrive(&h_ready);
+      float* yp = p.y_part + (int64_t)m * plane;
+      for (int j = 0; j < mt_dn; ++j) {
+        mbar_wait(&y_full[acc], aphase);
+        tc_fence_after();
+        float y[16];
+        tmem_ld16(tmem_base + lq + 32 + 16 * acc, y);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&y_empty[acc]);
+        if (++acc == 2) { acc = 0; aphase ^= 1; }
+        const int col = j * BM + fl;
+#pragma unroll
+        for (int n = 0; n < UN; ++n)
+          if (n < ntok) __stcg(yp + (int64_t)(r0 + n) * p.H + col, y[n]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(64));
+  }
+}
+
+// y[r, :] = sum over the F/128 unit partials of r's expert, for the rows of
+// experts in `mask`.  Eight threads per output element each add a
+// contiguous eighth of the partials in order, then the eight sums combine
+// in a fixed tree (shuffles): deterministic, and the partials' loads are
+// in flight together.
+__global__ void reduce_units_kernel(const float* __restrict__ part, int nparts, int rows, int H,
+                                    const int32_t* __restrict__ offsets, int E, uint64_t mask,
+                                    float* __restrict__ y, DevSpan* span) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int64_t n = (int64_t)rows * H;
+  const int sub = threadIdx.x & 7;
+  const int per = (nparts + 7) / 8;
+  const int s0 = sub * per, s1 = min(nparts, s0 + per);
+  for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3; i0 < n;
+       i0 += ((int64_t)gridDim.x * blockDim.x) >> 3) {
+    const int r = (int)(i0 / H);
+    int e = 0;
+    while (e < E - 1 && r >= offsets[e + 1]) ++e;
+    const bool live = (mask >> e) & 1ull;  // uniform over the 8 lanes of an element
+    float s = 0.0f;
+    if (live && s0 < s1) {
+      float v[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) v[t] = (s0 + t < s1) ? __ldcg(part + (int64_t)(s0 + t) * n + i0) : 0.0f;
+      s = v[0];
+#pragma unroll
+      for (int t = 1; t < 16; ++t)
+        if (s0 + t < s1) s = __fadd_rn(s, v[t]);
+      for (int t = s0 + 16; t < s1; ++t) s = __fadd_rn(s, __ldcg(part + (int64_t)t * n + i0));
+    }
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+    s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+    if (live && sub == 0) y[i0] = s;
+  }
+  span_end(span);
+}
+
 // y[r, :] = sum_s y_part[s][r, :] in split order (deterministic), only for
 // rows of experts in this launch's mask (other rows keep their values).
 __global__ void reduce_split_kernel(const float* __restrict__ part, int split, int rows, int H,
                                     const int32_t* __restrict__ offsets, int E, uint64_t mask,
-                                    float* __restrict__ y) {
+                                    float* __restrict__ y, DevSpan* span) {
   pdl_launch_dependents();
   pdl_wait();
   const int64_t n = (int64_t)rows * H;
@@ -575,6 +848,7 @@ __global__ void reduce_split_kernel(const float* __restrict__ part, int split, i
     for (int k = 1; k < split; ++k) s = __fadd_rn(s, part[(int64_t)k * n + i]);
     y[i] = s;
   }
+  span_end(span);
 }
 
 // h[r, f] = bf16(silu(sum_s g) * sum_s u), split order, masked rows only.
@@ -601,7 +875,9 @@ __global__ void reduce_swiglu_kernel(const float* __restrict__ part, int split, 
 
 // x_perm[r] = x[perm[r]] (activation rows grouped by expert for TMA).
 __global__ void gather_rows_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ perm,
-                                   const int32_t* __restrict__ offsets, int E, int H, uint16_t* __restrict__ out) {
+                                   const int32_t* __restrict__ offsets, int E, int H, uint16_t* __restrict__ out,
+                                   DevSpan* span) {
+  span_begin(span);
   pdl_launch_dependents();  // launched normally: its inputs are complete
   const int rows = offsets[E];
   const int nch = H >> 3;
@@ -728,8 +1004,9 @@ extern "C" int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, con
     const uint64_t sa[1] = {(uint64_t)F * 2};
     if (!make_map(&ma_dn, h_scratch, 2, da, sa, BN)) return (int)cudaErrorInvalidValue;
   }
+  DevSpan* span = (DevSpan*)k3_timing().dspan;
   k3_timing_begin(s);
-  gather_rows_kernel<<<nsms, 256, 0, s>>>(x, perm_token, expert_offsets, E, H, x_perm);
+  gather_rows_kernel<<<nsms, 256, 0, s>>>(x, perm_token, expert_offsets, E, H, x_perm, span);
   p.split = split_up;
   st = launch<true, 5>(mw_up, ma_up, p, nsms, s);
   if (st) return st;
@@ -740,11 +1017,12 @@ extern "C" int spmoe_expert_ffn_tc(const uint16_t* pool, int64_t slot_elems, con
   }
   p.split = split_dn;
   p.y_part = split_dn > 1 ? workspace : y;
+  p.span_end = split_dn > 1 ? nullptr : span;
   st = launch<false, 8>(mw_dn, ma_dn, p, nsms, s);
   if (st) return st;
   if (split_dn > 1) {
     st = (int)launch_pdl(reduce_split_kernel, dim3(nsms * 4), dim3(256), 0, s, (const float*)workspace, split_dn,
-                         rows, H, expert_offsets, E, expert_mask, y);
+                         rows, H, expert_offsets, E, expert_mask, y, span);
   }
   k3_timing_end(s);
   return st;
@@ -808,7 +1086,7 @@ extern "C" int spmoe_expert_ffn_tc_fused(const uint16_t* pool, int64_t slot_elem
   }
   void* args[] = {(void*)&mwu, (void*)&mx, (void*)&mwd, (void*)&mh, (void*)&p, (void*)&grid_sync};
   k3_timing_begin(s);
-  gather_rows_kernel<<<nsms, 256, 0, s>>>(x, perm_token, expert_offsets, E, H, x_perm);
+  gather_rows_kernel<<<nsms, 256, 0, s>>>(x, perm_token, expert_offsets, E, H, x_perm, nullptr);
   st = (int)cudaMemsetAsync(grid_sync, 0, sizeof(uint32_t), s);
   if (st) return st;
   st = (int)cudaLaunchCooperativeKernel((const void*)ffn_tc_fused_kernel<STAGES>, dim3(nsms), dim3(kThreads), args,
@@ -816,8 +1094,78 @@ extern "C" int spmoe_expert_ffn_tc_fused(const uint16_t* pool, int64_t slot_elem
   if (st) return st;
   if (split_dn > 1) {
     st = (int)launch_pdl(reduce_split_kernel, dim3(nsms * 4), dim3(256), 0, s, (const float*)workspace, split_dn,
-                         rows, H, expert_offsets, E, expert_mask, y);
+                         rows, H, expert_offsets, E, expert_mask, y, (DevSpan*)nullptr);
   }
   k3_timing_end(s);
   return st;
+}
+
+extern "C" int spmoe_expert_ffn_tc_units(const uint16_t* pool, int64_t slot_elems, const int32_t* slot_of_expert,
+                                         uint64_t expert_mask, const uint16_t* x, int T, int H, int F, int E,
+                                         int k, const int32_t* expert_offsets, const int32_t* perm_token,
+                                         int max_tokens_per_expert, uint16_t* x_perm, uint16_t* h_scratch,
+                                         float* y, float* workspace, void* stream) {
+  using namespace tc;
+  if (!pool || !slot_of_expert || !expert_offsets || T < 0 || E < 1 || E > kMaxExperts || k < 1)
+    return (int)cudaErrorInvalidValue;
+  if (H % BM || F % BM || max_tokens_per_expert < 0 || max_tokens_per_expert > UN)
+    return (int)cudaErrorInvalidValue;
+  if (T == 0 || expert_mask == 0) return 0;
+  if (!x || !perm_token || !x_perm || !y || !workspace) return (int)cudaErrorInvalidValue;
+  cudaStream_t s = (cudaStream_t)stream;
+  int dev = 0, nsms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsms, cudaDevAttrMultiProcessorCount, dev);
+  const int rows = T * k;
+  UnitParams p{};
+  p.offsets = expert_offsets;
+  p.h_out = h_scratch;
+  p.y_part = workspace;
+  p.H = H;
+  p.F = F;
+  p.rows = rows;
+  int max_slot = 0;
+  for (int e = 0; e < E; ++e) {
+    if (!((expert_mask >> e) & 1ull)) continue;
+    p.active[p.n_active] = e;
+    p.slot[p.n_active] = slot_of_expert[e];
+    max_slot = max(max_slot, slot_of_expert[e]);
+    ++p.n_active;
+  }
+  CUtensorMap mwu, mx, mwd;
+  const uint64_t sb = (uint64_t)slot_elems * 2;
+  {
+    const uint64_t d[3] = {(uint64_t)H, (uint64_t)2 * F, (uint64_t)max_slot + 1};
+    const uint64_t str[2] = {(uint64_t)H * 2, sb};
+    if (!make_map(&mwu, pool, 3, d, str, BM)) return (int)cudaErrorInvalidValue;
+    const uint64_t da[2] = {(uint64_t)H, (uint64_t)rows};
+    const uint64_t sa[1] = {(uint64_t)H * 2};
+    if (!make_map(&mx, x_perm, 2, da, sa, UN)) return (int)cudaErrorInvalidValue;
+    const uint64_t d2[3] = {(uint64_t)F, (uint64_t)H, (uint64_t)max_slot + 1};
+    const uint64_t str2[2] = {(uint64_t)F * 2, sb};
+    if (!make_map(&mwd, pool + (int64_t)2 * F * H, 3, d2, str2, BM)) return (int)cudaErrorInvalidValue;
+  }
+  constexpr int STAGES = 6;
+  const size_t smem = (size_t)STAGES * (2 * BM * BK * 2 + UN * BK * 2) + 2 * UN * BK * 2 + 1024;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(ffn_tc_unit_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  const int units = p.n_active * (F / BM);
+  DevSpan* span = (DevSpan*)k3_timing().dspan;
+  k3_timing_begin(s);
+  gather_rows_kernel<<<nsms, 256, 0, s>>>(x, perm_token, expert_offsets, E, H, x_perm, span);
+  int st = (int)launch_pdl(ffn_tc_unit_kernel<STAGES>, dim3(min(units, nsms)), dim3(kThreads), smem, s, mwu, mx, mwd,
+                           p);
+  if (st) return st;
+  st = (int)launch_pdl(reduce_units_kernel, dim3(nsms * 2), dim3(256), 0, s, (const float*)workspace, F / BM, rows, H,
+                       expert_offsets, E, expert_mask, y, span);
+  k3_timing_end(s);
+  return st;
+}
+
+/* floats of workspace: the F/128 partial planes of [rows, H] */
+extern "C" int64_t spmoe_expert_ffn_tc_units_workspace_floats(int rows, int H, int F) {
+  return (int64_t)(F / 128) * rows * H;
 }

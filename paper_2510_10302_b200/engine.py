@@ -95,11 +95,12 @@ class _Scratch:
         # tcgen05 path workspaces: gathered routed rows, split-K partials
         kmax = max(k, 1)
         self.xp = torch.empty((T * kmax, H), dtype=bf, device=device)
-        from .kernels import tc_split, tc_workspace_floats
+        from .kernels import tc_split, tc_units_workspace_floats, tc_workspace_floats
 
         need = 1
         for f in (arch.ffn, arch.d_ffn, arch.shared_ffn or arch.ffn):
-            need = max(need, tc_workspace_floats(T * kmax, H, f, tc_split(H), tc_split(f)))
+            need = max(need, tc_workspace_floats(T * kmax, H, f, tc_split(H), tc_split(f)),
+                       tc_units_workspace_floats(T * kmax, H, f))
         self.ysplit = torch.empty((need,), dtype=f32, device=device)
         self.pw = torch.empty((T, 64), dtype=f32, device=device)
         self.pidx = torch.empty((T, 64), dtype=i32, device=device)
@@ -142,6 +143,7 @@ class SpecMoEEngine:
         cuda_graphs: bool = True,
         ffn_impl: str = "auto",
         tc_min_tokens: int | None = None,
+        k3_units: bool = True,
         expert_parallel: bool = False,
         ep_group=None,
         host_codec: str | None = "auto",
@@ -160,6 +162,9 @@ class SpecMoEEngine:
         if tc_min_tokens is None:
             tc_min_tokens = 1
         self.tc_min_tokens = tc_min_tokens
+        # verify-sized experts (<= 16 tokens) take the unit-fused tcgen05 K3
+        # (one launch for both phases); False keeps the two-phase one
+        self.k3_units = k3_units
         # test hook: treat every resident expert as late (one launch each), to
         # check that outputs do not depend on launch grouping
         self.force_late = False
@@ -297,7 +302,12 @@ class SpecMoEEngine:
         self._stall_done = {"prefetch": 0.0, "demand": 0.0}
         self._iters_done: list[tuple[float, float]] = []  # (draft ms, verify ms)
         self._k3_done: list[tuple[float, int, int, int]] = []  # (ms, bytes, experts, rows)
+        self._k3_ev_ms: list[float] = []  # CUDA-event durations (time_k3 == "events")
         self.k3_events = []
+        self._k3_spans = getattr(self, "_k3_spans", None)
+        if self._k3_spans is not None:
+            self._k3_spans.zero_()
+        self._k3_span_next = 0
         self._slots_done: list[ComputeSlot] = []
 
     @property
@@ -372,26 +382,33 @@ class SpecMoEEngine:
                 self.decisions.append(("task", layer, ids))
         self._pushed = []
 
-    def _use_tc(self, F: int, ntok: int) -> bool:
-        """Kernel for ONE expert with ``ntok`` routed tokens: tcgen05 unless
-        pinned to the CUDA-core (bit-exact) path or the expert has fewer than
-        ``tc_min_tokens`` tokens (default 1: every expert on tensor cores).
-        Decided per expert, never per launch, so an expert's output
-        bits do not depend on which experts happen to share its launch (that
-        depends on copy timing)."""
+    def _k3_path(self, F: int, ntok: int) -> str:
+        """Kernel for ONE expert with ``ntok`` routed tokens: "cc" (the
+        CUDA-core, bit-exact path: ``ffn_impl="cuda_core"`` or fewer than
+        ``tc_min_tokens`` tokens), "units" (the unit-fused tcgen05 kernel,
+        <= 16 tokens: the verify regime) or "tc" (the two-phase tcgen05
+        kernels, more tokens: prefill, large batches).  Decided per expert,
+        never per launch, so an expert's output bits do not depend on which
+        experts happen to share its launch (that depends on copy timing)."""
         if self.ffn_impl == "cuda_core" or self.arch.hidden % 128 or F % 128:
-            return False
-        return self.ffn_impl == "tcgen05" or ntok >= self.tc_min_tokens
+            return "cc"
+        if self.ffn_impl != "tcgen05" and ntok < self.tc_min_tokens:
+            return "cc"
+        return "units" if (self.k3_units and ntok <= K.UNIT_MAX_TOKENS) else "tc"
+
+    def _use_tc(self, F: int, ntok: int) -> bool:
+        return self._k3_path(F, ntok) != "cc"
 
     def _ffn(self, pool, slots, mask, xn, F, k, offsets, perm, h, y, maxtok, s: _Scratch, counts=None,
-             use_tc: bool | None = None) -> None:
-        """K3 for the experts in ``mask`` (all on one path: ``use_tc``, by
-        default chosen from ``maxtok``); ``counts`` = routed tokens of each of
-        those experts (host-known)."""
-        if use_tc is None:
-            use_tc = self._use_tc(F, maxtok)
-        if use_tc:
-            rows = xn.shape[0] * k
+             use_tc=None) -> None:
+        """K3 for the experts in ``mask``, all on one path (``use_tc``: a
+        :meth:`_k3_path` name, or by default the path of ``maxtok`` tokens);
+        ``counts`` = routed tokens of each of those experts (host-known)."""
+        path = use_tc if isinstance(use_tc, str) else self._k3_path(F, maxtok)
+        rows = xn.shape[0] * k
+        if path == "units":
+            K.expert_ffn_tc_units(pool, slots, mask, xn, F, k, offsets, perm, maxtok, s.xp[:rows], None, y, s.ysplit)
+        elif path == "tc":
             # launch-independent split: bits do not depend on launch grouping
             su, sd = K.tc_plan_static(self.arch.hidden, F, self.num_sms)
             K.expert_ffn_tc(pool, slots, mask, xn, F, k, offsets, perm, s.xp[:rows], h, y, s.ysplit, su, sd)
@@ -412,11 +429,11 @@ class SpecMoEEngine:
         roofline."""
         a = self.arch
         k = a.top_k if k is None else k
-        groups: dict[bool, list[int]] = {}
+        groups: dict[str, list[int]] = {}
         for e in experts:
-            groups.setdefault(self._use_tc(a.ffn, int(counts[e])), []).append(e)
-        for use_tc, grp in groups.items():
-            self._timed_ffn_group(grp, counts, slots, sum(1 << e for e in grp), xn, offsets, perm, s, k, use_tc)
+            groups.setdefault(self._k3_path(a.ffn, int(counts[e])), []).append(e)
+        for path, grp in groups.items():
+            self._timed_ffn_group(grp, counts, slots, sum(1 << e for e in grp), xn, offsets, perm, s, k, path)
 
     def _timed_ffn_group(self, experts, counts, slots, mask, xn, offsets, perm, s, k, use_tc) -> None:
         a = self.arch
@@ -425,16 +442,29 @@ class SpecMoEEngine:
         if not self.time_k3:
             self._ffn(self.pool, slots, mask, xn, a.ffn, k, offsets, perm, s.h, s.y, maxtok, s, cnt, use_tc)
             return
-        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ea.record()  # creates the events; the launcher re-records them
-        eb.record()
-        # the C launcher records ea right before its first kernel and eb after
-        # its last, so host-side launch preparation is not counted
-        self._lib.spmoe_k3_timing(ea.cuda_event, eb.cuda_event)
+        # device-clock span of the call (first kernel's first CTA start ->
+        # last kernel's last CTA end): CUDA events around launches are skewed
+        # by tens of microseconds while the host link is saturated
+        # (profiles/r2_event_skew_probe.txt); time_k3 == "events" also
+        # brackets the call with CUDA events for comparison
+        if self._k3_spans is None:
+            self._k3_spans = torch.zeros((1 << 16, 2), dtype=torch.int64, device=self.device)
+        slot = self._k3_span_next % self._k3_spans.shape[0]
+        self._k3_span_next += 1
+        self._lib.spmoe_k3_devtiming(self._k3_spans[slot].data_ptr())
+        ea = eb = None
+        if self.time_k3 == "events":
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record()  # creates the events; the launcher re-records them
+            eb.record()
+            # the C launcher records ea right before its first kernel and eb
+            # after its last, so host-side launch preparation is not counted
+            self._lib.spmoe_k3_timing(ea.cuda_event, eb.cuda_event)
         self._ffn(self.pool, slots, mask, xn, a.ffn, k, offsets, perm, s.h, s.y, maxtok, s, cnt, use_tc)
+        self._lib.spmoe_k3_devtiming(None)
         rows = int(sum(int(counts[e]) for e in experts))
         act = rows * (a.hidden * 2 + 2 * a.ffn * 2 + a.hidden * 4)  # x in, h out+in, y out
-        self.k3_events.append((ea, eb, len(experts) * a.expert_bytes + act, len(experts), rows))
+        self.k3_events.append((ea, eb, len(experts) * a.expert_bytes + act, len(experts), rows, slot))
 
     def k3_roofline(self) -> dict:
         """Average algorithmic bytes / launch-pair duration of the timed K3 calls."""
@@ -454,6 +484,8 @@ class SpecMoEEngine:
             "rows_per_launch": sum(x[3] for x in done) / len(ms),
             "total_ms": tot_ms,
             "by_shape": self._k3_by_shape(done),
+            "clock": "device globaltimer span per call (first CTA start -> last CTA end)",
+            "events_ms_per_launch": (sum(self._k3_ev_ms) / len(self._k3_ev_ms)) if self._k3_ev_ms else None,
         }
 
     def _k3_by_shape(self, done) -> dict:
@@ -922,8 +954,19 @@ class SpecMoEEngine:
         for s_ in self.stalls:
             self._stall_done[s_.kind] += s_.a.elapsed_time(s_.b)
         self.stalls = []
-        for ea, eb, byts, ne, rows in self.k3_events:
-            self._k3_done.append((ea.elapsed_time(eb), byts, ne, rows))
+        if self.k3_events:
+            n = min(self._k3_span_next, self._k3_spans.shape[0])
+            spans = self._k3_spans[:n].cpu().numpy()
+            self._k3_spans[:n].zero_()
+            for ea, eb, byts, ne, rows, slot in self.k3_events:
+                t0, t1 = int(spans[slot, 0]), int(spans[slot, 1])
+                if ea is not None:
+                    self._k3_ev_ms.append(ea.elapsed_time(eb))
+                if t0 > 0 and t1 >= t0:
+                    self._k3_done.append(((t1 - t0) / 1e6, byts, ne, rows))
+                elif ea is not None:  # a path without device spans (CUDA-core K3)
+                    self._k3_done.append((ea.elapsed_time(eb), byts, ne, rows))
+            self._k3_span_next = 0
         self.k3_events = []
         for e0, e1, e2 in self.iter_events:
             self._iters_done.append((e0.elapsed_time(e1), e1.elapsed_time(e2)))

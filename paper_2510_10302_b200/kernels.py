@@ -368,6 +368,66 @@ def expert_ffn_tc_fused(
     )
 
 
+UNIT_MAX_TOKENS = 16
+
+
+def tc_units_workspace_floats(rows: int, hidden: int, ffn_dim: int) -> int:
+    return (ffn_dim // 128) * rows * hidden
+
+
+def expert_ffn_tc_units(
+    pool: torch.Tensor,
+    slot_of_expert: Sequence[int],
+    expert_mask: int,
+    x: torch.Tensor,
+    ffn_dim: int,
+    top_k: int,
+    offsets: torch.Tensor,
+    perm: torch.Tensor,
+    max_tokens_per_expert: int,
+    x_perm: torch.Tensor,
+    h_scratch: torch.Tensor | None,
+    y: torch.Tensor,
+    workspace: torch.Tensor,
+    stream=None,
+) -> None:
+    """Unit-fused tcgen05 K3: one launch runs both phases per (expert,
+    128-feature block) unit, a PDL-chained one sums the partials in a fixed
+    order; experts with at most :data:`UNIT_MAX_TOKENS` routed tokens.
+    ``workspace``: f32 of :func:`tc_units_workspace_floats` elements."""
+    _need(pool, BF16, "pool", 2)
+    _need(x, BF16, "x", 2)
+    T, H = x.shape
+    E = len(slot_of_expert)
+    if max_tokens_per_expert > UNIT_MAX_TOKENS:
+        raise ValueError(f"expert_ffn_tc_units takes <= {UNIT_MAX_TOKENS} tokens per expert")
+    need = tc_units_workspace_floats(T * top_k, H, ffn_dim)
+    if workspace is None or workspace.numel() < need:
+        raise ValueError(f"tcgen05 unit workspace needs {need} floats")
+    LAUNCHES["count"] += 3
+    _native.call(
+        "spmoe_expert_ffn_tc_units",
+        pool.data_ptr(),
+        pool.shape[1],
+        _slot_array(slot_of_expert, E),
+        expert_mask,
+        x.data_ptr(),
+        T,
+        H,
+        ffn_dim,
+        E,
+        top_k,
+        offsets.data_ptr(),
+        perm.data_ptr(),
+        max_tokens_per_expert,
+        x_perm.data_ptr(),
+        _ptr(h_scratch),
+        y.data_ptr(),
+        workspace.data_ptr(),
+        _stream(stream),
+    )
+
+
 # ---------------------------------------------------------------------------
 # K4
 # ---------------------------------------------------------------------------

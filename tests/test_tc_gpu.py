@@ -107,3 +107,63 @@ def test_tc_static_plan_grouping_invariant(oracle, H, F):
     for got in (each, mixed):
         assert np.array_equal(got[0], one[0]) and np.array_equal(got[1], one[1])
     check(*one)
+
+
+def run_units(oracle, T, H, F, E, k, seed, masks=None):
+    """The unit-fused tcgen05 K3 (spmoe_expert_ffn_tc_units) vs the oracle."""
+    from paper_2510_10302_b200 import kernels as K
+
+    rng = np.random.default_rng(seed)
+    g = torch.Generator().manual_seed(seed)
+    x = torch.randn((T, H), generator=g).to(torch.bfloat16)
+    idx = np.stack([rng.choice(E, size=k, replace=False) for _ in range(T)]).astype(np.int32)
+    pool = torch.empty((E + 1, 3 * F * H), dtype=torch.bfloat16, device="cuda")
+    K.fill_normal_(pool, seed + 1, 0, 0.02)
+    slots = list(rng.permutation(E + 1)[:E])
+    off, perm, inv = K.moe_permute(torch.from_numpy(idx).cuda(), E)
+    n = T * k
+    counts = np.bincount(idx.ravel(), minlength=E)
+    xd = x.cuda()
+    xp = torch.empty((n, H), dtype=torch.bfloat16, device="cuda")
+    h = torch.zeros((n, F), dtype=torch.bfloat16, device="cuda")
+    y = torch.zeros((n, H), dtype=torch.float32, device="cuda")
+    ws = torch.zeros((K.tc_units_workspace_floats(n, H, F),), dtype=torch.float32, device="cuda")
+    for m in masks or [(1 << E) - 1]:
+        K.expert_ffn_tc_units(pool, slots, m, xd, F, k, off, perm, int(counts.max()), xp, h, y, ws)
+    torch.cuda.synchronize()
+    pool_h = bits(pool)
+    o2, p2, _ = oracle.moe_permute(idx, E)
+    h_ref, y_ref = oracle.expert_ffn([pool_h[slots[e]] for e in range(E)], bits(x), F, o2, p2)
+    return bits(h), bits(y), h_ref[:n], y_ref[:n]
+
+
+@pytest.mark.parametrize("T,H,F,E,k", [(5, 256, 512, 8, 2), (5, 4096, 14336, 8, 2), (2, 4096, 14336, 1, 1),
+                                       (9, 2048, 1408, 64, 6), (16, 256, 1024, 2, 2), (16, 2048, 5632, 1, 1)])
+def test_tc_units_matches_oracle(oracle, T, H, F, E, k):
+    """Unit-fused K3 within the tcgen05 tolerance at the configs' shapes,
+    including a lone Mixtral expert (the single-expert late launch) and
+    experts with the full 16 tokens."""
+    oracle.set_threads(16)
+    check(*run_units(oracle, T, H, F, E, k, seed=T + E + 1))
+
+
+@pytest.mark.parametrize("H,F", [(4096, 14336), (2048, 1408)])
+def test_tc_units_grouping_invariant(oracle, H, F):
+    """An expert's output bits do not depend on which experts share the
+    launch (every unit reduces only its own expert's partials)."""
+    E, k, T = 8, 2, 5
+    one = run_units(oracle, T, H, F, E, k, seed=31)
+    each = run_units(oracle, T, H, F, E, k, seed=31, masks=[1 << e for e in range(E)])
+    mixed = run_units(oracle, T, H, F, E, k, seed=31, masks=[0b00110101, 1 << 1, 1 << 3, 0b11000000])
+    for got in (each, mixed):
+        assert np.array_equal(got[0], one[0]) and np.array_equal(got[1], one[1])
+    check(*one)
+
+
+def test_tc_units_rejects_more_than_16_tokens():
+    from paper_2510_10302_b200 import kernels as K
+
+    pool = torch.empty((1, 3 * 512 * 256), dtype=torch.bfloat16, device="cuda")
+    x = torch.zeros((17, 256), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError):
+        K.expert_ffn_tc_units(pool, [0], 1, x, 512, 1, None, None, 17, x, None, x, None)

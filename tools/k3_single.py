@@ -40,6 +40,7 @@ def main(iters=20, gap_cycles=20000, Ts=(1, 2, 3, 4), impls=("tc", "tc_fused", "
         xp = torch.empty((T, H), dtype=torch.bfloat16, device=dev)
         su, sd = K.tc_plan_static(H, F)
         ws = torch.empty((max(1, K.tc_workspace_floats(T, H, F, su, sd)),), dtype=torch.float32, device=dev)
+        wsu = torch.zeros((K.tc_units_workspace_floats(T, H, F),), dtype=torch.float32, device=dev)
         act = T * (H * 2 + 2 * F * 2 + H * 4)
         row = {"T": T, "split": [su, sd], "gap_cycles": gap_cycles, "h2d": h2d}
         for name in impls:
@@ -67,6 +68,8 @@ def main(iters=20, gap_cycles=20000, Ts=(1, 2, 3, 4), impls=("tc", "tc_fused", "
                 a.record()
                 if name == "tc":
                     K.expert_ffn_tc(pool, [slot], 1, x, F, 1, off, perm, xp, h, y, ws, su, sd)
+                elif name == "tc_units":
+                    K.expert_ffn_tc_units(pool, [slot], 1, x, F, 1, off, perm, T, xp, None, y, wsu)
                 elif name == "tc_fused":
                     K.expert_ffn_tc_fused(pool, [slot], 1, x, F, 1, off, perm, xp, h, y, ws, sd, sync)
                 else:

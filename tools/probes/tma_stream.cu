@@ -16,6 +16,11 @@
 
 #include <cstdio>
 #include <cstdint>
+#include <initializer_list>
+#include <ctime>
+#include <cstring>
+#include <cstdlib>
+#include <sys/mman.h>
 
 constexpr int kCols = 4096;  // K (hidden)
 
@@ -32,11 +37,17 @@ __device__ __forceinline__ void wait_bar(uint64_t* b, uint32_t ph) {
 // mode 0: tensor boxes of BOXR rows; mode 1: bulk contiguous chunks
 template <int MODE, int BOXR, int S>
 __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ CUtensorMap map, const char* base,
-                                                       int tiles_per_cta, unsigned* sink) {
+                                                       int tiles_per_cta, unsigned* sink,
+                                                       unsigned long long* stamps) {
   constexpr int STAGE = BOXR * 64 * 2;
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[S], empty[S];
+  if (threadIdx.x == 0 && stamps) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(&stamps[0], t);
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&full[s])));
@@ -83,15 +94,36 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
       if (++stage == S) { stage = 0; ph ^= 1; }
     }
     if (acc == 0xdeadbeef) sink[0] = acc;
+    if (stamps) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(&stamps[1], t);
+    }
   }
+}
+
+__global__ void stamp_kernel(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
 }
 
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+// optional concurrent pinned H2D copy during every timed launch
+static void* g_h2d_src = nullptr;
+static void* g_h2d_dst = nullptr;
+static size_t g_h2d_bytes = 0;
+static cudaStream_t g_side = nullptr;
+static unsigned long long* g_stamps = nullptr;
+static bool g_graph = false;
+static float g_gap0 = 0, g_gap1 = 0;  // us: stamp kernel -> first CTA start, last CTA end -> stamp kernel  // launch the kernel as a pre-uploaded CUDA graph
+
 template <int MODE, int BOXR, int S>
-void run(const char* name, void* buf, size_t rows, unsigned* sink, EncodeFn enc) {
+void run(const char* name, void* buf, size_t rows, unsigned* sink, EncodeFn enc, int per_cta_mb = 8,
+         std::initializer_list<int> grids = {16, 32, 64, 112, 128, 148, 296}) {
   CUtensorMap map;
   cuuint64_t d[2] = {(cuuint64_t)kCols, (cuuint64_t)rows}, st[1] = {(cuuint64_t)kCols * 2};
   cuuint32_t box[2] = {64, (cuuint32_t)BOXR}, es[2] = {1, 1};
@@ -102,28 +134,63 @@ void run(const char* name, void* buf, size_t rows, unsigned* sink, EncodeFn enc)
   cudaFuncSetAttribute(stream_kernel<MODE, BOXR, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const size_t tile_bytes = (size_t)BOXR * kCols * 2;
   const int total_tiles = (int)(rows / BOXR);
-  for (int G : {16, 32, 64, 112, 128, 148, 296}) {
-    // each CTA streams 8 MB (or as many whole tiles as fit)
-    int tpc = (int)((8u << 20) / tile_bytes);
+  for (int G : grids) {
+    // each CTA streams per_cta_mb MB (or as many whole tiles as fit)
+    int tpc = (int)(((size_t)per_cta_mb << 20) / tile_bytes);
     if (tpc < 1) tpc = 1;
     if ((size_t)G * tpc > (size_t)total_tiles) tpc = total_tiles / G;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    float best = 1e30f;
+    float best = 1e30f, best_in = 1e30f;
     for (int rep = 0; rep < 5; ++rep) {
-      cudaEventRecord(a);
-      stream_kernel<MODE, BOXR, S><<<G, 64, smem>>>(map, (const char*)buf, tpc, sink);
-      cudaEventRecord(b);
+      unsigned long long init[2] = {~0ull, 0ull};
+      cudaMemcpy(g_stamps, init, sizeof(init), cudaMemcpyHostToDevice);
+      cudaDeviceSynchronize();
+      cudaGraphExec_t ge = nullptr;
+      cudaStream_t cs = nullptr;
+      if (g_graph) {
+        cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+        cudaGraph_t gr;
+        cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+        stream_kernel<MODE, BOXR, S><<<G, 64, smem, cs>>>(map, (const char*)buf, tpc, sink, g_stamps);
+        cudaStreamEndCapture(cs, &gr);
+        cudaGraphInstantiate(&ge, gr, 0);
+        cudaGraphUpload(ge, cs);
+        cudaStreamSynchronize(cs);
+        cudaGraphDestroy(gr);
+      }
+      if (g_h2d_bytes) {
+        cudaMemcpyAsync(g_h2d_dst, g_h2d_src, g_h2d_bytes, cudaMemcpyHostToDevice, g_side);
+        struct timespec ts2 = {0, 200000};
+        nanosleep(&ts2, nullptr);
+      }
+      cudaEventRecord(a, cs);
+      stamp_kernel<<<1, 1, 0, cs>>>(g_stamps + 2);
+      if (g_graph) cudaGraphLaunch(ge, cs);
+      else stream_kernel<MODE, BOXR, S><<<G, 64, smem, cs>>>(map, (const char*)buf, tpc, sink, g_stamps);
+      stamp_kernel<<<1, 1, 0, cs>>>(g_stamps + 3);
+      cudaEventRecord(b, cs);
       cudaEventSynchronize(b);
       float ms;
       cudaEventElapsedTime(&ms, a, b);
       if (ms < best) best = ms;
+      if (ge) cudaGraphExecDestroy(ge);
+      if (cs) cudaStreamDestroy(cs);
+      unsigned long long st[4];
+      cudaMemcpy(st, g_stamps, sizeof(st), cudaMemcpyDeviceToHost);
+      const float in_ms = (float)(st[1] - st[0]) / 1e6f;
+      if (in_ms < best_in) {
+        best_in = in_ms;
+        g_gap0 = (float)(st[0] - st[2]) / 1e3f;
+        g_gap1 = (float)(st[3] - st[1]) / 1e3f;
+      }
     }
     const double bytes = (double)G * tpc * tile_bytes;
     const int active = G > 148 ? 148 : G;
-    printf("%-8s S=%2d stage=%5d B  G=%3d  %8.1f GB/s  %6.1f GB/s/SM  (%.1f us)\n", name, S, STAGE, G,
-           bytes / best / 1e6, bytes / best / 1e6 / active, best * 1e3);
+    printf("%-8s S=%2d stage=%5d B  G=%3d  %2d MB/CTA  %8.1f GB/s  %6.1f GB/s/SM  (%.1f us events, %.1f us first CTA start -> last CTA end; gaps %.1f / %.1f us)\n",
+           name, S, STAGE, G, tpc * (int)(tile_bytes >> 20), bytes / best / 1e6, bytes / best / 1e6 / active, best * 1e3,
+           best_in * 1e3, g_gap0, g_gap1);
     cudaEventDestroy(a);
     cudaEventDestroy(b);
   }
@@ -131,7 +198,7 @@ void run(const char* name, void* buf, size_t rows, unsigned* sink, EncodeFn enc)
   if (e) printf("error %s\n", cudaGetErrorString(e));
 }
 
-int main() {
+int main(int argc, char** argv) {
   void* ptr = nullptr;
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q);
@@ -142,6 +209,84 @@ int main() {
   cudaMemset(buf, 1, rows * kCols * 2);
   unsigned* sink;
   cudaMalloc(&sink, 64);
+  cudaMalloc(&g_stamps, 32);
+  if (argc > 1 && !strcmp(argv[1], "h2dsrc")) {
+    // does the pinned source's page size change the penalty?  cudaMallocHost
+    // vs 2 MB-aligned THP-advised memory registered with cudaHostRegister vs
+    // hugetlbfs pages
+    system("cat /sys/kernel/mm/transparent_hugepage/enabled; grep -i huge /proc/meminfo");
+    g_h2d_bytes = 1ull << 30;
+    cudaMalloc(&g_h2d_dst, g_h2d_bytes);
+    cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking);
+    for (int kind = 0; kind < 3; ++kind) {
+      void* src = nullptr;
+      const char* nm = "";
+      if (kind == 0) {
+        cudaMallocHost(&src, g_h2d_bytes);
+        nm = "cudaMallocHost";
+      } else if (kind == 1) {
+        if (posix_memalign(&src, 2u << 20, g_h2d_bytes)) src = nullptr;
+        if (src) {
+          madvise(src, g_h2d_bytes, MADV_HUGEPAGE);
+          memset(src, 1, g_h2d_bytes);
+          if (cudaHostRegister(src, g_h2d_bytes, cudaHostRegisterPortable) != cudaSuccess) src = nullptr;
+        }
+        nm = "THP+cudaHostRegister";
+      } else {
+        src = mmap(nullptr, g_h2d_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_HUGETLB, -1, 0);
+        if (src == MAP_FAILED) src = nullptr;
+        if (src) {
+          memset(src, 1, g_h2d_bytes);
+          if (cudaHostRegister(src, g_h2d_bytes, cudaHostRegisterPortable) != cudaSuccess) src = nullptr;
+        }
+        nm = "hugetlb+cudaHostRegister";
+      }
+      if (!src) {
+        printf("# %s: unavailable\n", nm);
+        cudaGetLastError();
+        continue;
+      }
+      system("grep -i AnonHugePages /proc/meminfo");
+      g_h2d_src = src;
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, g_side);
+      cudaMemcpyAsync(g_h2d_dst, src, g_h2d_bytes, cudaMemcpyHostToDevice, g_side);
+      cudaEventRecord(b, g_side);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      printf("# source %s: H2D %.1f GB/s\n", nm, g_h2d_bytes / ms / 1e6);
+      run<0, 128, 8>("tile128", buf, rows, sink, enc, 3, {112});
+      run<0, 128, 8>("tile128", buf, rows, sink, enc, 8, {148});
+    }
+    return 0;
+  }
+  if (argc > 1 && !strcmp(argv[1], "h2d")) {
+    // the same streaming with a 1 GiB pinned H2D copy in flight
+    g_h2d_bytes = 1ull << 30;
+    cudaMallocHost(&g_h2d_src, g_h2d_bytes);
+    cudaMalloc(&g_h2d_dst, g_h2d_bytes);
+    cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking);
+    for (int pass = 0; pass < 4; ++pass) {
+      g_graph = pass >= 2;
+      printf("# concurrent H2D: %s, %s\n", pass & 1 ? "on" : "off", g_graph ? "CUDA graph launch" : "stream launch");
+      if (!(pass & 1)) g_h2d_bytes = 0; else g_h2d_bytes = 1ull << 30;
+      run<0, 128, 8>("tile128", buf, rows, sink, enc, 3, {112, 148});
+      run<0, 128, 8>("tile128", buf, rows, sink, enc, 8, {112, 148});
+      run<1, 128, 8>("bulk16k", buf, rows, sink, enc, 8, {148});
+    }
+    return 0;
+  }
+  if (argc > 1) {
+    // short streams: K3's single-expert up phase is 2 MB per CTA on 112 CTAs
+    for (int mb : {1, 2, 3, 4, 8}) {
+      run<0, 128, 8>("tile128", buf, rows, sink, enc, mb, {112, 148});
+      run<0, 128, 12>("tile128", buf, rows, sink, enc, mb, {112, 148});
+    }
+    return 0;
+  }
   run<0, 128, 4>("tile128", buf, rows, sink, enc);
   run<0, 128, 8>("tile128", buf, rows, sink, enc);
   run<0, 128, 12>("tile128", buf, rows, sink, enc);
