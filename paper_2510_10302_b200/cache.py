@@ -366,7 +366,10 @@ class NativeExpertCache:
         with CUDA events on the decode stream, falsy stops."""
         from . import _native
 
-        mode = {"device": 2, "events": 1}.get(enable, 1 if enable is True else int(enable or 0))
+        if isinstance(enable, str):
+            mode = {"device": 2, "events": 1}[enable]
+        else:
+            mode = 1 if enable is True else int(enable or 0)
         _native.check("spmoe_rt_decode_timing", self._lib.spmoe_rt_decode_timing(self._h, mode))
 
     def decode_stats(self) -> dict:
