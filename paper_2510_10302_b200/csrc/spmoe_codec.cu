@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -200,6 +201,7 @@ struct DecSeg {
 struct DecParams {
   DecSeg seg[SPMOE_XC_MAX_SEG];
   spmoe::DevSpan* span;  // optional device-clock timing of this launch
+  int stream_stores;     // evict-first (.cs) output stores (default; SPMOE_XC_STCS=0 disables, A/B switch)
 };
 
 // Exponents of one block, lane-major with a 33-word pitch (conflict-free
@@ -355,7 +357,10 @@ __global__ void __launch_bounds__(kDecThreads) xc_decode_kernel(const DecParams 
         const uint32_t ws = __byte_perm(smw, 0u, sel), we = __byte_perm(exw, 0u, sel);
         o[pr] = ((ws & 0x00800080u) << 8) | (ws & 0x007f007fu) | (we << 7);
       }
-      reinterpret_cast<uint4*>(dst)[it * 32 + lane] = make_uint4(o[0], o[1], o[2], o[3]);
+      if (p.stream_stores)
+        __stcs(reinterpret_cast<uint4*>(dst) + it * 32 + lane, make_uint4(o[0], o[1], o[2], o[3]));
+      else
+        reinterpret_cast<uint4*>(dst)[it * 32 + lane] = make_uint4(o[0], o[1], o[2], o[3]);
     }
     __syncwarp();
   }
@@ -617,6 +622,14 @@ int spmoe_xc_decode_segments_timed(const uint8_t* blob, const spmoe_xc_header* h
   DecParams p;
   std::memset(&p, 0, sizeof(p));
   p.span = (spmoe::DevSpan*)span;
+  static const int stcs = [] {
+    // evict-first output stores: in the SD loop 0.605 -> 0.624 of the copy
+    // peak and the concurrent multi-expert K3 launches 346 -> 320 us
+    // (tools/ab_stcs.sh, one box)
+    const char* v = getenv("SPMOE_XC_STCS");
+    return v && v[0] == '0' ? 0 : 1;
+  }();
+  p.stream_stores = stcs;
   uint16_t* d = dst;
   for (int i = 0; i < first; ++i) d += hdr->seg[i].n;
   uint32_t maxblk = 0;

@@ -29,6 +29,10 @@ def main(iters=20, gap_cycles=20000, Ts=(1, 2, 3, 4), impls=("tc", "tc_fused", "
     if h2d:  # a concurrent host->HBM copy in flight during every launch (the SD loop's situation)
         hsrc = torch.empty((244 << 20,), dtype=torch.uint8).pin_memory()
         hdst = torch.empty((244 << 20,), dtype=torch.uint8, device=dev)
+    from paper_2510_10302_b200 import _native
+
+    lib = _native.load()
+    spans = torch.zeros((iters + 3, 2), dtype=torch.int64, device=dev)
     out = []
     for T in Ts:
         g = torch.Generator().manual_seed(T)
@@ -65,6 +69,7 @@ def main(iters=20, gap_cycles=20000, Ts=(1, 2, 3, 4), impls=("tc", "tc_fused", "
                             hdst.copy_(hsrc, non_blocking=True)
                     torch.cuda._sleep(gap_cycles)  # busy gap
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                lib.spmoe_k3_devtiming(spans[i].data_ptr())
                 a.record()
                 if name == "tc":
                     K.expert_ffn_tc(pool, [slot], 1, x, F, 1, off, perm, xp, h, y, ws, su, sd)
@@ -77,9 +82,16 @@ def main(iters=20, gap_cycles=20000, Ts=(1, 2, 3, 4), impls=("tc", "tc_fused", "
                 b.record()
                 ms.append((a, b))
             torch.cuda.synchronize()
+            lib.spmoe_k3_devtiming(None)
             t = [a.elapsed_time(b) for a, b in ms[3:]]
             med = float(np.median(t))
             row[name] = {"us": round(med * 1e3, 1), "tbs": round((eb + act) / (med / 1e3) / 1e12, 3)}
+            sp = spans.cpu().numpy()[3:]
+            if (sp[:, 0] > 0).all():
+                dmed = float(np.median(sp[:, 1] - sp[:, 0])) / 1e3
+                row[name]["device_us"] = round(dmed, 1)
+                row[name]["device_tbs"] = round((eb + act) / (dmed / 1e6) / 1e12, 3)
+            spans.zero_()
         out.append(row)
         print(json.dumps(row), flush=True)
     return out
