@@ -122,7 +122,7 @@ def gpu_raw_expert(eng):
     return lambda l, e: eng.host_pool.raw_row(eng.host_pool.row_of(l, e), eng.device)
 
 
-def big_engine(arch_name, ffn_impl, model_state=None, N=4, budget=0.25, prompt=8):
+def big_engine(arch_name, ffn_impl, model_state=None, N=4, budget=0.25, prompt=8, capture=()):
     from paper_2510_10302_b200 import HardwareSpec, Policy, PolicySpec, ProfiledTimings
     from paper_2510_10302_b200.engine import SpecMoEEngine
     from paper_2510_10302_b200.model import get_arch
@@ -135,7 +135,7 @@ def big_engine(arch_name, ffn_impl, model_state=None, N=4, budget=0.25, prompt=8
     pol = PolicySpec(policy=Policy.DRAFT_PREFETCH, prefetch_k=pk, draft_length=N, acceptance_rate=1.0, seed=1234,
                      cutoff_layer=1, cache_capacity_experts=cap)
     return SpecMoEEngine(a, hw, t, pol, batch=1, record=True, ffn_impl=ffn_impl, max_tokens=prompt + 16,
-                         model_state=model_state)
+                         model_state=model_state, capture_layers=capture)
 
 
 def margins(lg):
@@ -174,11 +174,37 @@ def test_e2e_real_shapes(arch_name):
             remaining = [remaining[0] - sd.step(remaining)[0]]
         compare_exact(eng, sd)
         check_policy_replay(eng, state0)
-        # default (tcgen05) engine on the same model: first verify step
-        eng2 = big_engine(arch_name, "auto", model_state=eng.model_state)
+        # default (tcgen05, XC tier) engine on the same model, the bench's
+        # configuration: first verify step, with layer captures and replay
+        L = eng.arch.num_layers
+        eng2 = big_engine(arch_name, "auto", model_state=eng.model_state, capture=(0, L // 2, L - 1))
         eng2.prefill(P)
+        state2 = ([tuple(e) for e in eng2.cache.lru_order], [eng2.cache.slot_of(*e) for e in eng2.cache.lru_order])
         eng2.step()
         torch.cuda.synchronize()
+        raw = gpu_raw_expert(eng2)
+        a = eng2.arch
+        for c in (c for c in eng2.captures if "layer" in c):
+            l = c["layer"]
+            xn = bits(c["xn"])
+            w_o, idx_o, _, sg_o = O.router_topk(xn, bits(eng2.weights.layers[l].router), a.top_k, a.renorm,
+                                                bits(eng2.weights.layers[l].shared_gate)
+                                                if eng2.weights.layers[l].shared_gate is not None else None)
+            assert np.array_equal(bits(c["idx"]), idx_o), f"routing differs at layer {l}"
+            off, perm, inv = O.moe_permute(idx_o, a.num_experts)
+            used = sorted(set(idx_o.ravel().tolist()))
+            blobs = [raw(l, e) if e in used else None for e in range(a.num_experts)]
+            _, y = O.expert_ffn(blobs, xn, a.ffn, off, perm)
+            ys = None
+            if a.shared_ffn:
+                sh = bits(eng2.weights.layers[l].shared)[0]
+                o1 = np.array([0, xn.shape[0]], np.int32)
+                _, ys = O.expert_ffn([sh], xn, a.shared_ffn, o1, np.arange(xn.shape[0], dtype=np.int32))
+            out = O.moe_combine(y, inv, w_o, xn.shape[0], a.hidden, a.top_k, ys=ys, sg=sg_o,
+                                residual=bits(c["resid"]))
+            got, ref = O.bf16_bits_to_f32(bits(c["out"])), O.bf16_bits_to_f32(out)
+            assert np.abs(got - ref).max() <= 2.0 ** -7 * np.abs(ref).max(), f"verify-MoE output off at layer {l}"
+        check_policy_replay(eng2, state2)
         cap = next(c for c in eng2.captures if "accept_logits" in c)
         g = bits(cap["accept_logits"])[0]  # [N+1, V]
         draft = bits(cap["draft"])
