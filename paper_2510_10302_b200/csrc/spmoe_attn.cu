@@ -38,11 +38,22 @@ __global__ void __launch_bounds__(256) rms_norm_kernel(const uint16_t* __restric
   const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)warp * H);
   const int n8 = H / 8;
   float ss = 0.0f;
-  for (int c = lane; c < n8; c += 32) {
-    float a[8];
-    unpack8(xr[c], a);
+  // loads of U rounds in flight together; the FMA order is unchanged
+  constexpr int U = 8;
+  for (int c0 = lane; c0 < n8; c0 += 32 * U) {
+    uint4 xa[U];
 #pragma unroll
-    for (int v = 0; v < 8; ++v) ss = fmaf(a[v], a[v], ss);  // bf16 squares are exact
+    for (int u = 0; u < U; ++u)
+      if (c0 + 32 * u < n8) xa[u] = xr[c0 + 32 * u];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (c0 + 32 * u < n8) {
+        float a[8];
+        unpack8(xa[u], a);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) ss = fmaf(a[v], a[v], ss);  // bf16 squares are exact
+      }
+    }
   }
   ss = warp_sum_fixed(ss);
   const float r = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)H), eps)));

@@ -52,15 +52,59 @@ router_topk_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ 
     const uint16_t* wrow = (e < E) ? wg + (size_t)e * H : sg_w;
     const uint4* wr = reinterpret_cast<const uint4*>(wrow);
     float acc = 0.0f;
-    for (int c = lane; c < nchunks; c += 32) {
-      float a[8], b[8];
-      unpack8(__ldg(xr + c), a);
-      unpack8(__ldg(wr + c), b);
+    // the loads of U chunk rounds are issued before any of their FMAs (one
+    // memory round trip per U rounds instead of per round); the FMAs still
+    // run chunk j, j+32, j+64, ... in order -- the fixed-order contract
+    constexpr int U = 8;
+    for (int c0 = lane; c0 < nchunks; c0 += 32 * U) {
+      uint4 xa[U], wb[U];
 #pragma unroll
-      for (int v = 0; v < 8; ++v) acc = fmaf(a[v], b[v], acc);  // exact products
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + 32 * u;
+        if (c < nchunks) {
+          xa[u] = __ldg(xr + c);
+          wb[u] = __ldg(wr + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (c0 + 32 * u < nchunks) {
+          float a[8], b[8];
+          unpack8(xa[u], a);
+          unpack8(wb[u], b);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) acc = fmaf(a[v], b[v], acc);  // exact products
+        }
+      }
     }
     acc = warp_sum_fixed(acc);
     if (lane == 0) s_logit[e] = acc;
+  }
+  __syncthreads();
+  __shared__ int s_sel[kMaxExperts];
+  if (warp == 0) {
+    // top-k by warp argmax rounds: value descending, lowest index on ties
+    // (the strictly-greater scan of the oracle), E <= 256 = 8 per lane
+    uint32_t taken = 0;  // bit j: expert lane + 32 j already selected
+    for (int i = 0; i < k; ++i) {
+      float bv = 0.0f;
+      int best = -1;
+      for (int j = 0; j < (E + 31) / 32; ++j) {
+        const int e = lane + 32 * j;
+        if (e < E && !(taken & (1u << j))) {
+          const float v = s_logit[e];
+          if (best < 0 || v > bv) { best = e; bv = v; }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const float ov = __shfl_xor_sync(SPMOE_FULL_MASK, bv, o);
+        const int oe = __shfl_xor_sync(SPMOE_FULL_MASK, best, o);
+        if (oe >= 0 && (best < 0 || ov > bv || (ov == bv && oe < best))) { best = oe; bv = ov; }
+      }
+      if ((best & 31) == lane) taken |= 1u << (best >> 5);
+      if (lane == 0) s_sel[i] = best;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -68,20 +112,7 @@ router_topk_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ 
       for (int e = 0; e < E; ++e) logits_out[(size_t)t * E + e] = s_logit[e];
     if (sg_w != nullptr && shared_gate != nullptr)
       shared_gate[t] = __fdiv_rn(1.0f, __fadd_rn(1.0f, det_exp(-s_logit[E])));
-    // top-k selection: strictly-greater scan keeps the lowest index on ties
-    int sel[kMaxExperts];
-    uint32_t taken[kMaxExperts / 32] = {0};
-    for (int i = 0; i < k; ++i) {
-      int best = -1;
-      float bv = 0.0f;
-      for (int e = 0; e < E; ++e) {
-        if (taken[e >> 5] & (1u << (e & 31))) continue;
-        const float v = s_logit[e];
-        if (best < 0 || v > bv) { best = e; bv = v; }
-      }
-      sel[i] = best;
-      taken[best >> 5] |= 1u << (best & 31);
-    }
+    const int* sel = s_sel;
     const float m = s_logit[sel[0]];
     float sum = 0.0f;
     if (renorm) {
@@ -361,11 +392,22 @@ struct LinParams {
 // r = 1 / sqrt(ss / H + eps) with IEEE division and square root.
 __device__ __forceinline__ float rms_scale_row(const uint4* xr, int nchunks, int H, float eps, int lane) {
   float acc = 0.0f;
-  for (int c = lane; c < nchunks; c += 32) {
-    float a[8];
-    unpack8(__ldg(xr + c), a);
+  // loads of U rounds issued before their FMAs; FMA order unchanged
+  constexpr int U = 8;
+  for (int c0 = lane; c0 < nchunks; c0 += 32 * U) {
+    uint4 xa[U];
 #pragma unroll
-    for (int v = 0; v < 8; ++v) acc = fmaf(a[v], a[v], acc);  // exact squares
+    for (int u = 0; u < U; ++u)
+      if (c0 + 32 * u < nchunks) xa[u] = __ldg(xr + c0 + 32 * u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (c0 + 32 * u < nchunks) {
+        float a[8];
+        unpack8(xa[u], a);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc = fmaf(a[v], a[v], acc);  // exact squares
+      }
+    }
   }
   acc = warp_sum_fixed(acc);
   const float mean = __fdiv_rn(acc, (float)H);
