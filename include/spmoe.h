@@ -315,34 +315,41 @@ int spmoe_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, uint64_t off
 /*   weight is sign(1) | exponent(8) | mantissa(7); the exponent of      */
 /*   trained or N(0, s^2) weights has ~2.5 bits of entropy.  XC stores   */
 /*   each value as one sign|mantissa byte                                */
-/*   and the exponent as a per-segment canonical Huffman code (<= 12     */
-/*   bits, 32 independent lane substreams per 4096-value block so a warp */
-/*   decodes a block in parallel).  Decoding is exact: decode(encode(x)) */
-/*   == x bit for bit.  Per-value coding only: no cross-value or         */
+/*   and the exponent as a 4-bit symbol (its offset from the segment's   */
+/*   base exponent, 15 = escape) in a per-segment canonical Huffman code */
+/*   (<= 12 bits, 32 independent lane substreams per 4096-value block so */
+/*   a warp decodes a block in parallel); escaped exponents travel in a  */
+/*   per-block exception list.  Decoding is exact: decode(encode(x)) ==  */
+/*   x bit for bit.  Per-value coding only: no cross-value or            */
 /*   cross-expert modelling.                                             */
 /* --------------------------------------------------------------------- */
-#define SPMOE_XC_MAGIC 0x33435853u /* "SXC3" */
+#define SPMOE_XC_MAGIC 0x34435853u /* "SXC4" */
 #define SPMOE_XC_BLOCK 4096        /* values per coding block */
 #define SPMOE_XC_LANES 32          /* exponent substreams per block */
-#define SPMOE_XC_LMAX 12           /* longest exponent code, bits */
+#define SPMOE_XC_LMAX 12           /* longest symbol code, bits */
+#define SPMOE_XC_NSYM 16           /* 15 in-window offsets + escape */
 #define SPMOE_XC_MAX_SEG 4
 
 /*
  * One segment = one weight matrix of n bf16 values (n % SPMOE_XC_BLOCK == 0),
- * nb = n / SPMOE_XC_BLOCK blocks.  Exponents are coded with the segment's
- * canonical Huffman code, lengths len[] (1..SPMOE_XC_LMAX, 0 = exponent
- * absent) built deterministically from the exponent histogram (two-queue
- * Huffman, ties to leaves and lower ids; lengths over LMAX capped and the
- * Kraft excess repaid by lengthening the longest codes under LMAX, rarest
- * then highest id first; codes assigned in (length, exponent) order).
+ * nb = n / SPMOE_XC_BLOCK blocks.  base = the lowest exponent b <= 240 whose
+ * window [b, b + 14] holds the most values (ties: lowest b); exponent e
+ * codes as symbol e - base inside the window, else as the escape symbol 15.
+ * Symbols are coded with the segment's canonical Huffman code, lengths
+ * len[16] (1..SPMOE_XC_LMAX, 0 = symbol absent) built deterministically from
+ * the symbol histogram (two-queue Huffman, ties to leaves and lower ids;
+ * lengths over LMAX capped and the Kraft excess repaid by lengthening the
+ * longest codes under LMAX, rarest then highest id first; codes assigned in
+ * (length, symbol) order).
  * Streams (byte offsets from the blob start, each 256-byte aligned, in this
  * order, so a segment's bytes are contiguous from its off_lut):
  *   lut   [4096]    u32  multi-symbol decode table: entry p (the next 12
- *                        code bits, LSB first) = up to three whole codes,
- *                        sym0 | sym1 << 8 | sym2 << 16 | count << 24 |
- *                        bits << 26 (count >= 1: an unused pattern of an
- *                        incomplete code advances one bit); derived from
- *                        len[] at encode time, so a decoder loads it
+ *                        code bits, LSB first) = up to five whole codes,
+ *                        sym_i << 4 i (i < 5) | 4 count << 20 |
+ *                        bits << 25 (count >= 1: an unused pattern of an
+ *                        incomplete code advances one bit as symbol 0);
+ *                        derived from len[] at encode time, so a decoder
+ *                        loads it
  *   sm    [n]       u8   (v >> 8 & 0x80) | (v & 0x7f)
  *   ex    [ex_words] u32 per block, SPMOE_XC_LANES lane substreams back to
  *                        back; lane l holds the bit-reversed codes of values
@@ -351,14 +358,18 @@ int spmoe_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, uint64_t off
  *                        the stream)
  *   bofs  [nb+1]    u32  first ex word of each block (exclusive prefix)
  *   lanes [nb*32]   u8   word count of each lane substream
+ *   xofs  [nb+1]    u32  first exception of each block (exclusive prefix)
+ *   xrec  [n_exc]   u32  escaped values in value order: index in block << 8
+ *                        | exponent
  * Every bf16 bit pattern round-trips (zeros, denormals, inf, NaN).
  */
 typedef struct spmoe_xc_segment {
   uint64_t n;
-  uint64_t off_lut, off_sm, off_ex, off_bofs, off_lanes;
-  uint32_t ex_words, pad;
-  uint8_t len[256];
-} spmoe_xc_segment; /* 312 bytes */
+  uint64_t off_lut, off_sm, off_ex, off_bofs, off_lanes, off_xofs, off_xrec;
+  uint32_t ex_words, n_exc;
+  uint32_t base, pad;
+  uint8_t len[SPMOE_XC_NSYM];
+} spmoe_xc_segment; /* 96 bytes */
 
 typedef struct spmoe_xc_header {
   uint32_t magic; /* SPMOE_XC_MAGIC */
@@ -366,13 +377,13 @@ typedef struct spmoe_xc_header {
   uint64_t blob_bytes; /* header + streams (what crosses the host link) */
   uint64_t raw_bytes;  /* 2 * sum(n) */
   spmoe_xc_segment seg[SPMOE_XC_MAX_SEG];
-} spmoe_xc_header; /* 1272 bytes; the first stream starts at 1280 */
+} spmoe_xc_header; /* 408 bytes; the first stream starts at 512 */
 
 /* Device workspace bytes spmoe_xc_plan needs for these segments. */
 size_t spmoe_xc_work_bytes(int nseg, const int64_t* seg_n);
 /*
  * Encoder step 1 (synchronous on `stream`): histogram each segment's
- * exponents, choose its code tables, count each block's escape words and
+ * exponents, choose its base and code, count each block's code words and
  * exceptions, and fill *hdr (host) with the blob layout.  src: the nseg
  * segments back to back on the device.  work: device, spmoe_xc_work_bytes.
  * Returns 1 (invalid value) if a segment size is not a multiple of

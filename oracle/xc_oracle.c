@@ -1,6 +1,6 @@
 /*
  * xc_oracle.c — CPU ORACLE of the XC expert-blob codec (include/spmoe.h,
- * "XC", format SXC3).  TEST INFRASTRUCTURE ONLY: tests/ compare the sm_100a
+ * "XC", format SXC4).  TEST INFRASTRUCTURE ONLY: tests/ compare the sm_100a
  * encoder's blob byte for byte against oracle_xc_encode and the decoder's
  * output against the original bits; the product path never links this file.
  *
@@ -9,16 +9,21 @@
  * reference golden vector; parity is pinned by the format's own invariant
  * decode(encode(x)) == x (checked here on CPU too) and by GPU == CPU blob
  * bytes.  Straight-line scalar code in value order:
- *   code   exponent histogram -> two-queue Huffman lengths (ties: leaves
+ *   base   the lowest b <= 240 whose exponent window [b, b+14] holds the
+ *          most values; exponent e -> symbol e - b inside it, else 15
+ *          (escape, the exponent goes to the block's exception list);
+ *   code   symbol histogram -> two-queue Huffman lengths (ties: leaves
  *          before internal nodes, lower ids first) -> lengths capped at
  *          SPMOE_XC_LMAX with the Kraft excess repaid by lengthening the
  *          longest sub-LMAX code (rarest, then highest id) -> canonical
- *          codes in (length, exponent) order, written bit-reversed (LSB
+ *          codes in (length, symbol) order, written bit-reversed (LSB
  *          first);
  *   block  4096 values: sign|mantissa bytes; 32 lane substreams of the
  *          codes of values 128 l .. 128 l + 127, each padded to a word;
- *   layout header at 0, streams from 1280 on 256-byte boundaries in the
- *          order lut (multi-symbol, u32), sm, ex (+ 8 slack bytes), bofs, lanes per segment.
+ *          exception records (index << 8 | exponent) in value order;
+ *   layout header at 0, streams from 512 on 256-byte boundaries in the
+ *          order lut (multi-symbol, u32), sm, ex (+ 8 slack bytes), bofs,
+ *          lanes, xofs, xrec per segment.
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -28,14 +33,33 @@
 
 #define LMAX SPMOE_XC_LMAX
 #define LANES SPMOE_XC_LANES
+#define NSYM SPMOE_XC_NSYM
+#define ESC (NSYM - 1)
 #define PER_LANE (SPMOE_XC_BLOCK / LANES)
 
 static uint64_t a256(uint64_t x) { return (x + 255) & ~(uint64_t)255; }
 
-void oracle_xc_code_lengths(const uint64_t cnt[256], uint8_t len[256]) {
-  memset(len, 0, 256);
-  int sym[256], n = 0;
-  for (int s = 0; s < 256; ++s)
+/* The segment's base exponent from its exponent histogram. */
+uint32_t oracle_xc_base(const uint64_t hist[256]) {
+  uint32_t best = 0;
+  uint64_t best_mass = 0;
+  for (uint32_t b = 0; b + ESC <= 255 && b <= 240; ++b) {
+    uint64_t m = 0;
+    for (uint32_t e = b; e < b + ESC; ++e) m += hist[e];
+    if (m > best_mass) {
+      best_mass = m;
+      best = b;
+    }
+  }
+  return best;
+}
+
+static int sym_of(int e, uint32_t base) { return (e >= (int)base && e < (int)base + ESC) ? e - (int)base : ESC; }
+
+void oracle_xc_code_lengths(const uint64_t cnt[NSYM], uint8_t len[NSYM]) {
+  memset(len, 0, NSYM);
+  int sym[NSYM], n = 0;
+  for (int s = 0; s < NSYM; ++s)
     if (cnt[s]) sym[n++] = s;
   if (n == 0) return;
   if (n == 1) {
@@ -51,8 +75,8 @@ void oracle_xc_code_lengths(const uint64_t cnt[256], uint8_t len[256]) {
     }
     sym[j + 1] = x;
   }
-  uint64_t w[511];
-  int parent[511], depth[511];
+  uint64_t w[2 * NSYM];
+  int parent[2 * NSYM], depth[2 * NSYM];
   for (int i = 0; i < n; ++i) w[i] = cnt[sym[i]];
   int li = 0, ii = n, next = n;
   for (int k = 0; k < n - 1; ++k) {
@@ -70,20 +94,19 @@ void oracle_xc_code_lengths(const uint64_t cnt[256], uint8_t len[256]) {
   for (int v = root - 1; v >= 0; --v) depth[v] = depth[parent[v]] + 1;
   int maxlen = 0;
   for (int i = 0; i < n; ++i) {
-    const int d = depth[i];
-    len[sym[i]] = (uint8_t)(d > 255 ? 255 : d);
-    if (d > maxlen) maxlen = d;
+    len[sym[i]] = (uint8_t)depth[i];
+    if (depth[i] > maxlen) maxlen = depth[i];
   }
   if (maxlen <= LMAX) return;
   int64_t kraft = 0;
-  for (int s = 0; s < 256; ++s) {
+  for (int s = 0; s < NSYM; ++s) {
     if (!len[s]) continue;
     if (len[s] > LMAX) len[s] = LMAX;
     kraft += (int64_t)1 << (LMAX - len[s]);
   }
   while (kraft > ((int64_t)1 << LMAX)) {
     int best = -1;
-    for (int s = 0; s < 256; ++s) {
+    for (int s = 0; s < NSYM; ++s) {
       if (!len[s] || len[s] >= LMAX) continue;
       if (best < 0 || len[s] > len[best] ||
           (len[s] == len[best] && (cnt[s] < cnt[best] || (cnt[s] == cnt[best] && s > best))))
@@ -95,12 +118,12 @@ void oracle_xc_code_lengths(const uint64_t cnt[256], uint8_t len[256]) {
 }
 
 /* canonical codes, bit-reversed for LSB-first packing */
-static void rev_codes(const uint8_t len[256], uint16_t rev[256]) {
-  memset(rev, 0, 512);
+static void rev_codes(const uint8_t len[NSYM], uint16_t rev[NSYM]) {
+  memset(rev, 0, sizeof(uint16_t) * NSYM);
   uint32_t code = 0;
   int prev = 0;
   for (int L = 1; L <= LMAX; ++L)
-    for (int s = 0; s < 256; ++s) {
+    for (int s = 0; s < NSYM; ++s) {
       if (len[s] != L) continue;
       if (prev) code <<= (L - prev);
       prev = L;
@@ -111,39 +134,35 @@ static void rev_codes(const uint8_t len[256], uint16_t rev[256]) {
     }
 }
 
-void oracle_xc_lut(const uint8_t len[256], uint16_t lut[1 << LMAX]) {
-  uint16_t rev[256];
+/* single-symbol table: entry q (12 peeked bits) = symbol | length << 8 */
+void oracle_xc_lut(const uint8_t len[NSYM], uint16_t lut[1 << LMAX]) {
+  uint16_t rev[NSYM];
   rev_codes(len, rev);
   memset(lut, 0, sizeof(uint16_t) << LMAX);
-  for (int s = 0; s < 256; ++s) {
+  for (int s = 0; s < NSYM; ++s) {
     const int L = len[s];
     if (!L) continue;
     for (uint32_t q = 0; q < (1u << (LMAX - L)); ++q) lut[rev[s] | (q << L)] = (uint16_t)(s | (L << 8));
   }
 }
 
-/* Multi-symbol table from the single-symbol one (restates the derivation
- * in xc_lut2_of, paper_2510_10302_b200/csrc/spmoe_codec.cu): entry q = up to
- * three whole codes that fit in the 12 peeked bits.  An unused pattern of
- * an incomplete code (length 0) still advances by one bit. */
+/* Multi-symbol table from the single-symbol one (restates lut2_of in
+ * paper_2510_10302_b200/csrc/spmoe_codec.cu): entry q = up to five whole
+ * codes that fit in the 12 peeked bits.  An unused pattern of an
+ * incomplete code (length 0) still advances by one bit. */
 void oracle_xc_lut2(const uint16_t lut[1 << LMAX], uint32_t lut2[1 << LMAX]) {
   for (uint32_t q = 0; q < (1u << LMAX); ++q) {
     const uint32_t e0 = lut[q];
-    uint32_t tot = e0 >> 8, cnt = 1, syms = e0 & 0xffu;
+    uint32_t tot = e0 >> 8, cnt = 1, syms = e0 & 0xfu;
     if (tot == 0) tot = 1;
-    const uint32_t e1 = lut[q >> tot], l1 = e1 >> 8;
-    if (l1 && tot + l1 <= LMAX) {
-      syms |= (e1 & 0xffu) << 8;
-      cnt = 2;
-      tot += l1;
-      const uint32_t e2 = lut[q >> tot], l2 = e2 >> 8;
-      if (l2 && tot + l2 <= LMAX) {
-        syms |= (e2 & 0xffu) << 16;
-        cnt = 3;
-        tot += l2;
-      }
+    while (cnt < 5) {
+      const uint32_t e = lut[q >> tot], l = e >> 8;
+      if (!l || tot + l > LMAX) break;
+      syms |= (e & 0xfu) << (4 * cnt);
+      ++cnt;
+      tot += l;
     }
-    lut2[q] = syms | (cnt << 24) | (tot << 26);
+    lut2[q] = syms | ((4 * cnt) << 20) | (tot << 25);
   }
 }
 
@@ -159,24 +178,29 @@ uint64_t oracle_xc_encode(const uint16_t* src, int nseg, const int64_t* seg_n, u
   memset(&hdr, 0, sizeof(hdr));
   hdr.magic = SPMOE_XC_MAGIC;
   hdr.nseg = (uint32_t)nseg;
-  uint16_t revs[SPMOE_XC_MAX_SEG][256];
-  /* pass 1: codes, sizes, layout */
+  uint16_t revs[SPMOE_XC_MAX_SEG][NSYM];
+  /* pass 1: base, codes, sizes, layout */
   const uint16_t* s = src;
   uint64_t pos = a256(sizeof(spmoe_xc_header)), raw = 0;
   for (int i = 0; i < nseg; ++i) {
     spmoe_xc_segment* g = &hdr.seg[i];
     const int64_t n = seg_n[i], nb = n / SPMOE_XC_BLOCK;
-    uint64_t cnt[256];
+    uint64_t hist[256], cnt[NSYM];
+    memset(hist, 0, sizeof(hist));
     memset(cnt, 0, sizeof(cnt));
-    for (int64_t k = 0; k < n; ++k) cnt[(s[k] >> 7) & 0xff]++;
+    for (int64_t k = 0; k < n; ++k) hist[(s[k] >> 7) & 0xff]++;
+    g->base = oracle_xc_base(hist);
+    for (int e = 0; e < 256; ++e) cnt[sym_of(e, g->base)] += hist[e];
     oracle_xc_code_lengths(cnt, g->len);
     rev_codes(g->len, revs[i]);
     g->n = (uint64_t)n;
+    g->n_exc = (uint32_t)cnt[ESC];
     uint64_t words = 0;
     for (int64_t b = 0; b < nb; ++b)
       for (int l = 0; l < LANES; ++l) {
         uint64_t bits = 0;
-        for (int j = 0; j < PER_LANE; ++j) bits += g->len[(s[b * SPMOE_XC_BLOCK + l * PER_LANE + j] >> 7) & 0xff];
+        for (int j = 0; j < PER_LANE; ++j)
+          bits += g->len[sym_of((s[b * SPMOE_XC_BLOCK + l * PER_LANE + j] >> 7) & 0xff, g->base)];
         words += (bits + 31) / 32;
       }
     g->ex_words = (uint32_t)words;
@@ -185,6 +209,8 @@ uint64_t oracle_xc_encode(const uint16_t* src, int nseg, const int64_t* seg_n, u
     g->off_ex = pos; pos = a256(pos + words * 4 + 8);
     g->off_bofs = pos; pos = a256(pos + (uint64_t)(nb + 1) * 4);
     g->off_lanes = pos; pos = a256(pos + (uint64_t)nb * LANES);
+    g->off_xofs = pos; pos = a256(pos + (uint64_t)(nb + 1) * 4);
+    g->off_xrec = pos; pos = a256(pos + (uint64_t)g->n_exc * 4);
     raw += 2 * (uint64_t)n;
     s += n;
   }
@@ -206,9 +232,12 @@ uint64_t oracle_xc_encode(const uint16_t* src, int nseg, const int64_t* seg_n, u
     uint32_t* ex = (uint32_t*)(out + g->off_ex);
     uint32_t* bofs = (uint32_t*)(out + g->off_bofs);
     uint8_t* lanes = out + g->off_lanes;
-    uint32_t w = 0;
+    uint32_t* xofs = (uint32_t*)(out + g->off_xofs);
+    uint32_t* xrec = (uint32_t*)(out + g->off_xrec);
+    uint32_t w = 0, x = 0;
     for (int64_t b = 0; b < nb; ++b) {
       bofs[b] = w;
+      xofs[b] = x;
       for (int l = 0; l < LANES; ++l) {
         uint64_t buf = 0;
         int nbits = 0;
@@ -216,10 +245,11 @@ uint64_t oracle_xc_encode(const uint16_t* src, int nseg, const int64_t* seg_n, u
         for (int j = 0; j < PER_LANE; ++j) {
           const int64_t k = b * SPMOE_XC_BLOCK + l * PER_LANE + j;
           const uint16_t v = s[k];
-          const int e = (v >> 7) & 0xff;
+          const int e = (v >> 7) & 0xff, y = sym_of(e, g->base);
           sm[k] = (uint8_t)(((v >> 8) & 0x80) | (v & 0x7f));
-          buf |= (uint64_t)revs[i][e] << nbits;
-          nbits += g->len[e];
+          if (y == ESC) xrec[x++] = ((uint32_t)(l * PER_LANE + j) << 8) | (uint32_t)e;
+          buf |= (uint64_t)revs[i][y] << nbits;
+          nbits += g->len[y];
           if (nbits >= 32) {
             ex[w++] = (uint32_t)buf;
             buf >>= 32;
@@ -231,6 +261,7 @@ uint64_t oracle_xc_encode(const uint16_t* src, int nseg, const int64_t* seg_n, u
       }
     }
     bofs[nb] = w;
+    xofs[nb] = x;
     s += n;
   }
   return pos;
@@ -245,15 +276,17 @@ int oracle_xc_decode(const uint8_t* blob, uint16_t* dst) {
   for (uint32_t i = 0; i < hdr.nseg; ++i) {
     const spmoe_xc_segment* g = &hdr.seg[i];
     const int64_t n = (int64_t)g->n, nb = n / SPMOE_XC_BLOCK;
-    if (n <= 0 || n % SPMOE_XC_BLOCK) return 1;
+    if (n <= 0 || n % SPMOE_XC_BLOCK || g->base > 240) return 1;
     uint16_t lut[1 << LMAX];  /* the decoder walks the single-symbol table built from len[] */
     oracle_xc_lut(g->len, lut);
     const uint8_t* sm = blob + g->off_sm;
     const uint32_t* ex = (const uint32_t*)(blob + g->off_ex);
     const uint32_t* bofs = (const uint32_t*)(blob + g->off_bofs);
     const uint8_t* lanes = blob + g->off_lanes;
+    const uint32_t* xofs = (const uint32_t*)(blob + g->off_xofs);
+    const uint32_t* xrec = (const uint32_t*)(blob + g->off_xrec);
     for (int64_t b = 0; b < nb; ++b) {
-      uint32_t w = bofs[b];
+      uint32_t w = bofs[b], x = xofs[b];
       for (int l = 0; l < LANES; ++l) {
         const uint32_t* p = ex + w;
         uint64_t buf = (uint64_t)p[0] | ((uint64_t)p[1] << 32);
@@ -269,12 +302,17 @@ int oracle_xc_decode(const uint8_t* blob, uint16_t* dst) {
             nbits += 32;
           }
           const int64_t k = b * SPMOE_XC_BLOCK + l * PER_LANE + j;
+          uint32_t expo = g->base + (e & 0xfu);
+          if ((e & 0xfu) == ESC) {
+            if (x >= xofs[b + 1] || (xrec[x] >> 8) != (uint32_t)(l * PER_LANE + j)) return 1;
+            expo = xrec[x++] & 0xffu;
+          }
           const uint8_t bb = sm[k];
-          d[k] = (uint16_t)(((bb & 0x80) << 8) | ((e & 0xff) << 7) | (bb & 0x7f));
+          d[k] = (uint16_t)(((bb & 0x80) << 8) | (expo << 7) | (bb & 0x7f));
         }
         w += lanes[b * LANES + l];
       }
-      if (w != bofs[b + 1]) return 1;
+      if (w != bofs[b + 1] || x != xofs[b + 1]) return 1;
     }
     d += n;
   }
