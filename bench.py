@@ -483,7 +483,8 @@ def main():
             "analytic_cutoff": cutoff_analytic,
             "measured_timings_ms": {"t_comp_draft": measured.t_comp_draft * 1e3,
                                     "t_comp_target": measured.t_comp_target * 1e3,
-                                    "t_io_expert": measured.t_io_expert * 1e3},
+                                    "t_io_expert": measured.t_io_expert * 1e3,
+                                    "t_predict": measured.t_predict * 1e3},
             "window_tokens": cfg["N"],
             "k_eff_measured": getattr(eng, "k_eff", None),
         },

@@ -9,7 +9,8 @@ The reference takes ``ProfiledTimings`` from desk measurements
   HBM bandwidth (the decode step is weight-bandwidth bound) + a fixed
   per-layer launch overhead; :func:`measure_timings` replaces these model
   values with CUDA-event measurements of a live engine;
-* ``t_predict`` = K1 router latency.
+* ``t_predict`` = K1 router latency: a constant in the analytic model,
+  measured by CUDA events on the live engine in :func:`measure_timings`.
 
 :func:`write_profiled_config` emits the reference YAML (``config.py:436-482``)
 so moesim's simulator can run calibrated what-if sweeps.
@@ -24,7 +25,7 @@ from .config import HardwareSpec, ProfiledTimings
 
 ROOT = Path(__file__).resolve().parents[1]
 LAYER_OVERHEAD_S = 40e-6  # measured order of host launch overhead per layer
-K1_LATENCY_S = 25e-6  # K1 router latency measured on B200 (tools/bench_kernels.py)
+K1_LATENCY_S = 25e-6  # analytic-model K1 latency; measure_timings times the live K1
 COPY_OVERHEAD_S = 20e-6
 
 
@@ -48,10 +49,36 @@ def b200_timings(arch, hw: HardwareSpec, hbm_efficiency: float = 0.7) -> Profile
                            t_predict=K1_LATENCY_S)
 
 
+def measure_k1(engine, reps: int = 20) -> float:
+    """Seconds per K1 call as the predictor issues it (Algorithm 1 line 2-3:
+    one token per sequence through a target router, top prefetch_k), by CUDA
+    events around ``reps`` back-to-back launches on the engine's stream."""
+    import torch
+
+    from . import kernels as K
+
+    a = engine.arch
+    k = max(1, min(a.num_experts, int(engine.policy.prefetch_k or a.top_k)))
+    x = torch.randn((engine.batch, a.hidden), device=engine.device).to(torch.bfloat16)
+    wg = engine.weights.layers[0].router
+    st = engine.stream
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            K.router_topk(x, wg, k, True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            K.router_topk(x, wg, k, True)
+        e1.record(st)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / reps
+
+
 def measure_timings(engine, steps: int = 3) -> ProfiledTimings:
     """Per-layer draft / verify compute from CUDA events on a live engine
     (fully resident layers only would be ideal; we subtract measured copy
-    stalls instead), and t_io from the engine's transfer log."""
+    stalls instead), t_io from the engine's transfer log and t_predict from
+    timed K1 launches (:func:`measure_k1`)."""
     rep = engine.report()
     ts = engine.timing_summary()
     n_it = max(1, len(engine.iter_records))
@@ -66,7 +93,7 @@ def measure_timings(engine, steps: int = 3) -> ProfiledTimings:
     # with the bandwidth in raw expert bytes (XC tier: link peak / wire ratio)
     t_io = max(t_io, engine.arch.expert_bytes / engine.effective_hw().pcie_bandwidth)
     return ProfiledTimings(t_comp_target=target_layer, t_comp_draft=draft_layer, t_io_expert=t_io,
-                           t_predict=K1_LATENCY_S)
+                           t_predict=measure_k1(engine))
 
 
 def write_profiled_config(path, model, hw, timings, policy) -> None:

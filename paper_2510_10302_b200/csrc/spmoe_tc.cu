@@ -92,6 +92,25 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// Same with an L2 cache policy (createpolicy): weights are read once per
+// launch, so they stream through L2 as evict-first and leave the lines a
+// preceding decode just wrote (the slot's last segment) for the reads that
+// follow.
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
@@ -646,6 +665,7 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
       uint32_t phase = 0;
       bool waited = false;
       int pend_stage[STAGES], pend_kb[STAGES], pend_row[STAGES], npend = 0;
+      const uint64_t ef = l2_evict_first_policy();
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int a = u / mt_up, m = u - a * mt_up;
         const int e = p.active[a], slot = p.slot[a];
@@ -654,8 +674,8 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * STAGE_BYTES;
           mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
-          tma_load_3d(st, &map_wu, &full_bar[stage], kb * BK, m * BM, slot);
-          tma_load_3d(st + A_BYTES, &map_wu, &full_bar[stage], kb * BK, p.F + m * BM, slot);
+          tma_load_3d_hint(st, &map_wu, &full_bar[stage], kb * BK, m * BM, slot, ef);
+          tma_load_3d_hint(st + A_BYTES, &map_wu, &full_bar[stage], kb * BK, p.F + m * BM, slot, ef);
           if (waited) {
             tma_load_2d(st + 2 * A_BYTES, &map_x, &full_bar[stage], kb * BK, arow);
           } else {
@@ -677,8 +697,8 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * STAGE_BYTES;
           mbar_expect_tx(&full_bar[stage], 2 * A_BYTES);
-          tma_load_3d(st, &map_wd, &full_bar[stage], m * BM, j * BM, slot);
-          tma_load_3d(st + A_BYTES, &map_wd, &full_bar[stage], m * BM + BK, j * BM, slot);
+          tma_load_3d_hint(st, &map_wd, &full_bar[stage], m * BM, j * BM, slot, ef);
+          tma_load_3d_hint(st + A_BYTES, &map_wd, &full_bar[stage], m * BM + BK, j * BM, slot, ef);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
