@@ -323,7 +323,7 @@ int spmoe_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, uint64_t off
 /*   x bit for bit.  Per-value coding only: no cross-value or            */
 /*   cross-expert modelling.                                             */
 /* --------------------------------------------------------------------- */
-#define SPMOE_XC_MAGIC 0x34435853u /* "SXC4" */
+#define SPMOE_XC_MAGIC 0x35435853u /* "SXC5" */
 #define SPMOE_XC_BLOCK 4096        /* values per coding block */
 #define SPMOE_XC_LANES 32          /* exponent substreams per block */
 #define SPMOE_XC_LMAX 12           /* longest symbol code, bits */
@@ -353,11 +353,17 @@ int spmoe_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, uint64_t off
  *   sm    [n]       u8   (v >> 8 & 0x80) | (v & 0x7f)
  *   ex    [ex_words] u32 per block, SPMOE_XC_LANES lane substreams back to
  *                        back; lane l holds the bit-reversed codes of values
- *                        128 l .. 128 l + 127 of the block, LSB first,
- *                        padded to a whole word (8 readable slack bytes after
- *                        the stream)
+ *                        128 l .. 128 l + 127 of the block, LSB first; in
+ *                        bit mode the substreams are bit-contiguous and only
+ *                        the block's run is padded to a whole word, in word
+ *                        mode each substream is padded to a whole word (8
+ *                        readable slack bytes after the stream)
  *   bofs  [nb+1]    u32  first ex word of each block (exclusive prefix)
- *   lanes [nb*32]   u8   word count of each lane substream
+ *   lanes [nb*32]   u8   per lane: bit mode, its code bits - the block's
+ *                        lbase; word mode, its word count
+ *   lbase [nb]      u16  bit 15 = word mode (a block whose lane lengths
+ *                        spread over more than 255 bits); bits 0-14 = the
+ *                        shortest lane's code bits (bit mode)
  *   xofs  [nb+1]    u32  first exception of each block (exclusive prefix)
  *   xrec  [n_exc]   u32  escaped values in value order: index in block << 8
  *                        | exponent
@@ -365,11 +371,11 @@ int spmoe_fill_normal_bf16(uint16_t* dst, int64_t n, uint64_t seed, uint64_t off
  */
 typedef struct spmoe_xc_segment {
   uint64_t n;
-  uint64_t off_lut, off_sm, off_ex, off_bofs, off_lanes, off_xofs, off_xrec;
+  uint64_t off_lut, off_sm, off_ex, off_bofs, off_lanes, off_lbase, off_xofs, off_xrec;
   uint32_t ex_words, n_exc;
   uint32_t base, pad;
   uint8_t len[SPMOE_XC_NSYM];
-} spmoe_xc_segment; /* 96 bytes */
+} spmoe_xc_segment; /* 104 bytes */
 
 typedef struct spmoe_xc_header {
   uint32_t magic; /* SPMOE_XC_MAGIC */
@@ -377,7 +383,7 @@ typedef struct spmoe_xc_header {
   uint64_t blob_bytes; /* header + streams (what crosses the host link) */
   uint64_t raw_bytes;  /* 2 * sum(n) */
   spmoe_xc_segment seg[SPMOE_XC_MAX_SEG];
-} spmoe_xc_header; /* 408 bytes; the first stream starts at 512 */
+} spmoe_xc_header; /* 440 bytes; the first stream starts at 512 */
 
 /* Device workspace bytes spmoe_xc_plan needs for these segments. */
 size_t spmoe_xc_work_bytes(int nseg, const int64_t* seg_n);

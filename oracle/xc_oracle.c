@@ -1,6 +1,6 @@
 /*
  * xc_oracle.c — CPU ORACLE of the XC expert-blob codec (include/spmoe.h,
- * "XC", format SXC4).  TEST INFRASTRUCTURE ONLY: tests/ compare the sm_100a
+ * "XC", format SXC5).  TEST INFRASTRUCTURE ONLY: tests/ compare the sm_100a
  * encoder's blob byte for byte against oracle_xc_encode and the decoder's
  * output against the original bits; the product path never links this file.
  *
@@ -19,8 +19,11 @@
  *          codes in (length, symbol) order, written bit-reversed (LSB
  *          first);
  *   block  4096 values: sign|mantissa bytes; 32 lane substreams of the
- *          codes of values 128 l .. 128 l + 127, each padded to a word;
- *          exception records (index << 8 | exponent) in value order;
+ *          codes of values 128 l .. 128 l + 127, bit-contiguous with the
+ *          block's run padded to a word (bit mode), or each padded to a
+ *          word when the lanes' bit lengths spread over more than 255
+ *          (word mode); exception records (index << 8 | exponent) in value
+ *          order;
  *   layout header at 0, streams from 512 on 256-byte boundaries in the
  *          order lut (multi-symbol, u32), sm, ex (+ 8 slack bytes), bofs,
  *          lanes, xofs, xrec per segment.
@@ -166,6 +169,34 @@ void oracle_xc_lut2(const uint16_t lut[1 << LMAX], uint32_t lut2[1 << LMAX]) {
   }
 }
 
+/* Code bits of each lane of block b. */
+static void block_lane_bits(const uint16_t* s, int64_t b, const spmoe_xc_segment* g, uint32_t lb[LANES]) {
+  for (int l = 0; l < LANES; ++l) {
+    uint32_t bits = 0;
+    for (int j = 0; j < PER_LANE; ++j) bits += g->len[sym_of((s[b * SPMOE_XC_BLOCK + l * PER_LANE + j] >> 7) & 0xff, g->base)];
+    lb[l] = bits;
+  }
+}
+
+/* Word mode when the lane lengths spread over more than 255 bits. */
+static int block_word_mode(const uint32_t lb[LANES]) {
+  uint32_t lo = lb[0], hi = lb[0];
+  for (int l = 1; l < LANES; ++l) {
+    if (lb[l] < lo) lo = lb[l];
+    if (lb[l] > hi) hi = lb[l];
+  }
+  return hi - lo > 255;
+}
+
+static uint32_t block_words(const uint32_t lb[LANES]) {
+  uint32_t w = 0, bits = 0;
+  for (int l = 0; l < LANES; ++l) {
+    w += (lb[l] + 31) / 32;
+    bits += lb[l];
+  }
+  return block_word_mode(lb) ? w : (bits + 31) / 32;
+}
+
 /* Encode nseg segments (back to back in src).  Returns the blob size; the
  * blob is written only if out != NULL and cap >= size.  0 on invalid
  * segment sizes. */
@@ -196,19 +227,18 @@ uint64_t oracle_xc_encode(const uint16_t* src, int nseg, const int64_t* seg_n, u
     g->n = (uint64_t)n;
     g->n_exc = (uint32_t)cnt[ESC];
     uint64_t words = 0;
-    for (int64_t b = 0; b < nb; ++b)
-      for (int l = 0; l < LANES; ++l) {
-        uint64_t bits = 0;
-        for (int j = 0; j < PER_LANE; ++j)
-          bits += g->len[sym_of((s[b * SPMOE_XC_BLOCK + l * PER_LANE + j] >> 7) & 0xff, g->base)];
-        words += (bits + 31) / 32;
-      }
+    for (int64_t b = 0; b < nb; ++b) {
+      uint32_t lb[LANES];
+      block_lane_bits(s, b, g, lb);
+      words += block_words(lb);
+    }
     g->ex_words = (uint32_t)words;
     g->off_lut = pos; pos = a256(pos + (4u << LMAX));
     g->off_sm = pos; pos = a256(pos + (uint64_t)n);
     g->off_ex = pos; pos = a256(pos + words * 4 + 8);
     g->off_bofs = pos; pos = a256(pos + (uint64_t)(nb + 1) * 4);
     g->off_lanes = pos; pos = a256(pos + (uint64_t)nb * LANES);
+    g->off_lbase = pos; pos = a256(pos + (uint64_t)nb * 2);
     g->off_xofs = pos; pos = a256(pos + (uint64_t)(nb + 1) * 4);
     g->off_xrec = pos; pos = a256(pos + (uint64_t)g->n_exc * 4);
     raw += 2 * (uint64_t)n;
@@ -234,31 +264,33 @@ uint64_t oracle_xc_encode(const uint16_t* src, int nseg, const int64_t* seg_n, u
     uint8_t* lanes = out + g->off_lanes;
     uint32_t* xofs = (uint32_t*)(out + g->off_xofs);
     uint32_t* xrec = (uint32_t*)(out + g->off_xrec);
+    uint16_t* lbase = (uint16_t*)(out + g->off_lbase);
     uint32_t w = 0, x = 0;
     for (int64_t b = 0; b < nb; ++b) {
       bofs[b] = w;
       xofs[b] = x;
+      uint32_t lb[LANES];
+      block_lane_bits(s, b, g, lb);
+      const int wm = block_word_mode(lb);
+      uint32_t lo = lb[0];
+      for (int l = 1; l < LANES; ++l)
+        if (lb[l] < lo) lo = lb[l];
+      lbase[b] = (uint16_t)(wm ? 0x8000u : lo);
+      uint64_t bitpos = (uint64_t)w * 32; /* the lane's first bit within ex */
       for (int l = 0; l < LANES; ++l) {
-        uint64_t buf = 0;
-        int nbits = 0;
-        const uint32_t w0 = w;
+        lanes[b * LANES + l] = (uint8_t)(wm ? (lb[l] + 31) / 32 : lb[l] - lo);
         for (int j = 0; j < PER_LANE; ++j) {
           const int64_t k = b * SPMOE_XC_BLOCK + l * PER_LANE + j;
           const uint16_t v = s[k];
           const int e = (v >> 7) & 0xff, y = sym_of(e, g->base);
           sm[k] = (uint8_t)(((v >> 8) & 0x80) | (v & 0x7f));
           if (y == ESC) xrec[x++] = ((uint32_t)(l * PER_LANE + j) << 8) | (uint32_t)e;
-          buf |= (uint64_t)revs[i][y] << nbits;
-          nbits += g->len[y];
-          if (nbits >= 32) {
-            ex[w++] = (uint32_t)buf;
-            buf >>= 32;
-            nbits -= 32;
-          }
+          for (int t = 0; t < g->len[y]; ++t, ++bitpos)
+            if ((revs[i][y] >> t) & 1u) ex[bitpos >> 5] |= 1u << (bitpos & 31);
         }
-        if (nbits > 0) ex[w++] = (uint32_t)buf;
-        lanes[b * LANES + l] = (uint8_t)(w - w0);
+        if (wm) bitpos = (bitpos + 31) & ~(uint64_t)31;
       }
+      w += block_words(lb);
     }
     bofs[nb] = w;
     xofs[nb] = x;
@@ -285,22 +317,24 @@ int oracle_xc_decode(const uint8_t* blob, uint16_t* dst) {
     const uint8_t* lanes = blob + g->off_lanes;
     const uint32_t* xofs = (const uint32_t*)(blob + g->off_xofs);
     const uint32_t* xrec = (const uint32_t*)(blob + g->off_xrec);
+    const uint16_t* lbase = (const uint16_t*)(blob + g->off_lbase);
     for (int64_t b = 0; b < nb; ++b) {
-      uint32_t w = bofs[b], x = xofs[b];
+      uint32_t x = xofs[b];
+      const int wm = lbase[b] >> 15;
+      uint64_t bitpos = (uint64_t)bofs[b] * 32;
       for (int l = 0; l < LANES; ++l) {
-        const uint32_t* p = ex + w;
-        uint64_t buf = (uint64_t)p[0] | ((uint64_t)p[1] << 32);
-        int nbits = 64, r = 2;
+        const uint32_t lane_bits = wm ? 32u * lanes[b * LANES + l] : (uint32_t)(lbase[b] & 0x7fff) + lanes[b * LANES + l];
+        const uint64_t end = bitpos + lane_bits;
         for (int j = 0; j < PER_LANE; ++j) {
-          const uint16_t e = lut[buf & ((1u << LMAX) - 1)];
+          uint32_t peek = 0; /* the next LMAX bits, LSB first */
+          for (int t = 0; t < LMAX; ++t) {
+            const uint64_t q = bitpos + t;
+            if (q < (uint64_t)bofs[b + 1] * 32) peek |= ((ex[q >> 5] >> (q & 31)) & 1u) << t;
+          }
+          const uint16_t e = lut[peek];
           const int L = e >> 8;
           if (L == 0) return 1;
-          buf >>= L;
-          nbits -= L;
-          if (nbits < 32) {
-            buf |= (uint64_t)p[r++] << nbits;
-            nbits += 32;
-          }
+          bitpos += L;
           const int64_t k = b * SPMOE_XC_BLOCK + l * PER_LANE + j;
           uint32_t expo = g->base + (e & 0xfu);
           if ((e & 0xfu) == ESC) {
@@ -310,9 +344,11 @@ int oracle_xc_decode(const uint8_t* blob, uint16_t* dst) {
           const uint8_t bb = sm[k];
           d[k] = (uint16_t)(((bb & 0x80) << 8) | (expo << 7) | (bb & 0x7f));
         }
-        w += lanes[b * LANES + l];
+        if (bitpos > end) return 1;
+        bitpos = end;
       }
-      if (w != bofs[b + 1] || x != xofs[b + 1]) return 1;
+      if ((bitpos + 31) / 32 > bofs[b + 1]) return 1;
+      if (x != xofs[b + 1]) return 1;
     }
     d += n;
   }

@@ -2,11 +2,11 @@
 
 The offload tier's cost is bytes over PCIe (``IoChannel.transfer``,
 ``prefetch.py:45-74``; ``t_io = size / bw + overhead``, ``config.py:229-231``).
-XC (format SXC4 in ``include/spmoe.h``) stores each bf16 weight as its
+XC (format SXC5 in ``include/spmoe.h``) stores each bf16 weight as its
 sign|mantissa byte plus its exponent as a 4-bit offset from the segment's
 base exponent (15 = escape, exponent in a per-block exception list) in the
-segment's canonical Huffman code (<= 12 bits, 32 lane substreams per
-4096-value block), so a routed expert
+segment's canonical Huffman code (<= 12 bits, 32 bit-contiguous lane
+substreams per 4096-value block), so a routed expert
 crosses the link as ~67.5 % of its raw bytes and is expanded bit-exactly
 into its HBM slot by the copy path's warp-per-block decode kernel.
 Only the encoder orchestration lives here; encode / decode run on the GPU
@@ -23,7 +23,7 @@ import torch
 
 from . import _native
 
-XC_MAGIC = 0x34435853  # "SXC4"
+XC_MAGIC = 0x35435853  # "SXC5"
 XC_NSYM = 16
 XC_BLOCK = 4096
 XC_MAX_SEG = 4
@@ -37,6 +37,7 @@ class XcSegment(C.Structure):
         ("off_ex", C.c_uint64),
         ("off_bofs", C.c_uint64),
         ("off_lanes", C.c_uint64),
+        ("off_lbase", C.c_uint64),
         ("off_xofs", C.c_uint64),
         ("off_xrec", C.c_uint64),
         ("ex_words", C.c_uint32),
@@ -57,7 +58,7 @@ class XcHeader(C.Structure):
     ]
 
 
-assert C.sizeof(XcSegment) == 96 and C.sizeof(XcHeader) == 408
+assert C.sizeof(XcSegment) == 104 and C.sizeof(XcHeader) == 440
 
 
 def expert_segments(ffn: int, hidden: int) -> list[int]:

@@ -1,5 +1,5 @@
 // spmoe_codec.cu — XC, the lossless exponent coding of expert blobs that
-// cross the host link (format SXC4: include/spmoe.h, "XC").
+// cross the host link (format SXC5: include/spmoe.h, "XC").
 //
 // Why: with an offload budget the verify stage is bound by the pinned
 // host -> HBM copies of routed experts (IoChannel.transfer,
@@ -21,10 +21,11 @@
 //
 // Kernels:
 //   xc_hist_kernel    exponent histogram per segment (per-warp smem bins)
-//   xc_count_kernel   per block and lane: code words; per block: words and
-//                     escapes
+//   xc_count_kernel   per block and lane: code bits; per block: bit or word
+//                     mode, words and escapes
 //   xc_scan_kernel    exclusive prefix of the per-block counts (1 CTA)
-//   xc_write_kernel   sign|mantissa bytes, lane substreams, exceptions
+//   xc_write_kernel   sign|mantissa bytes, lane substreams (bit-contiguous),
+//                     exceptions
 //   xc_decode_kernel  the inverse; HBM-bound target (reads ~1.35 B, writes
 //                     2 B per value)
 // Code construction (host) restates oracle/xc_oracle.c exactly.
@@ -93,9 +94,17 @@ __device__ __forceinline__ void lane_vals(const uint16_t* src, int64_t blk, int 
 
 // ------------------------------------------------------------------ count
 // One warp per block: lane word counts and the block's total.
+// Per lane: its code bits (bit mode: minus the block's shortest lane) or
+// words (word mode, when the lanes spread over more than 255 bits).
+__device__ __forceinline__ uint32_t lane_bits_of(uint32_t v, uint32_t lbase) {
+  return (lbase >> 15) ? 32u * v : (lbase & 0x7fffu) + v;
+}
+
+// One warp per block: lane lengths, the block's mode, words and escapes.
 __global__ void __launch_bounds__(kThreads) xc_count_kernel(const uint16_t* __restrict__ src, int64_t nb,
                                                             const Codes c, uint32_t* __restrict__ bwords,
-                                                            uint8_t* __restrict__ lanes, uint32_t* __restrict__ bexc) {
+                                                            uint8_t* __restrict__ lanes, uint16_t* __restrict__ lbase,
+                                                            uint32_t* __restrict__ bexc) {
   __shared__ uint8_t s_len[256];
   s_len[threadIdx.x] = c.len[threadIdx.x];
   __syncthreads();
@@ -114,15 +123,20 @@ __global__ void __launch_bounds__(kThreads) xc_count_kernel(const uint16_t* __re
     }
   }
   const uint32_t words = (bits + 31) / 32;
-  lanes[blk * kLanes + lane] = (uint8_t)words;
-  uint32_t tot = words;
+  uint32_t lo = bits, hi = bits, tbits = bits, twords = words;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    tbits += __shfl_xor_sync(0xffffffffu, tbits, o);
+    twords += __shfl_xor_sync(0xffffffffu, twords, o);
     nx += __shfl_xor_sync(0xffffffffu, nx, o);
   }
+  const bool word_mode = hi - lo > 255;
+  lanes[blk * kLanes + lane] = (uint8_t)(word_mode ? words : bits - lo);
   if (lane == 0) {
-    bwords[blk] = tot;
+    lbase[blk] = (uint16_t)(word_mode ? 0x8000u : lo);
+    bwords[blk] = word_mode ? twords : (tbits + 31) / 32;
     bexc[blk] = nx;
   }
 }
@@ -162,6 +176,7 @@ struct WriteParams {
   uint32_t* ex;
   const uint32_t* bofs;
   const uint8_t* lanes;
+  const uint16_t* lbase;
   const uint32_t* xofs;  // first exception of each block
   uint32_t* xrec;
   Codes c;
@@ -177,13 +192,18 @@ __global__ void __launch_bounds__(kThreads) xc_write_kernel(const WriteParams p)
   const int lane = threadIdx.x & 31;
   const int64_t blk = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (blk >= p.nb) return;
-  uint32_t words = p.lanes[blk * kLanes + lane], pre = words;
+  // this lane's first bit: the block's first word + the bits of the lanes
+  // before it (word mode: their whole words)
+  const uint32_t lbits = lane_bits_of(p.lanes[blk * kLanes + lane], p.lbase[blk]);
+  uint32_t pre = lbits;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t u = __shfl_up_sync(0xffffffffu, pre, o);
     if (lane >= o) pre += u;
   }
-  uint32_t* out = p.ex + p.bofs[blk] + (pre - words);
+  const uint32_t start = pre - lbits;
+  // neighbouring lanes share boundary words: OR into the zeroed stream
+  uint32_t* out = p.ex + p.bofs[blk] + (start >> 5);
   // this lane's exceptions follow those of the lanes before it
   uint32_t nx = 0;
   for (int q = 0; q < kPerLane / 8; ++q) {
@@ -201,7 +221,7 @@ __global__ void __launch_bounds__(kThreads) xc_write_kernel(const WriteParams p)
   }
   uint32_t* xout = p.xrec + p.xofs[blk] + (xpre - nx);
   uint64_t buf = 0;
-  int nbits = 0;
+  int nbits = (int)(start & 31);
   for (int q = 0; q < kPerLane / 8; ++q) {
     uint32_t w[4];
     lane_vals(p.src, blk, lane, q, w);
@@ -215,14 +235,14 @@ __global__ void __launch_bounds__(kThreads) xc_write_kernel(const WriteParams p)
       buf |= (uint64_t)s_rev[e] << nbits;
       nbits += s_len[e];
       if (nbits >= 32) {
-        *out++ = (uint32_t)buf;
+        atomicOr(out++, (uint32_t)buf);
         buf >>= 32;
         nbits -= 32;
       }
     }
     *reinterpret_cast<uint2*>(p.sm + blk * SPMOE_XC_BLOCK + lane * kPerLane + 8 * q) = make_uint2(smw[0], smw[1]);
   }
-  if (nbits > 0) *out = (uint32_t)buf;
+  if (nbits > 0) atomicOr(out, (uint32_t)buf);
 }
 
 // ----------------------------------------------------------------- decode
@@ -232,6 +252,7 @@ struct DecSeg {
   const uint32_t* ex;
   const uint32_t* bofs;
   const uint8_t* lanes;
+  const uint16_t* lbase;
   const uint32_t* xofs;
   const uint32_t* xrec;
   uint16_t* dst;
@@ -274,13 +295,12 @@ __device__ __forceinline__ uint32_t sh_u32(const void* p) { return (uint32_t)__c
 // over-long block).  Up to five symbols per lookup; they queue in a
 // register and leave as whole words.
 template <bool kStaged>
-__device__ __forceinline__ void decode_lane(const uint32_t* __restrict__ s_lut2, const uint32_t* wp,
+__device__ __forceinline__ void decode_lane(const uint32_t* __restrict__ s_lut2, const uint32_t* wp, uint32_t pos,
                                             uint32_t* __restrict__ erow) {
   // bit window = (nxt:cur) >> pos, pos < 32: at least 33 valid bits; the
   // word after nxt is fetched one refill ahead, so a refill never waits on
   // a load (the only load on the serial chain is the table lookup)
   uint32_t cur = wp[0], nxt = wp[1], ahead = wp[2];
-  uint32_t pos = 0;
   wp += 3;
   uint64_t q = 0;
   uint32_t nq = 0;  // queued bits (4 per symbol)
@@ -375,14 +395,15 @@ __global__ void __launch_bounds__(kDecThreads, CTAS) xc_decode_kernel(const DecP
   // warp-major block order: the last, partial wave's blocks go to one warp
   // of many CTAs (one per SM) instead of every warp of a few CTAs
   for (uint32_t blk = warp * gridDim.x + blockIdx.x; blk < S.nblk; blk += gridDim.x * kDecWarps) {
-    // this lane's substream: block start + words of the lanes before it
-    const uint32_t words = __ldg(S.lanes + (uint64_t)blk * kLanes + lane);
-    uint32_t pre = words;
+    // this lane's substream: block start + bits of the lanes before it
+    const uint32_t lbits = lane_bits_of(__ldg(S.lanes + (uint64_t)blk * kLanes + lane), __ldg(S.lbase + blk));
+    uint32_t pre = lbits;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t u = __shfl_up_sync(0xffffffffu, pre, o);
       if (lane >= o) pre += u;
     }
+    const uint32_t start = pre - lbits;
     const uint32_t w0 = __ldg(S.bofs + blk), nw = __ldg(S.bofs + blk + 1) - w0;
     const uint32_t x0 = __ldg(S.xofs + blk), x1 = __ldg(S.xofs + blk + 1);
     const uint32_t* run = S.ex + w0;
@@ -417,9 +438,9 @@ __global__ void __launch_bounds__(kDecThreads, CTAS) xc_decode_kernel(const DecP
           "r"(phase)
           : "memory");
       phase ^= 1;
-      decode_lane<true>(s_lut2, stage + (delta >> 2) + (pre - words), erow);
+      decode_lane<true>(s_lut2, stage + (delta >> 2) + (start >> 5), start & 31, erow);
     } else {
-      decode_lane<false>(s_lut2, run + (pre - words), erow);
+      decode_lane<false>(s_lut2, run + (start >> 5), start & 31, erow);
     }
     __syncwarp();
     // assembly: 16 rounds of 8 consecutive values per lane (one symbol
@@ -467,10 +488,11 @@ inline uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
 inline int64_t nblocks(int64_t n) { return n / SPMOE_XC_BLOCK; }
 
 // work layout per segment (u32 words):
-//   hist[256] | bofs[nb+1] | lanes[nb*32 bytes] | xofs[nb+1]
+//   hist[256] | bofs[nb+1] | lanes[nb*32 bytes] | xofs[nb+1] | lbase[nb u16]
 inline size_t seg_lanes_words(int64_t n) { return (size_t)nblocks(n) * kLanes / 4; }
-inline size_t seg_work_words(int64_t n) { return 256 + 2 * (size_t)(nblocks(n) + 1) + seg_lanes_words(n); }
 inline size_t seg_xofs_word(int64_t n) { return 256 + (size_t)(nblocks(n) + 1) + seg_lanes_words(n); }
+inline size_t seg_lbase_word(int64_t n) { return seg_xofs_word(n) + (size_t)(nblocks(n) + 1); }
+inline size_t seg_work_words(int64_t n) { return seg_lbase_word(n) + (size_t)(nblocks(n) + 1) / 2; }
 
 // The segment's base exponent (restates oracle_xc_base, oracle/xc_oracle.c):
 // the lowest b <= 240 whose window [b, b + 14] holds the most values.
@@ -676,7 +698,8 @@ int spmoe_xc_plan(const uint16_t* src, int nseg, const int64_t* seg_n, void* wor
     uint32_t* bofs = wk + off + 256;
     uint8_t* lanes = (uint8_t*)(bofs + nb + 1);
     uint32_t* xofs = wk + off + seg_xofs_word(n);
-    xc_count_kernel<<<(unsigned)((nb + kWarps - 1) / kWarps), kThreads, 0, st>>>(s, nb, c, bofs, lanes, xofs);
+    uint16_t* lbase = (uint16_t*)(wk + off + seg_lbase_word(n));
+    xc_count_kernel<<<(unsigned)((nb + kWarps - 1) / kWarps), kThreads, 0, st>>>(s, nb, c, bofs, lanes, lbase, xofs);
     xc_scan_kernel<<<1, 1024, 0, st>>>(bofs, nb);
     xc_scan_kernel<<<1, 1024, 0, st>>>(xofs, nb);
     off += seg_work_words(n);
@@ -704,6 +727,7 @@ int spmoe_xc_plan(const uint16_t* src, int nseg, const int64_t* seg_n, void* wor
     g.off_ex = pos; pos = align256(pos + (uint64_t)g.ex_words * 4 + 8);
     g.off_bofs = pos; pos = align256(pos + (uint64_t)(nb + 1) * 4);
     g.off_lanes = pos; pos = align256(pos + (uint64_t)nb * kLanes);
+    g.off_lbase = pos; pos = align256(pos + (uint64_t)nb * 2);
     g.off_xofs = pos; pos = align256(pos + (uint64_t)(nb + 1) * 4);
     g.off_xrec = pos; pos = align256(pos + (uint64_t)g.n_exc * 4);
     raw += 2 * (uint64_t)n;
@@ -740,12 +764,14 @@ int spmoe_xc_encode(const uint16_t* src, const spmoe_xc_header* hdr, const void*
     p.bofs = wk + off + 256;
     p.lanes = (const uint8_t*)(p.bofs + nb + 1);
     p.xofs = wk + off + seg_xofs_word(n);
+    p.lbase = (const uint16_t*)(wk + off + seg_lbase_word(n));
     p.xrec = (uint32_t*)(blob + g.off_xrec);
     codes_of(g, &p.c);
     xc_write_kernel<<<(unsigned)((nb + kWarps - 1) / kWarps), kThreads, 0, st>>>(p);
     cudaMemcpyAsync(blob + g.off_bofs, p.bofs, (nb + 1) * 4, cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(blob + g.off_lanes, p.lanes, nb * kLanes, cudaMemcpyDeviceToDevice, st);
     cudaMemcpyAsync(blob + g.off_xofs, p.xofs, (nb + 1) * 4, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(blob + g.off_lbase, p.lbase, nb * 2, cudaMemcpyDeviceToDevice, st);
     lut_of(g.len, &luts[(size_t)i * kLutSize]);
     lut2_of(&luts[(size_t)i * kLutSize], &luts2[(size_t)i * kLutSize]);
     cudaMemcpyAsync(blob + g.off_lut, &luts2[(size_t)i * kLutSize], 4 * kLutSize, cudaMemcpyHostToDevice, st);
@@ -785,6 +811,7 @@ int spmoe_xc_decode_segments_timed(const uint8_t* blob, const spmoe_xc_header* h
     S.ex = (const uint32_t*)(blob + g.off_ex);
     S.bofs = (const uint32_t*)(blob + g.off_bofs);
     S.lanes = blob + g.off_lanes;
+    S.lbase = (const uint16_t*)(blob + g.off_lbase);
     S.xofs = (const uint32_t*)(blob + g.off_xofs);
     S.xrec = (const uint32_t*)(blob + g.off_xrec);
     S.dst = d;
