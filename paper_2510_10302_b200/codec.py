@@ -62,9 +62,12 @@ assert C.sizeof(XcSegment) == 104 and C.sizeof(XcHeader) == 440
 
 
 def expert_segments(ffn: int, hidden: int) -> list[int]:
-    """An expert blob W1 | W3 | W2 codes as three segments (one per matrix:
-    W2's scale differs, so it gets its own code tables)."""
-    return [ffn * hidden] * 3
+    """An expert blob W1 | W3 | W2 codes as two segments: W1 | W3 (same
+    shape and init scale: one code table, one decode launch of twice the
+    blocks, so a smaller share of partial waves) and W2 (its scale differs;
+    the last segment on the link, the only decode on the layer's critical
+    path)."""
+    return [2 * ffn * hidden, ffn * hidden]
 
 
 def codec_applies(segments: Sequence[int]) -> bool:
