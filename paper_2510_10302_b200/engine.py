@@ -185,8 +185,8 @@ class SpecMoEEngine:
         if expert_parallel:
             from .ep import ExpertParallelExchange
 
-            if policy.policy is not Policy.ON_DEMAND:
-                raise ValidationError("expert_parallel runs the on_demand policy (no cross-rank prefetch)")
+            if policy.policy not in (Policy.ON_DEMAND, Policy.DRAFT_PREFETCH):
+                raise ValidationError("expert_parallel runs the on_demand or draft_prefetch policy")
             self.ep = ExpertParallelExchange(arch.num_experts, arch.top_k, ep_group)
             per_layer = len(self.ep.local_experts)
         if self.capacity < per_layer:
@@ -788,7 +788,24 @@ class SpecMoEEngine:
     def _predict_and_enqueue(self, l: int, x_last: torch.Tensor, step: int) -> None:
         pk = self.policy.prefetch_k
         i, hptr, ev = self.predictor.predict(x_last, self.weights.layers[l].router, pk, True, self.pred_w, self.pred_idx)
+        if self.ep is not None:
+            self._ep_enqueue(l, i, step)
+            return
         self.cache.push_task(l, hptr, self.predictor.width, ev, step)
+
+    def _ep_enqueue(self, l: int, i: int, step: int) -> None:
+        """Expert-parallel Algorithm 1 l.8-9 (ep.py): once predictor entry i
+        has landed, every rank's predicted experts for layer l are gathered
+        on the host and this rank enqueues the ones it owns (its cache is
+        the one the verify reads).  The task's index array is host memory
+        kept alive (in ``_pushed``) until the drain that logs it."""
+        from . import _native
+
+        _native.check("spmoe_event_synchronize", self._lib.spmoe_event_synchronize(self.predictor.events[i]))
+        share = self.ep.prefetch_share(self.predictor.view[i].copy())
+        if share.size:
+            self.cache.push_task(l, share.ctypes.data, int(share.size), 0, step)
+            self._pushed.append((l, share))
         self._pushed.append((l, i))
         if not self.policy.worker_prefetch:
             # vanilla executor: block until the copies are issued, and make the
@@ -841,6 +858,9 @@ class SpecMoEEngine:
                 # waits on this replay's event nodes (Algorithm 1 l.8-9)
                 for l in range(self.cutoff + 1):
                     i = d * L + l
+                    if self.ep is not None:
+                        self._ep_enqueue(l, i, d)
+                        continue
                     self.cache.push_task(l, self.predictor.host_ptr_of(i), width, self.predictor.events[i], d)
                     self._pushed.append((l, i))
         ev1.record(self.stream)

@@ -12,6 +12,14 @@ contiguous blocks, rank r owning ``[lo_r, hi_r)``, and each verify layer does
     -> K4 weighted combine + residual (K2's inverse map indexes the returned
        rows directly, because the send order IS K2's permuted order).
 
+With the draft_prefetch policy each rank drafts its own stream and runs
+Algorithm 1's predictor (K1) on it; the predicted expert ids of every
+(draft step, layer <= cutoff) are all-gathered on the host (a gloo group
+beside the NCCL one, E-sized int vectors) and each rank enqueues the union
+of every rank's predictions that it OWNS (rank order, then token order,
+first occurrence) into its own prefetch worker: the owner's cache is the one
+the verify will read, whichever stream's draft predicted the expert.
+
 Because expert ids are contiguous per owner, K2's stable expert order is
 already grouped by destination rank: no extra sort, the send counts are
 prefix sums of the per-expert counts the host already holds for its cache
@@ -52,6 +60,19 @@ def send_counts_of(counts: np.ndarray, world: int) -> list[int]:
     return [int(counts[slice(*shard_range(E, r, world))].sum()) for r in range(world)]
 
 
+def owned_predictions(all_idx: np.ndarray, lo: int, hi: int) -> np.ndarray:
+    """The experts in ``[lo, hi)`` among every rank's predicted ids
+    (``all_idx [world, n]``, -1 = none), in rank order then token order,
+    each once (first occurrence)."""
+    out, seen = [], set()
+    for e in np.asarray(all_idx).reshape(-1):
+        e = int(e)
+        if lo <= e < hi and e not in seen:
+            seen.add(e)
+            out.append(e)
+    return np.asarray(out, dtype=np.int32)
+
+
 def _default_gather(src: torch.Tensor, idx: torch.Tensor, div: int, out: torch.Tensor | None = None):
     from .kernels import gather_rows
 
@@ -82,6 +103,12 @@ class ExpertParallelExchange:
         self.E, self.k = num_experts, top_k
         self.lo, self.hi = shard_range(num_experts, self.rank, self.world)
         self.gather = gather or _default_gather
+        # host-side exchanges (predicted experts) go through a CPU group: the
+        # NCCL group itself when it is gloo, else a gloo group of the same ranks
+        self.host_group = None
+        if not self.local_only:
+            ranks = dist.get_process_group_ranks(group) if group is not None else list(range(dist.get_world_size()))
+            self.host_group = group if dist.get_backend(group) == "gloo" else dist.new_group(ranks=ranks, backend="gloo")
         self._send: list[int] = []
         self._recv: list[int] = []
         self.bytes_sent = 0
@@ -109,6 +136,21 @@ class ExpertParallelExchange:
         allc = torch.empty((self.world, counts.shape[1]), dtype=torch.int64, device=dev)
         self.dist.all_gather_into_tensor(allc, mine, group=self.group)
         return allc.cpu().numpy()
+
+    def gather_predictions(self, idx: np.ndarray) -> np.ndarray:
+        """Every rank's predicted expert ids for one (draft step, layer):
+        ``[world, n]`` host int32 (equal n on every rank)."""
+        idx = np.ascontiguousarray(np.asarray(idx, dtype=np.int32).reshape(1, -1))
+        if self.local_only:
+            return idx
+        mine = torch.from_numpy(idx.copy())
+        parts = [torch.empty_like(mine) for _ in range(self.world)]
+        self.dist.all_gather(parts, mine, group=self.host_group)
+        return torch.cat(parts, dim=0).numpy()
+
+    def prefetch_share(self, idx: np.ndarray) -> np.ndarray:
+        """This rank's experts among all ranks' predictions (see module doc)."""
+        return owned_predictions(self.gather_predictions(idx), self.lo, self.hi)
 
     def dispatch(self, x: torch.Tensor, perm_token: torch.Tensor, counts: np.ndarray):
         """x ``[T, H]``; perm_token = K2's ``perm_token`` (the token of every

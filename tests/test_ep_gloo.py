@@ -112,3 +112,52 @@ def test_gloo_expert_parallel_exchange(world, E, k):
         assert p.exitcode == 0
     assert all(ok for _, ok, _ in res), res
     assert sum(b for *_, b in res) > 0
+
+
+def test_owned_predictions_order_and_dedup():
+    from paper_2510_10302_b200.ep import owned_predictions
+
+    allidx = np.array([[3, 1, -1, 3], [0, 2, 1, 3]], dtype=np.int32)
+    assert owned_predictions(allidx, 1, 4).tolist() == [3, 1, 2]  # rank order, token order, first occurrence
+    assert owned_predictions(allidx, 0, 1).tolist() == [0]
+    assert owned_predictions(allidx, 4, 8).size == 0
+    assert owned_predictions(np.full((3, 2), -1), 0, 8).size == 0
+
+
+def _pred_worker(rank, world, port, q, E, n):
+    import torch.distributed as dist
+
+    from paper_2510_10302_b200.ep import ExpertParallelExchange, owned_predictions
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ex = ExpertParallelExchange(E, 2, gather=_gather)
+        ok = True
+        for step in range(4):
+            # every rank can reconstruct every rank's predictions from the seeds
+            preds = [np.random.default_rng(1000 * step + r).integers(-1, E, size=n).astype(np.int32)
+                     for r in range(world)]
+            share = ex.prefetch_share(preds[rank])
+            ok &= share.tolist() == owned_predictions(np.stack(preds), ex.lo, ex.hi).tolist()
+            ok &= bool(((share >= ex.lo) & (share < ex.hi)).all())
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,E", [(2, 8), (3, 60)])
+def test_gloo_prefetch_share(world, E):
+    """EP draft_prefetch hand-off: each rank enqueues exactly the union of all
+    ranks' predictions that it owns (ep.ExpertParallelExchange.prefetch_share)."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_pred_worker, args=(r, world, port, q, E, 6)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res), res

@@ -2,7 +2,7 @@
 torch indexing, and the EP engine (world size 1 without a process group,
 and over a one-rank NCCL group so the all-to-all path runs) against the
 oracle at captured layer boundaries and against the non-EP engine token
-for token."""
+for token, with the on_demand and the draft_prefetch policy."""
 
 from __future__ import annotations
 
@@ -69,11 +69,47 @@ def test_ep_engine_matches_local(oracle, batch):
     assert seq_ep == seq_ref
 
 
-def test_ep_engine_rejects_prefetch_policy():
+def test_ep_engine_rejects_other_prefetch_policies():
     from paper_2510_10302_b200.config import ValidationError
 
-    with pytest.raises(ValidationError):
-        make_engine(expert_parallel=True)
+    for kind in ("gating_next_layer", "coarse_history"):
+        with pytest.raises(ValidationError):
+            make_engine(expert_parallel=True, policy_kind=kind, cutoff=None)
+
+
+@pytest.mark.parametrize("batch", [1, 2])
+def test_ep_engine_draft_prefetch_matches_local(oracle, batch):
+    """EP with the draft_prefetch policy (ep.py: predictions gathered on the
+    host, each rank enqueues the ones it owns): at world size 1 the owned
+    union is the rank's own prediction, so tokens, cache decisions and
+    counters equal the non-EP engine's (which hands the indices to the worker
+    through mapped memory and event waits instead)."""
+    kw = dict(policy_kind="draft_prefetch", cutoff=3, capacity=12, batch=batch, capture=(0, 3))
+    ep = make_engine(expert_parallel=True, **kw)
+    try:
+        em_ep, seq_ep = _run(ep)
+        check_layer_captures(ep, oracle)
+        check_acceptance(ep, oracle)
+        rep_ep = ep.report()
+        dec_ep = list(ep.decisions)
+    finally:
+        ep.close()
+    ref = make_engine(**kw)
+    try:
+        em_ref, seq_ref = _run(ref)
+        rep_ref = ref.report()
+        dec_ref = list(ref.decisions)
+    finally:
+        ref.close()
+    assert em_ep == em_ref and seq_ep == seq_ref
+    assert rep_ep.counters["prefetch_insertions"] == rep_ref.counters["prefetch_insertions"] > 0
+    for key in ("hits", "misses", "demand_insertions", "evictions"):
+        assert rep_ep.counters[key] == rep_ref.counters[key], key
+    # the same prefetch tasks in the same order (EP drops the -1 padding and
+    # duplicates: compare the expert sets of each task)
+    tasks_ep = [(l, sorted(set(i for i in ids if i >= 0))) for kind, l, ids in dec_ep if kind == "task"]
+    tasks_ref = [(l, sorted(set(i for i in ids if i >= 0))) for kind, l, ids in dec_ref if kind == "task"]
+    assert [t for t in tasks_ep if t[1]] == [t for t in tasks_ref if t[1]]
 
 
 def _free_port():
