@@ -790,8 +790,22 @@ class SpecMoEEngine:
         i, hptr, ev = self.predictor.predict(x_last, self.weights.layers[l].router, pk, True, self.pred_w, self.pred_idx)
         if self.ep is not None:
             self._ep_enqueue(l, i, step)
-            return
-        self.cache.push_task(l, hptr, self.predictor.width, ev, step)
+        else:
+            self.cache.push_task(l, hptr, self.predictor.width, ev, step)
+            self._pushed.append((l, i))
+        if not self.policy.worker_prefetch:
+            # vanilla executor: block until the copies are issued, and make the
+            # next layer wait for them (prefetch.py:241-273)
+            self._drain()
+            sp = self.stream.cuda_stream
+            for e in sorted(set(int(v) for v in self.predictor.view[i] if v >= 0)):
+                sl = self.cache.slot_of(l, e)
+                if sl >= 0 and not self.cache.slot_ready(sl):
+                    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    ea.record()
+                    self.cache.wait_slot(sl, sp)
+                    eb.record()
+                    self.stalls.append(_Stall("prefetch", l, ea, eb))
 
     def _ep_enqueue(self, l: int, i: int, step: int) -> None:
         """Expert-parallel Algorithm 1 l.8-9 (ep.py): once predictor entry i
@@ -806,20 +820,6 @@ class SpecMoEEngine:
         if share.size:
             self.cache.push_task(l, share.ctypes.data, int(share.size), 0, step)
             self._pushed.append((l, share))
-        self._pushed.append((l, i))
-        if not self.policy.worker_prefetch:
-            # vanilla executor: block until the copies are issued, and make the
-            # next layer wait for them (prefetch.py:241-273)
-            self._drain()
-            sp = self.stream.cuda_stream
-            for e in sorted(set(int(v) for v in self.predictor.view[i] if v >= 0)):
-                sl = self.cache.slot_of(l, e)
-                if sl >= 0 and not self.cache.slot_ready(sl):
-                    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    ea.record()
-                    self.cache.wait_slot(sl, sp)
-                    eb.record()
-                    self.stalls.append(_Stall("prefetch", l, ea, eb))
 
     def _target_forward(self, tokens: torch.Tensor, start: torch.Tensor, kv_len_max: int, s: _Scratch,
                         logits: bool = True) -> torch.Tensor | None:

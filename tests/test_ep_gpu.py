@@ -91,25 +91,26 @@ def test_ep_engine_draft_prefetch_matches_local(oracle, batch):
         check_layer_captures(ep, oracle)
         check_acceptance(ep, oracle)
         rep_ep = ep.report()
-        dec_ep = list(ep.decisions)
+        xfer_ep = [(t.kind, t.layer, tuple(t.experts)) for t in ep.transfers()]
+        tasks_ep = [(l, sorted(set(i for i in ids if i >= 0))) for kind, l, ids in ep.decisions if kind == "task"]
     finally:
         ep.close()
     ref = make_engine(**kw)
     try:
         em_ref, seq_ref = _run(ref)
         rep_ref = ref.report()
-        dec_ref = list(ref.decisions)
+        xfer_ref = [(t.kind, t.layer, tuple(t.experts)) for t in ref.transfers()]
+        tasks_ref = [(l, sorted(set(i for i in ids if i >= 0))) for kind, l, ids in ref.decisions if kind == "task"]
     finally:
         ref.close()
     assert em_ep == em_ref and seq_ep == seq_ref
     assert rep_ep.counters["prefetch_insertions"] == rep_ref.counters["prefetch_insertions"] > 0
     for key in ("hits", "misses", "demand_insertions", "evictions"):
         assert rep_ep.counters[key] == rep_ref.counters[key], key
-    # the same prefetch tasks in the same order (EP drops the -1 padding and
-    # duplicates: compare the expert sets of each task)
-    tasks_ep = [(l, sorted(set(i for i in ids if i >= 0))) for kind, l, ids in dec_ep if kind == "task"]
-    tasks_ref = [(l, sorted(set(i for i in ids if i >= 0))) for kind, l, ids in dec_ref if kind == "task"]
-    assert [t for t in tasks_ep if t[1]] == [t for t in tasks_ref if t[1]]
+    # the same prefetch tasks (EP drops the -1 padding and duplicates) and
+    # the same copy batches (prefetch and demand), layers and experts, in order
+    assert tasks_ep == [t for t in tasks_ref if t[1]]
+    assert xfer_ep == xfer_ref
 
 
 def _free_port():
