@@ -363,10 +363,13 @@ __device__ __forceinline__ void decode_lane(const uint32_t* __restrict__ s_lut2,
   }
 }
 
-// grid.y = segment; each warp decodes whole blocks of its segment.  CTAS =
-// resident CTAs per SM the registers are budgeted for (shared memory allows 3).
-template <int CTAS, int SMPRE>
-__global__ void __launch_bounds__(kDecThreads, CTAS) xc_decode_kernel(const DecParams p) {
+// grid.y = segment; each warp decodes whole blocks of its segment.  The
+// registers are budgeted for 2 resident CTAs per SM (3 fit in shared memory,
+// but at 40 registers the decode runs 30 % slower); the first kSmPre of the 16
+// sign|mantissa rounds are fetched before the serial decode (all 16: +2 %).
+constexpr int kDecCtas = 2;
+constexpr int kSmPre = 8;
+__global__ void __launch_bounds__(kDecThreads, kDecCtas) xc_decode_kernel(const DecParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
   // multi-symbol table: entry p (12 peeked bits) = up to five whole codes:
   // syms (4 bits each) | 4 count << 20 | bits << 25
@@ -409,9 +412,9 @@ __global__ void __launch_bounds__(kDecThreads, CTAS) xc_decode_kernel(const DecP
     const uint32_t* run = S.ex + w0;
     // the first sign|mantissa rounds are fetched before the serial decode
     const uint8_t* smb = S.sm + (uint64_t)blk * SPMOE_XC_BLOCK;
-    uint2 sm[SMPRE];
+    uint2 sm[kSmPre];
 #pragma unroll
-    for (int it = 0; it < SMPRE; ++it) sm[it] = __ldg(reinterpret_cast<const uint2*>(smb) + it * 32 + lane);
+    for (int it = 0; it < kSmPre; ++it) sm[it] = __ldg(reinterpret_cast<const uint2*>(smb) + it * 32 + lane);
     if (nw <= (uint32_t)kStageWords) {
       const uint32_t delta = (uint32_t)((uintptr_t)run & 15);  // 0, 4, 8 or 12
       if (lane == 0) {
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(kDecThreads, CTAS) xc_decode_kernel(const DecP
       const uint32_t lo = nib & 0x0f0f0f0fu, hi = (nib >> 4) & 0x0f0f0f0fu;
       // exponents of values 0..3 and 4..7 (no byte carries: base <= 240)
       const uint32_t ea = __byte_perm(lo, hi, 0x5140) + base4, eb = __byte_perm(lo, hi, 0x7362) + base4;
-      const uint2 m = it < SMPRE ? sm[it] : __ldg(reinterpret_cast<const uint2*>(smb) + it * 32 + lane);
+      const uint2 m = it < kSmPre ? sm[it] : __ldg(reinterpret_cast<const uint2*>(smb) + it * 32 + lane);
       uint32_t o[4];
 #pragma unroll
       for (int pr = 0; pr < 4; ++pr) {
@@ -821,27 +824,14 @@ int spmoe_xc_decode_segments_timed(const uint8_t* blob, const spmoe_xc_header* h
     maxblk = std::max(maxblk, S.nblk);
     d += g.n;
   }
-  // variant (A/B switch SPMOE_XC_DEC): resident CTAs per SM the registers
-  // are budgeted for (16 warps, 76 KB of shared memory each) and how many
-  // of the 16 sign|mantissa rounds are fetched before the serial decode
-  static const int var = [] {
-    const char* v = getenv("SPMOE_XC_DEC");
-    const int x = v ? atoi(v) : 0;
-    cudaFuncSetAttribute(xc_decode_kernel<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmemBytes);
-    cudaFuncSetAttribute(xc_decode_kernel<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmemBytes);
-    cudaFuncSetAttribute(xc_decode_kernel<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmemBytes);
-    return x;
+  static const bool attr = [] {
+    cudaFuncSetAttribute(xc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmemBytes);
+    return true;
   }();
-  const int ctas = var == 2 ? 3 : 2;
-  const uint32_t want = (uint32_t)std::max(1, ctas * num_sms() / count);
+  (void)attr;
+  const uint32_t want = (uint32_t)std::max(1, kDecCtas * num_sms() / count);
   const uint32_t gx = std::max(1u, std::min(want, (maxblk + kDecWarps - 1) / kDecWarps));
-  const dim3 grid(gx, count);
-  if (var == 1)
-    xc_decode_kernel<2, 16><<<grid, kDecThreads, kDecSmemBytes, (cudaStream_t)stream>>>(p);
-  else if (var == 2)
-    xc_decode_kernel<3, 8><<<grid, kDecThreads, kDecSmemBytes, (cudaStream_t)stream>>>(p);
-  else
-    xc_decode_kernel<2, 8><<<grid, kDecThreads, kDecSmemBytes, (cudaStream_t)stream>>>(p);
+  xc_decode_kernel<<<dim3(gx, count), kDecThreads, kDecSmemBytes, (cudaStream_t)stream>>>(p);
   return (int)cudaGetLastError();
 }
 

@@ -1,6 +1,6 @@
 """A/B of the XC segment decode across library builds on ONE box (box-to-box
 spread is ~5 %): every build in argv (paths to libspmoe.so variants, plus
-env SPMOE_XC_DEC settings as "path:var") encodes the same Mixtral-8x7B
+an A/B environment switch the build reads as "path:value" in SPMOE_XC_DEC) encodes the same Mixtral-8x7B
 expert with its own encoder (builds may differ in format details that keep
 the header layout) and decodes its W1 segment back to back, interleaved
 round-robin, timed by device clock (globaltimer span of the launch).
