@@ -239,6 +239,8 @@ class SpecMoEEngine:
             if policy.policy is Policy.DRAFT_PREFETCH
             else None
         )
+        if self.ep is not None:
+            self.cutoff = self.ep.agree(self.cutoff)  # one predictor exchange schedule for all ranks
         N = policy.draft_length
         self.max_tokens = max_tokens
         self.draft_kv = KVCache(arch, batch, self.device, max_seq=min(arch.max_seq, max_tokens + N + 8))
@@ -343,6 +345,8 @@ class SpecMoEEngine:
             layers = (self.cutoff + 1) if self.cutoff is not None else 0
             self.k_eff = max(self.policy.prefetch_k, round(pre / (n_it * layers))) if layers else None
             new = effective_cutoff(self.model, self.hw, t, self.policy, self.window_tokens, self.k_eff)
+            if self.ep is not None:
+                new = self.ep.agree(new)
             if new != self.cutoff:
                 self.cutoff = new
                 if self._graphs_ready:
@@ -1003,7 +1007,9 @@ class SpecMoEEngine:
         a, pol = self.arch, self.policy
         B = self.batch
         N = pol.draft_length
-        if remaining is not None and B == 1:
+        if remaining is not None and B == 1 and self.ep is None:
+            # (expert-parallel ranks draft in lockstep: they always draft N
+            # and clip the emitted tokens below)
             N = max(1, min(N, remaining[0]))
         dev = self.device
         st = self.stream

@@ -148,6 +148,18 @@ class ExpertParallelExchange:
         self.dist.all_gather(parts, mine, group=self.host_group)
         return torch.cat(parts, dim=0).numpy()
 
+    def agree(self, value: int | None) -> int | None:
+        """Rank 0's value on every rank (None travels as -1): the predictor
+        exchange runs once per (draft step, layer <= cutoff), so every rank
+        must use the same cutoff even when their measured timings differ."""
+        if self.local_only:
+            return value
+        t = torch.tensor([-1 if value is None else int(value)], dtype=torch.int64)
+        self.dist.broadcast(t, src=self.dist.get_global_rank(self.host_group, 0) if self.group is not None else 0,
+                            group=self.host_group)
+        v = int(t.item())
+        return None if v < 0 else v
+
     def prefetch_share(self, idx: np.ndarray) -> np.ndarray:
         """This rank's experts among all ranks' predictions (see module doc)."""
         return owned_predictions(self.gather_predictions(idx), self.lo, self.hi)

@@ -141,6 +141,8 @@ def _pred_worker(rank, world, port, q, E, n):
             share = ex.prefetch_share(preds[rank])
             ok &= share.tolist() == owned_predictions(np.stack(preds), ex.lo, ex.hi).tolist()
             ok &= bool(((share >= ex.lo) & (share < ex.hi)).all())
+        # every rank runs rank 0's cutoff (None travels too)
+        ok &= ex.agree(3 + rank) == 3 and ex.agree(None if rank == 0 else 5) is None
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()
@@ -149,7 +151,8 @@ def _pred_worker(rank, world, port, q, E, n):
 @pytest.mark.parametrize("world,E", [(2, 8), (3, 60)])
 def test_gloo_prefetch_share(world, E):
     """EP draft_prefetch hand-off: each rank enqueues exactly the union of all
-    ranks' predictions that it owns (ep.ExpertParallelExchange.prefetch_share)."""
+    ranks' predictions that it owns (ep.ExpertParallelExchange.prefetch_share),
+    on the cutoff all ranks agreed on (rank 0's)."""
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
