@@ -248,8 +248,8 @@ class CpuWeights:
 
 def _draft_proxy(a: Arch, mean: np.ndarray, shared: np.ndarray | None, router: np.ndarray) -> np.ndarray:
     """model._draft_proxy restated: mean routed expert with W2 scaled by the
-    gate mass, concatenated along F with the shared expert (W2 x 0.5 for a
-    sigmoid-gated shared expert)."""
+    gate mass, concatenated along F with the shared expert (not with a
+    sigmoid-gated one: the draft runs it beside, CpuSD._draft_ffn)."""
     H, F = a.hidden, a.ffn
     mass = gate_mass(O.bf16_bits_to_f32(router), a.top_k, a.renorm)
     w1 = mean[: F * H].reshape(F, H)
@@ -257,14 +257,12 @@ def _draft_proxy(a: Arch, mean: np.ndarray, shared: np.ndarray | None, router: n
     w2 = mean[2 * F * H:].reshape(H, F).copy()
     if mass != 1.0:
         O.lib().cpu_scale_bf16(w2.ctypes.data, w2.size, float(mass))
-    if shared is None:
+    if shared is None or a.shared_gate:
         return np.concatenate([w1.reshape(-1), w3.reshape(-1), w2.reshape(-1)])
     Fs = a.shared_ffn
     s1 = shared[: Fs * H].reshape(Fs, H)
     s3 = shared[Fs * H: 2 * Fs * H].reshape(Fs, H)
-    s2 = shared[2 * Fs * H:].reshape(H, Fs).copy()
-    if a.shared_gate:
-        O.lib().cpu_scale_bf16(s2.ctypes.data, s2.size, 0.5)
+    s2 = shared[2 * Fs * H:].reshape(H, Fs)
     d1 = np.concatenate([w1, s1], axis=0)
     d3 = np.concatenate([w3, s3], axis=0)
     d2 = np.concatenate([w2, s2], axis=1)
@@ -302,6 +300,18 @@ class CpuSD:
         _, y = O.lm_expert_ffn(blob, self.a.hidden, F, hn, n=n)
         return O.moe_combine(y, np.arange(n, dtype=np.int32), None, n, self.a.hidden, 1, residual=x)
 
+    def _draft_ffn(self, l: int, hn: np.ndarray, x: np.ndarray) -> np.ndarray:
+        """engine._draft_ffn restated: the dense FFN, or for a sigmoid-gated
+        shared expert the mean-expert FFN + the gated shared expert (K4)."""
+        a, lw = self.a, self.w.layers[l]
+        if not (a.shared_gate and lw.shared is not None and lw.sgate is not None):
+            return self._dense(lw.draft, a.d_ffn, hn, x)
+        n = hn.shape[0]
+        _, y = O.lm_expert_ffn(lw.draft, a.hidden, a.d_ffn, hn, n=n)
+        _, ys = O.lm_expert_ffn(lw.shared, a.hidden, a.shared_ffn, hn, n=n)
+        _, _, _, sg = O.router_topk(hn, lw.router, 1, a.renorm, lw.sgate)
+        return O.moe_combine(y, np.arange(n, dtype=np.int32), None, n, a.hidden, 1, ys=ys, sg=sg, residual=x)
+
     def draft_forward(self, tokens: np.ndarray, start: np.ndarray, step: int | None) -> np.ndarray:
         """tokens [B, T] -> last-token logits [B, V] f32 (draft KV appended)."""
         a, w = self.a, self.w
@@ -315,7 +325,7 @@ class CpuSD:
                 last = hn.reshape(B, T, -1)[:, -1, :]
                 _, idx, _, _ = O.router_topk(last, lw.router, self.pk, True)
                 self.predictions.append((step, l, idx))
-            x = self._dense(lw.draft, a.d_ffn, hn, x)
+            x = self._draft_ffn(l, hn, x)
         last = np.ascontiguousarray(x.reshape(B, T, -1)[:, -1, :])
         return O.lm_linear(w.lm_head, a.hidden, last, norm_w=w.final_norm, eps=a.rms_eps, f32=True)
 

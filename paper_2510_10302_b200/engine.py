@@ -425,6 +425,22 @@ class SpecMoEEngine:
         self._ffn(blob, [0], 1, xn, F, 1, off, perm, s.hd, s.yd, T, s)
         return K.moe_combine(s.yd, perm, None, T, self.arch.hidden, 1, residual=resid, out=out)
 
+    def _draft_ffn(self, l: int, xn: torch.Tensor, resid: torch.Tensor, s: _Scratch) -> torch.Tensor:
+        """The draft's MLP at layer l: its dense FFN; with a sigmoid-gated
+        shared expert (Qwen1.5-MoE) the mean-expert FFN plus the target's
+        shared expert under its per-token gate (K1's shared-gate output),
+        combined by K4 like the target's shared path."""
+        a, lw = self.arch, self.weights.layers[l]
+        if not (a.shared_gate and lw.shared is not None and lw.shared_gate is not None):
+            return self._dense_ffn(lw.draft_ffn, a.d_ffn, xn, resid, s)
+        T = xn.shape[0]
+        off, pm = s.dense(T)
+        self._ffn(lw.draft_ffn, [0], 1, xn, a.d_ffn, 1, off, pm, s.hd, s.yd, T, s)
+        ys = s.y[:T]
+        self._ffn(lw.shared, [0], 1, xn, a.shared_ffn, 1, off, pm, s.hd, ys, T, s)
+        _, _, _, sg = K.router_topk(xn, lw.router, 1, a.renorm, shared_gate_w=lw.shared_gate)
+        return K.moe_combine(s.yd, pm, None, T, a.hidden, 1, residual=resid, y_shared=ys, shared_gate=sg)
+
     def _timed_ffn(self, experts, counts, slots, mask, xn, offsets, perm, s, maxtok, k=None) -> None:
         """K3 over ``experts`` (one launch per kernel path: experts are
         grouped by their own token counts); with ``time_k3`` set, brackets
@@ -712,7 +728,7 @@ class SpecMoEEngine:
                 else:
                     self.predictor.predict_at(ring_base + l, hn[:, -1, :].contiguous(), lw.router, pk, True,
                                               self.pred_w, self.pred_idx)
-            x = self._dense_ffn(lw.draft_ffn, a.d_ffn, hn.reshape(B * T, -1), x.reshape(B * T, -1), s).view(B, T, -1)
+            x = self._draft_ffn(l, hn.reshape(B * T, -1), x.reshape(B * T, -1), s).view(B, T, -1)
         return lm_logits(w, x[:, -1, :])
 
     # ------------------------------------------------------------ CUDA graphs

@@ -100,8 +100,10 @@ class ArchSpec:
     @property
     def d_ffn(self) -> int:
         """Draft dense FFN width: explicit, else the derived proxy (mean routed
-        expert, plus the shared expert(s) concatenated along F)."""
-        return self.draft_ffn or (self.ffn + self.shared_ffn)
+        expert, plus the shared expert(s) concatenated along F -- unless the
+        shared expert is sigmoid-gated: then the draft runs the target's
+        shared expert and gate beside the mean expert, see _draft_proxy)."""
+        return self.draft_ffn or (self.ffn + (0 if self.shared_gate else self.shared_ffn))
 
     @property
     def qkv_dim(self) -> int:
@@ -502,15 +504,16 @@ def _draft_proxy(arch: ArchSpec, mean: torch.Tensor, shared: torch.Tensor | None
     w1 = mean[: F * H].view(F, H)
     w3 = mean[F * H : 2 * F * H].view(F, H)
     w2 = (mean[2 * F * H :].view(H, F).float() * mass).to(mean.dtype)
-    if shared is None:
+    if shared is None or arch.shared_gate:
+        # a sigmoid-gated shared expert (Qwen1.5-MoE) cannot be folded into
+        # one dense FFN (its gate is per token): the draft applies the
+        # target's shared expert and gate itself (engine._draft_ffn)
         return torch.cat([w1.reshape(-1), w3.reshape(-1), w2.reshape(-1)]).view(1, -1)
     Fs = arch.shared_ffn
     s = shared[0]
     s1 = s[: Fs * H].view(Fs, H)
     s3 = s[Fs * H : 2 * Fs * H].view(Fs, H)
     s2 = s[2 * Fs * H :].view(H, Fs)
-    if arch.shared_gate:
-        s2 = (s2.float() * 0.5).to(s.dtype)
     d1 = torch.cat([w1, s1], dim=0)
     d3 = torch.cat([w3, s3], dim=0)
     d2 = torch.cat([w2, s2], dim=1)

@@ -44,8 +44,9 @@ def test_draft_proxy_shapes_and_mass():
     router = (torch.randn(8, H) / 8).to(torch.bfloat16)
     d = _draft_proxy(a, mean, None, router)
     assert d.shape == (1, 3 * F * H) and torch.equal(d[0], mean)  # renorm: mass 1, no shared
-    b = replace(a, renorm=False, shared_ffn=64, shared_gate=True)
     shared = torch.randn(1, 3 * 64 * H).to(torch.bfloat16)
+    # an ungated shared expert is concatenated along F
+    b = replace(a, renorm=False, shared_ffn=64, shared_gate=False)
     d2 = _draft_proxy(b, mean, shared, router)
     Fd = F + 64
     assert b.d_ffn == Fd and d2.shape == (1, 3 * Fd * H)
@@ -54,6 +55,13 @@ def test_draft_proxy_shapes_and_mass():
     w2 = d2[0, 2 * Fd * H :].view(H, Fd).float()
     ratio = (w2[:, :F] / mean[2 * F * H :].view(H, F).float()).median().item()
     assert 0.0 < ratio < 1.0  # top-k mass without renorm
+    assert torch.equal(w2[:, F:], shared[0, 2 * 64 * H :].view(H, 64).float())
+    # a sigmoid-gated one stays out of the dense FFN (the draft runs it
+    # under its per-token gate beside the mean expert)
+    g = replace(b, shared_gate=True)
+    d3 = _draft_proxy(g, mean, shared, router)
+    assert g.d_ffn == F and d3.shape == (1, 3 * F * H)
+    assert torch.equal(d3[0, : 2 * F * H], mean[: 2 * F * H])
 
 
 def test_oracle_fill_matches_seed_helper(oracle):
