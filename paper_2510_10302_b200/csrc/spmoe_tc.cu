@@ -19,6 +19,7 @@
 // spmoe_kernels.cu is the bit-exact one.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "../../include/spmoe.h"
@@ -954,7 +955,8 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const int no_pdl = getenv("SPMOE_NO_PDL") != nullptr;  // A/B switch
+  cfg.numAttrs = no_pdl ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 

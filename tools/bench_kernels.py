@@ -24,6 +24,10 @@ CASES = {
     "mixtral_T1": dict(H=4096, F=14336, E=8, k=2, T=1),
     "mixtral_T9": dict(H=4096, F=14336, E=8, k=2, T=9),
     "mixtral_T72": dict(H=4096, F=14336, E=8, k=2, T=72),
+    # prefill-sized batches: 128 / 512 routed tokens per expert (the
+    # tensor-core regime: report tensor-pipe use for B(N+1) >= 32)
+    "mixtral_T512": dict(H=4096, F=14336, E=8, k=2, T=512),
+    "mixtral_T2048": dict(H=4096, F=14336, E=8, k=2, T=2048),
     "deepseek_T5": dict(H=2048, F=1408, E=64, k=6, T=5),
     "qwen_T5": dict(H=2048, F=1408, E=60, k=4, T=5),
     "qwen_T72": dict(H=2048, F=1408, E=60, k=4, T=72),
