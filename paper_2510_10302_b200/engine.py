@@ -740,9 +740,21 @@ class SpecMoEEngine:
             fn()  # warm-up outside capture (kernel selection, workspaces)
         torch.cuda.current_stream(self.device).wait_stream(side)
         # thread_local: the prefetch worker thread may call CUDA (event
-        # queries, copies on its own stream) while the main thread captures
-        with torch.cuda.graph(g, capture_error_mode="thread_local"):
-            fn()
+        # queries, copies on its own stream) while the main thread captures.
+        # Python's GC stays off during the capture: a collected object whose
+        # finaliser frees pinned or device memory (cudaFreeHost, cudaFree) on
+        # this thread would invalidate it (seen when earlier work in the
+        # process left such objects in reference cycles)
+        import gc
+
+        gc_on = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                fn()
+        finally:
+            if gc_on:
+                gc.enable()
         return g
 
     def _ensure_graphs(self) -> None:
