@@ -131,6 +131,23 @@ __global__ void __launch_bounds__(256) rope_kv_kernel(const uint16_t* __restrict
 constexpr int kAttnQC = 8;
 constexpr int kAttnNW = 8;
 
+// The PL bf16 of row `key` that lane owns (dims lane*PL ..), as fp32: one
+// 8-byte (PL = 4) or 4-byte (PL = 2) load.
+template <int PL>
+__device__ __forceinline__ void load_row(const uint16_t* base, int key, int hd, int lane, float (&out)[PL]) {
+  const uint16_t* p = base + (int64_t)key * hd + lane * PL;
+  if constexpr (PL == 4) {
+    const uint2 w = *reinterpret_cast<const uint2*>(p);
+    out[0] = bf16_lo(w.x);
+    out[1] = bf16_hi(w.x);
+    out[2] = bf16_lo(w.y);
+    out[3] = bf16_hi(w.y);
+  } else {
+#pragma unroll
+    for (int j = 0; j < PL; ++j) out[j] = bf16_to_f32(p[j]);
+  }
+}
+
 template <int HD>
 __global__ void __launch_bounds__(32 * kAttnNW) attn_kernel(const uint16_t* __restrict__ q,
                                                          const uint16_t* __restrict__ kc,
@@ -162,19 +179,44 @@ __global__ void __launch_bounds__(32 * kAttnNW) attn_kernel(const uint16_t* __re
                         : 0.0f;
   const uint16_t* kb = kc + ((int64_t)b * nkv + kh) * S * HD;
   const uint16_t* vb = vc + ((int64_t)b * nkv + kh) * S * HD;
-  // pass 1: scores
-  for (int key = warp; key < klen; key += NW) {
-    float kv[PL];
+  // pass 1: scores.  The K rows of KU keys are loaded together (one vector
+  // load per lane per key) before their dot products: same arithmetic per
+  // key, KU memory latencies overlapped instead of one per key.
+  constexpr int KU = 4;
+  for (int key0 = warp; key0 < klen; key0 += NW * KU) {
+    float kv[KU][PL];
 #pragma unroll
-    for (int j = 0; j < PL; ++j) kv[j] = bf16_to_f32(kb[(int64_t)key * HD + lane * PL + j]);
+    for (int u = 0; u < KU; ++u) {
+      const int key = key0 + u * NW;
+      load_row<PL>(kb, key < klen ? key : key0, HD, lane, kv[u]);
+    }
+    // every (key, query) lane partial first, then the xor butterflies of
+    // all of them level by level (the same per-value order as
+    // warp_sum_fixed, with KU*QC independent shuffle chains in flight)
+    float sp[KU][QC];
 #pragma unroll
-    for (int i = 0; i < QC; ++i) {
-      if (i >= nq || key > p0 + i) continue;  // causal (warp-uniform)
-      float s = 0.0f;
+    for (int u = 0; u < KU; ++u)
 #pragma unroll
-      for (int j = 0; j < PL; ++j) s = __fadd_rn(s, __fmul_rn(qv[i][j], kv[j]));
-      s = warp_sum_fixed(s);
-      if (lane == 0) s_p[i * S + key] = s;
+      for (int i = 0; i < QC; ++i) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int j = 0; j < PL; ++j) acc = __fadd_rn(acc, __fmul_rn(qv[i][j], kv[u][j]));
+        sp[u][i] = acc;
+      }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+      for (int u = 0; u < KU; ++u)
+#pragma unroll
+        for (int i = 0; i < QC; ++i) sp[u][i] = __fadd_rn(sp[u][i], __shfl_xor_sync(SPMOE_FULL_MASK, sp[u][i], off));
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const int key = key0 + u * NW;
+#pragma unroll
+        for (int i = 0; i < QC; ++i)
+          if (key < klen && i < nq && key <= p0 + i) s_p[i * S + key] = sp[u][i];  // causal keys only
+      }
     }
   }
   __syncthreads();
@@ -197,17 +239,25 @@ __global__ void __launch_bounds__(32 * kAttnNW) attn_kernel(const uint16_t* __re
 #pragma unroll
     for (int j = 0; j < PL; ++j) acc[i][j] = 0.0f;
   }
-  for (int key = warp; key < klen; key += NW) {
-    float vv[PL];
+  for (int key0 = warp; key0 < klen; key0 += NW * KU) {
+    float vv[KU][PL];
 #pragma unroll
-    for (int j = 0; j < PL; ++j) vv[j] = bf16_to_f32(vb[(int64_t)key * HD + lane * PL + j]);
+    for (int u = 0; u < KU; ++u) {
+      const int key = key0 + u * NW;
+      load_row<PL>(vb, key < klen ? key : key0, HD, lane, vv[u]);
+    }
 #pragma unroll
-    for (int i = 0; i < QC; ++i) {
-      if (i >= nq || key > p0 + i) continue;
-      const float pj = s_p[i * S + key];
-      l[i] = __fadd_rn(l[i], pj);
+    for (int u = 0; u < KU; ++u) {  // keys ascending: the stream's fixed order
+      const int key = key0 + u * NW;
+      if (key >= klen) break;
 #pragma unroll
-      for (int j = 0; j < PL; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(pj, vv[j]));
+      for (int i = 0; i < QC; ++i) {
+        if (i >= nq || key > p0 + i) continue;
+        const float pj = s_p[i * S + key];
+        l[i] = __fadd_rn(l[i], pj);
+#pragma unroll
+        for (int j = 0; j < PL; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(pj, vv[u][j]));
+      }
     }
   }
 #pragma unroll

@@ -279,6 +279,40 @@ __device__ __forceinline__ void stream_rows(const uint4* const (&wr)[NR], const 
   }
 }
 
+// Same dot products with the activations pre-widened to fp32 in shared
+// memory (two float4 planes per 16-byte chunk: elements 0-3 and 4-7, so the
+// lanes' loads stay contiguous): no per-row bf16 unpack of the activations,
+// identical FMA order.
+template <int TT, int UNR>
+__device__ __forceinline__ void stream_rows_f32(const uint4* wr, const float4* act, int nchunks, int nt, int lane,
+                                                float (&acc)[TT]) {
+  for (int base = 0; base < nchunks; base += 32 * UNR) {
+    uint4 w[UNR];
+#pragma unroll
+    for (int i = 0; i < UNR; ++i) {
+      const int c = base + lane + 32 * i;
+      w[i] = (c < nchunks) ? ldg_stream(wr + c) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int i = 0; i < UNR; ++i) {
+      const int c = base + lane + 32 * i;
+      if (c < nchunks) {
+        float wf[8];
+        unpack8(w[i], wf);
+#pragma unroll
+        for (int t = 0; t < TT; ++t) {
+          if (t < nt) {
+            const float4 a0 = act[(2 * t) * nchunks + c], a1 = act[(2 * t + 1) * nchunks + c];
+            const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+            for (int v = 0; v < 8; ++v) acc[t] = fmaf(wf[v], af[v], acc[t]);
+          }
+        }
+      }
+    }
+  }
+}
+
 // K3 phase kernel.  UP: rows f of W1 and W3 (NR=2, K=H) -> h = bf16(silu(g)*u);
 // DOWN: rows h of W2 (NR=1, K=F) -> y fp32.  The (active expert, 16-row
 // tile) space is split into one contiguous range per CTA (balanced to one
@@ -423,7 +457,9 @@ __device__ __forceinline__ uint32_t rms_apply2(uint32_t xw, uint32_t gw, float r
 
 template <int TT>
 __global__ void __launch_bounds__(kFfnThreads, 1) linear_kernel(const LinParams p) {
-  extern __shared__ __align__(16) uint4 s_act[];
+  // activations widened to fp32: plane 2t (elements 0-3 of every chunk) and
+  // plane 2t+1 (elements 4-7) of token t
+  extern __shared__ __align__(16) float4 s_actf[];
   __shared__ float s_r[TT];
   constexpr int kRowsPerTile = kFfnThreads / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -450,21 +486,24 @@ __global__ void __launch_bounds__(kFfnThreads, 1) linear_kernel(const LinParams 
         v = make_uint4(rms_apply2(v.x, g.x, r), rms_apply2(v.y, g.y, r), rms_apply2(v.z, g.z, r),
                        rms_apply2(v.w, g.w, r));
       }
-      s_act[t * nchunks + c] = v;
+      float f[8];
+      unpack8(v, f);
+      s_actf[(2 * t) * nchunks + c] = make_float4(f[0], f[1], f[2], f[3]);
+      s_actf[(2 * t + 1) * nchunks + c] = make_float4(f[4], f[5], f[6], f[7]);
     }
     __syncthreads();
     for (int tile = t_begin; tile < t_end; ++tile) {
       const int row = tile * kRowsPerTile + warp;
       if (row >= p.N) continue;
-      const uint4* wr[1] = {reinterpret_cast<const uint4*>(p.w + (int64_t)row * p.K)};
-      float acc[1][TT];
+      const uint4* wr = reinterpret_cast<const uint4*>(p.w + (int64_t)row * p.K);
+      float acc[TT];
 #pragma unroll
-      for (int t = 0; t < TT; ++t) acc[0][t] = 0.0f;
-      stream_rows<TT, 1, 16>(wr, s_act, nchunks, nt, nchunks, lane, acc);
+      for (int t = 0; t < TT; ++t) acc[t] = 0.0f;
+      stream_rows_f32<TT, 16>(wr, s_actf, nchunks, nt, lane, acc);
 #pragma unroll
       for (int t = 0; t < TT; ++t) {
         if (t < nt) {
-          const float s = warp_sum_fixed(acc[0][t]);
+          const float s = warp_sum_fixed(acc[t]);
           if (lane == t) {
             const int64_t tt = t0 + t;
             if (p.y_f32 != nullptr) p.y_f32[tt * p.ldy + row] = s;
@@ -483,7 +522,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) linear_kernel(const LinParams 
 
 template <int TT>
 int launch_linear(const LinParams& p, cudaStream_t s) {
-  const size_t smem = (size_t)TT * p.K * 2;
+  const size_t smem = (size_t)TT * p.K * 4;  // fp32 activation stage
   if (smem > (size_t)kActSmemCap) return (int)cudaErrorInvalidValue;
   static bool configured = false;
   if (!configured) {
@@ -786,7 +825,7 @@ int spmoe_linear(const uint16_t* w, const uint16_t* x, int64_t ldx, int T, int K
   p.T = T; p.K = K; p.N = N;
   p.y_f32 = y_f32; p.ldy = ldy; p.y_bf16 = y_bf16; p.resid = resid;
   int tt = T <= 1 ? 1 : T <= 2 ? 2 : T <= 4 ? 4 : T <= 8 ? 8 : 16;
-  while (tt > 1 && (size_t)tt * K * 2 > (size_t)kActSmemCap) tt >>= 1;
+  while (tt > 1 && (size_t)tt * K * 4 > (size_t)kActSmemCap) tt >>= 1;
   cudaStream_t s = (cudaStream_t)stream;
   switch (tt) {
     case 1: return launch_linear<1>(p, s);
