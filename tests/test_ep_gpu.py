@@ -121,7 +121,11 @@ def _free_port():
     return p
 
 
-def test_ep_engine_nccl_group_of_one(oracle):
+@pytest.mark.parametrize("policy_kind,cutoff", [("on_demand", None), ("draft_prefetch", 3)])
+def test_ep_engine_nccl_group_of_one(oracle, policy_kind, cutoff):
+    """The all-to-all path over a real (one-rank) NCCL group; with
+    draft_prefetch also the host-side prediction exchange and the cutoff
+    agreement over the gloo group the exchange creates beside it."""
     import torch.distributed as dist
 
     if dist.is_initialized():
@@ -130,12 +134,14 @@ def test_ep_engine_nccl_group_of_one(oracle):
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
-        eng = make_engine(expert_parallel=True, policy_kind="on_demand", cutoff=None, capacity=16, capture=(1,))
+        eng = make_engine(expert_parallel=True, policy_kind=policy_kind, cutoff=cutoff, capacity=16, capture=(1,))
         try:
-            assert not eng.ep.local_only
+            assert not eng.ep.local_only and eng.ep.host_group is not None
             _run(eng, steps=3)
             check_layer_captures(eng, oracle)
             check_acceptance(eng, oracle)
+            if policy_kind == "draft_prefetch":
+                assert eng.cutoff == cutoff and eng.report().counters["prefetch_insertions"] > 0
         finally:
             eng.close()
     finally:
