@@ -28,38 +28,45 @@ using namespace spmoe;
 namespace {
 
 // ------------------------------------------------------------------ RMSNorm
-// One warp per row; H % 8 == 0.  ss = dot_fixed(x, x) (lane-strided 8-value
-// chunks, butterfly), r = 1 / sqrt(ss / H + eps), y = bf16((x * r) * w).
+// One CTA per row; H % 8 == 0.  Warp 0 computes ss = dot_fixed(x, x)
+// (lane-strided 8-value chunks, butterfly) and r = 1 / sqrt(ss / H + eps);
+// every thread of the CTA then writes its chunks of y = bf16((x * r) * w)
+// (elementwise: the split does not change a bit).
 __global__ void __launch_bounds__(256) rms_norm_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w,
                                                        int rows, int H, float eps, uint16_t* __restrict__ out) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  __shared__ float s_r;
+  const int row = blockIdx.x;
   const int lane = threadIdx.x & 31;
-  if (warp >= rows) return;
-  const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)warp * H);
+  if (row >= rows) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)row * H);
   const int n8 = H / 8;
-  float ss = 0.0f;
-  // loads of U rounds in flight together; the FMA order is unchanged
-  constexpr int U = 8;
-  for (int c0 = lane; c0 < n8; c0 += 32 * U) {
-    uint4 xa[U];
+  if (threadIdx.x < 32) {
+    float ss = 0.0f;
+    // loads of U rounds in flight together; the FMA order is unchanged
+    constexpr int U = 8;
+    for (int c0 = lane; c0 < n8; c0 += 32 * U) {
+      uint4 xa[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (c0 + 32 * u < n8) xa[u] = xr[c0 + 32 * u];
+      for (int u = 0; u < U; ++u)
+        if (c0 + 32 * u < n8) xa[u] = xr[c0 + 32 * u];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (c0 + 32 * u < n8) {
-        float a[8];
-        unpack8(xa[u], a);
+      for (int u = 0; u < U; ++u) {
+        if (c0 + 32 * u < n8) {
+          float a[8];
+          unpack8(xa[u], a);
 #pragma unroll
-        for (int v = 0; v < 8; ++v) ss = fmaf(a[v], a[v], ss);  // bf16 squares are exact
+          for (int v = 0; v < 8; ++v) ss = fmaf(a[v], a[v], ss);  // bf16 squares are exact
+        }
       }
     }
+    ss = warp_sum_fixed(ss);
+    if (lane == 0) s_r = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)H), eps)));
   }
-  ss = warp_sum_fixed(ss);
-  const float r = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)H), eps)));
+  __syncthreads();
+  const float r = s_r;
   const uint4* wr = reinterpret_cast<const uint4*>(w);
-  uint4* orow = reinterpret_cast<uint4*>(out + (int64_t)warp * H);
-  for (int i = lane; i < n8; i += 32) {
+  uint4* orow = reinterpret_cast<uint4*>(out + (int64_t)row * H);
+  for (int i = threadIdx.x; i < n8; i += blockDim.x) {
     const uint4 v = xr[i], g = wr[i];
     const uint32_t u[4] = {v.x, v.y, v.z, v.w}, gw[4] = {g.x, g.y, g.z, g.w};
     uint32_t o[4];
@@ -74,7 +81,9 @@ __global__ void __launch_bounds__(256) rms_norm_kernel(const uint16_t* __restric
 }
 
 // ------------------------------------------------------------- RoPE + KV
-// One CTA per (token row); threads walk the nh + 2 nkv heads' dims.
+// grid.x = token row, grid.y = 256-element slices of the row's nh + 2 nkv
+// heads' dims: one element per thread, so a row's loads are all in flight
+// at once (elementwise, the arithmetic does not depend on the split).
 // y[d] = bf16(x[d] * cos[pos][d] + rot[d] * sin[pos][d]), rot = [-x2, x1],
 // the two products and the sum each IEEE-rounded.  Positions at or beyond
 // the cache (S) or the RoPE table (max_pos) write nothing (the host checks
@@ -94,7 +103,7 @@ __global__ void __launch_bounds__(256) rope_kv_kernel(const uint16_t* __restrict
   const float* sn = sin_t + pos * hd;
   const int half = hd / 2;
   const int total = (nh + 2 * nkv) * hd;
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < total; i += gridDim.y * blockDim.x) {
     const int head = i / hd, d = i % hd;
     const float x = bf16_to_f32(src[i]);
     if (head < nh + nkv) {
@@ -292,8 +301,7 @@ extern "C" {
 int spmoe_rms_norm(const uint16_t* x, const uint16_t* w, int rows, int H, float eps, uint16_t* out, void* stream) {
   if (rows < 0 || H <= 0 || H % 8 || !x || !w || !out) return (int)cudaErrorInvalidValue;
   if (rows == 0) return 0;
-  const int threads = 256, per = threads / 32;
-  rms_norm_kernel<<<(rows + per - 1) / per, threads, 0, (cudaStream_t)stream>>>(x, w, rows, H, eps, out);
+  rms_norm_kernel<<<rows, 256, 0, (cudaStream_t)stream>>>(x, w, rows, H, eps, out);
   return (int)cudaGetLastError();
 }
 
@@ -304,8 +312,9 @@ int spmoe_rope_kv(const uint16_t* qkv, const float* cos_t, const float* sin_t, c
       !k_cache || !v_cache || !cos_t || !sin_t || !start)
     return (int)cudaErrorInvalidValue;
   if (B * T == 0) return 0;
-  rope_kv_kernel<<<B * T, 256, 0, (cudaStream_t)stream>>>(qkv, cos_t, sin_t, start, T, nh, nkv, hd, S, max_pos,
-                                                          q_out, k_cache, v_cache);
+  const int slices = ((nh + 2 * nkv) * hd + 255) / 256;
+  rope_kv_kernel<<<dim3(B * T, slices), 256, 0, (cudaStream_t)stream>>>(qkv, cos_t, sin_t, start, T, nh, nkv, hd, S,
+                                                                      max_pos, q_out, k_cache, v_cache);
   return (int)cudaGetLastError();
 }
 
