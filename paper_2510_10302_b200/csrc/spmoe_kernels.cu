@@ -283,7 +283,7 @@ __device__ __forceinline__ void stream_rows(const uint4* const (&wr)[NR], const 
 // memory (two float4 planes per 16-byte chunk: elements 0-3 and 4-7, so the
 // lanes' loads stay contiguous): no per-row bf16 unpack of the activations,
 // identical FMA order.
-template <int TT, int UNR>
+template <int TT, int UNR, bool FULL>
 __device__ __forceinline__ void stream_rows_f32(const uint4* wr, const float4* act, int nchunks, int nt, int lane,
                                                 float (&acc)[TT]) {
   for (int base = 0; base < nchunks; base += 32 * UNR) {
@@ -299,13 +299,29 @@ __device__ __forceinline__ void stream_rows_f32(const uint4* wr, const float4* a
       if (c < nchunks) {
         float wf[8];
         unpack8(w[i], wf);
+        if (FULL) {
+          // every token row present: no branches, the TT independent FMA
+          // chains interleave (each keeps its own element order)
+          float af[TT][8];
 #pragma unroll
-        for (int t = 0; t < TT; ++t) {
-          if (t < nt) {
+          for (int t = 0; t < TT; ++t) {
             const float4 a0 = act[(2 * t) * nchunks + c], a1 = act[(2 * t + 1) * nchunks + c];
-            const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            af[t][0] = a0.x; af[t][1] = a0.y; af[t][2] = a0.z; af[t][3] = a0.w;
+            af[t][4] = a1.x; af[t][5] = a1.y; af[t][6] = a1.z; af[t][7] = a1.w;
+          }
 #pragma unroll
-            for (int v = 0; v < 8; ++v) acc[t] = fmaf(wf[v], af[v], acc[t]);
+          for (int v = 0; v < 8; ++v)
+#pragma unroll
+            for (int t = 0; t < TT; ++t) acc[t] = fmaf(wf[v], af[t][v], acc[t]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < TT; ++t) {
+            if (t < nt) {
+              const float4 a0 = act[(2 * t) * nchunks + c], a1 = act[(2 * t + 1) * nchunks + c];
+              const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+              for (int v = 0; v < 8; ++v) acc[t] = fmaf(wf[v], af[v], acc[t]);
+            }
           }
         }
       }
@@ -499,7 +515,10 @@ __global__ void __launch_bounds__(kFfnThreads, 1) linear_kernel(const LinParams 
       float acc[TT];
 #pragma unroll
       for (int t = 0; t < TT; ++t) acc[t] = 0.0f;
-      stream_rows_f32<TT, 16>(wr, s_actf, nchunks, nt, lane, acc);
+      if (nt == TT)
+        stream_rows_f32<TT, 8, true>(wr, s_actf, nchunks, nt, lane, acc);
+      else
+        stream_rows_f32<TT, 8, false>(wr, s_actf, nchunks, nt, lane, acc);
 #pragma unroll
       for (int t = 0; t < TT; ++t) {
         if (t < nt) {
@@ -824,13 +843,19 @@ int spmoe_linear(const uint16_t* w, const uint16_t* x, int64_t ldx, int T, int K
   p.w = w; p.x = x; p.norm_w = norm_w; p.eps = eps; p.ldx = ldx;
   p.T = T; p.K = K; p.N = N;
   p.y_f32 = y_f32; p.ldy = ldy; p.y_bf16 = y_bf16; p.resid = resid;
-  int tt = T <= 1 ? 1 : T <= 2 ? 2 : T <= 4 ? 4 : T <= 8 ? 8 : 16;
-  while (tt > 1 && (size_t)tt * K * 4 > (size_t)kActSmemCap) tt >>= 1;
+  // the register tile matches T exactly up to 8 rows (no predicated-off
+  // token lanes in the inner loop), then 16-row groups
+  int tt = T <= 8 ? T : 16;
+  while (tt > 1 && (size_t)tt * K * 4 > (size_t)kActSmemCap) tt = tt > 8 ? 8 : tt / 2;
   cudaStream_t s = (cudaStream_t)stream;
   switch (tt) {
     case 1: return launch_linear<1>(p, s);
     case 2: return launch_linear<2>(p, s);
+    case 3: return launch_linear<3>(p, s);
     case 4: return launch_linear<4>(p, s);
+    case 5: return launch_linear<5>(p, s);
+    case 6: return launch_linear<6>(p, s);
+    case 7: return launch_linear<7>(p, s);
     case 8: return launch_linear<8>(p, s);
     default: return launch_linear<16>(p, s);
   }
