@@ -283,6 +283,41 @@ __device__ __forceinline__ void stream_rows(const uint4* const (&wr)[NR], const 
 // memory (two float4 planes per 16-byte chunk: elements 0-3 and 4-7, so the
 // lanes' loads stay contiguous): no per-row bf16 unpack of the activations,
 // identical FMA order.
+// Two weight rows per pass sharing every activation load (half the shared-
+// memory traffic per row); each row's FMA chains keep their order.
+template <int TT, int UNR>
+__device__ __forceinline__ void stream_rows2_f32(const uint4* wr0, const uint4* wr1, const float4* act, int nchunks,
+                                                 int lane, float (&acc0)[TT], float (&acc1)[TT]) {
+  for (int base = 0; base < nchunks; base += 32 * UNR) {
+    uint4 w0[UNR], w1[UNR];
+#pragma unroll
+    for (int i = 0; i < UNR; ++i) {
+      const int c = base + lane + 32 * i;
+      w0[i] = (c < nchunks) ? ldg_stream(wr0 + c) : make_uint4(0u, 0u, 0u, 0u);
+      w1[i] = (c < nchunks) ? ldg_stream(wr1 + c) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int i = 0; i < UNR; ++i) {
+      const int c = base + lane + 32 * i;
+      if (c < nchunks) {
+        float wf0[8], wf1[8];
+        unpack8(w0[i], wf0);
+        unpack8(w1[i], wf1);
+#pragma unroll
+        for (int t = 0; t < TT; ++t) {
+          const float4 a0 = act[(2 * t) * nchunks + c], a1 = act[(2 * t + 1) * nchunks + c];
+          const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            acc0[t] = fmaf(wf0[v], af[v], acc0[t]);
+            acc1[t] = fmaf(wf1[v], af[v], acc1[t]);
+          }
+        }
+      }
+    }
+  }
+}
+
 template <int TT, int UNR, bool FULL>
 __device__ __forceinline__ void stream_rows_f32(const uint4* wr, const float4* act, int nchunks, int nt, int lane,
                                                 float (&acc)[TT]) {
@@ -480,10 +515,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) linear_kernel(const LinParams 
   constexpr int kRowsPerTile = kFfnThreads / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nchunks = p.K >> 3;
-  const int tiles = (p.N + kRowsPerTile - 1) / kRowsPerTile;
-  const int t_begin = (int)((int64_t)tiles * blockIdx.x / gridDim.x);
-  const int t_end = (int)((int64_t)tiles * (blockIdx.x + 1) / gridDim.x);
-  if (t_begin >= t_end) return;
+  const int r_begin = (int)((int64_t)p.N * blockIdx.x / gridDim.x);
+  const int r_end = (int)((int64_t)p.N * (blockIdx.x + 1) / gridDim.x);
+  if (r_begin >= r_end) return;
   for (int t0 = 0; t0 < p.T; t0 += TT) {
     const int nt = min(TT, p.T - t0);
     __syncthreads();  // previous group's readers are done
@@ -508,9 +542,40 @@ __global__ void __launch_bounds__(kFfnThreads, 1) linear_kernel(const LinParams 
       s_actf[(2 * t + 1) * nchunks + c] = make_float4(f[4], f[5], f[6], f[7]);
     }
     __syncthreads();
-    for (int tile = t_begin; tile < t_end; ++tile) {
-      const int row = tile * kRowsPerTile + warp;
-      if (row >= p.N) continue;
+    // this CTA's rows [r_begin, r_end); warp w takes rows r_begin + w + 16 k,
+    // two at a time while it has two (full token groups), else one
+    auto emit = [&](int row, const float (&acc)[TT]) {
+#pragma unroll
+      for (int t = 0; t < TT; ++t) {
+        if (t < nt) {
+          const float sum = warp_sum_fixed(acc[t]);
+          if (lane == t) {
+            const int64_t tt = t0 + t;
+            if (p.y_f32 != nullptr) p.y_f32[tt * p.ldy + row] = sum;
+            if (p.y_bf16 != nullptr) {
+              uint16_t o = f32_to_bf16(sum);
+              if (p.resid != nullptr)
+                o = f32_to_bf16(__fadd_rn(bf16_to_f32(p.resid[tt * p.N + row]), bf16_to_f32(o)));
+              p.y_bf16[tt * p.N + row] = o;
+            }
+          }
+        }
+      }
+    };
+    int row = r_begin + warp;
+    if (nt == TT) {
+      for (; row + kRowsPerTile < r_end; row += 2 * kRowsPerTile) {
+        float acc0[TT], acc1[TT];
+#pragma unroll
+        for (int t = 0; t < TT; ++t) acc0[t] = acc1[t] = 0.0f;
+        stream_rows2_f32<TT, 4>(reinterpret_cast<const uint4*>(p.w + (int64_t)row * p.K),
+                                reinterpret_cast<const uint4*>(p.w + (int64_t)(row + kRowsPerTile) * p.K), s_actf,
+                                nchunks, lane, acc0, acc1);
+        emit(row, acc0);
+        emit(row + kRowsPerTile, acc1);
+      }
+    }
+    for (; row < r_end; row += kRowsPerTile) {
       const uint4* wr = reinterpret_cast<const uint4*>(p.w + (int64_t)row * p.K);
       float acc[TT];
 #pragma unroll
@@ -519,22 +584,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) linear_kernel(const LinParams 
         stream_rows_f32<TT, 8, true>(wr, s_actf, nchunks, nt, lane, acc);
       else
         stream_rows_f32<TT, 8, false>(wr, s_actf, nchunks, nt, lane, acc);
-#pragma unroll
-      for (int t = 0; t < TT; ++t) {
-        if (t < nt) {
-          const float s = warp_sum_fixed(acc[t]);
-          if (lane == t) {
-            const int64_t tt = t0 + t;
-            if (p.y_f32 != nullptr) p.y_f32[tt * p.ldy + row] = s;
-            if (p.y_bf16 != nullptr) {
-              uint16_t o = f32_to_bf16(s);
-              if (p.resid != nullptr)
-                o = f32_to_bf16(__fadd_rn(bf16_to_f32(p.resid[tt * p.N + row]), bf16_to_f32(o)));
-              p.y_bf16[tt * p.N + row] = o;
-            }
-          }
-        }
-      }
+      emit(row, acc);
     }
   }
 }
