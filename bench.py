@@ -486,6 +486,7 @@ def main():
                                     "t_io_expert": measured.t_io_expert * 1e3,
                                     "t_predict": measured.t_predict * 1e3},
             "window_tokens": cfg["N"],
+            "cutoff_source": getattr(eng, "cutoff_source", None),
             "k_eff_measured": getattr(eng, "k_eff", None),
         },
         "latency_breakdown": rep.latency_breakdown,

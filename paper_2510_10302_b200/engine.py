@@ -234,6 +234,7 @@ class SpecMoEEngine:
             self.decode_stream = torch.cuda.Stream(device=self.device)
             self.cache.set_codec(stride, self.staging.data_ptr(), stride, n_staging, self.decode_stream.cuda_stream)
         self.window_tokens = window_tokens
+        self.cutoff_source = "explicit" if policy.cutoff_layer is not None else "solver"
         self.cutoff = (
             effective_cutoff(self.model, hw, timings, policy, window_tokens)
             if policy.policy is Policy.DRAFT_PREFETCH
@@ -345,6 +346,18 @@ class SpecMoEEngine:
             layers = (self.cutoff + 1) if self.cutoff is not None else 0
             self.k_eff = max(self.policy.prefetch_k, round(pre / (n_it * layers))) if layers else None
             new = effective_cutoff(self.model, self.hw, t, self.policy, self.window_tokens, self.k_eff)
+            self.cutoff_source = "explicit" if self.policy.cutoff_layer is not None else "solver"
+            if new is None and self.policy.cutoff_layer is None and self.cutoff is not None:
+                # the analytic window test failed even at L = 0 (k_eff copies
+                # do not fit in the measured drafting window).  The runs just
+                # measured ran WITH drafting-stage prefetch: if its copies
+                # were in fact hidden (the paper's >= 0.8 target), keep the
+                # first layer's prefetch instead of degenerating to on-demand
+                # with the link idle through the whole drafting stage.
+                hf = self.report().extras.get("hidden_prefetch_fraction")
+                if hf is not None and hf >= 0.8:
+                    new = 0
+                    self.cutoff_source = f"measured (solver infeasible; hidden fraction {hf:.2f} at cutoff {self.cutoff})"
             if self.ep is not None:
                 new = self.ep.agree(new)
             if new != self.cutoff:
