@@ -125,7 +125,9 @@ __global__ void __launch_bounds__(256) rope_kv_kernel(const uint16_t* __restrict
 }
 
 // ------------------------------------------------------------ attention
-// One CTA (NW = 8 warps) per (b, head, chunk of QC = 8 queries).  The fixed
+// One CTA (NW = 8 warps) per (b, head, chunk of QC queries: 1 for a
+// verify / draft step's few queries -- more CTAs in flight --, 8 for a
+// prefill; QC only groups queries, it is not part of the order).  The fixed
 // order, restated by oracle_attention:
 //   qs[d]  = q[d] * scale
 //   s_j    = sum_d qs[d] * k_j[d]: lane l sums its PL = hd/32 consecutive
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(256) rope_kv_kernel(const uint16_t* __restrict
 //   l = l_0 + l_1 + ... + l_7 (in w order), acc[d] likewise,
 //   out[d] = bf16(acc[d] / l).
 // Pass 1 keeps the scores of the chunk in shared memory ([QC][S] fp32).
-constexpr int kAttnQC = 8;
+constexpr int kAttnQCMax = 8;
 constexpr int kAttnNW = 8;
 
 // The PL bf16 of row `key` that lane owns (dims lane*PL ..), as fp32: one
@@ -157,13 +159,13 @@ __device__ __forceinline__ void load_row(const uint16_t* base, int key, int hd, 
   }
 }
 
-template <int HD>
+template <int HD, int QC>
 __global__ void __launch_bounds__(32 * kAttnNW) attn_kernel(const uint16_t* __restrict__ q,
                                                          const uint16_t* __restrict__ kc,
                                                          const uint16_t* __restrict__ vc,
                                                          const int64_t* __restrict__ start, int T, int nh, int nkv,
                                                          int S, float scale, uint16_t* __restrict__ out) {
-  constexpr int QC = kAttnQC, NW = kAttnNW;
+  constexpr int NW = kAttnNW;
   constexpr int PL = HD / 32;  // dims per lane
   extern __shared__ __align__(16) float sm[];
   float* s_p = sm;                        // [QC][S] scores, then probabilities
@@ -288,8 +290,8 @@ __global__ void __launch_bounds__(32 * kAttnNW) attn_kernel(const uint16_t* __re
   }
 }
 
-size_t attn_smem(int S, int hd) {
-  return ((size_t)kAttnQC * S + (size_t)kAttnNW * kAttnQC * hd + kAttnNW * kAttnQC) * sizeof(float);
+size_t attn_smem(int S, int hd, int qc) {
+  return ((size_t)qc * S + (size_t)kAttnNW * qc * hd + kAttnNW * qc) * sizeof(float);
 }
 
 constexpr size_t kAttnSmemCap = 200 * 1024;
@@ -324,21 +326,31 @@ int spmoe_attention(const uint16_t* q, const uint16_t* k_cache, const uint16_t* 
       !k_cache || !v_cache || !start)
     return (int)cudaErrorInvalidValue;
   if (B * T == 0) return 0;
-  const size_t smem = attn_smem(S, hd);
+  // a verify / draft step (T <= 8 queries): one query per CTA, B*nh*T CTAs
+  const int qc = T <= kAttnQCMax ? 1 : kAttnQCMax;
+  const size_t smem = attn_smem(S, hd, qc);
   if (smem > kAttnSmemCap) return (int)cudaErrorInvalidValue;
-  const int nqc = (T + kAttnQC - 1) / kAttnQC;
+  const int nqc = (T + qc - 1) / qc;
   const dim3 grid(B * nh * nqc);
   cudaStream_t st = (cudaStream_t)stream;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmemCap);
-    cudaFuncSetAttribute(attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmemCap);
+    cudaFuncSetAttribute(attn_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmemCap);
+    cudaFuncSetAttribute(attn_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmemCap);
+    cudaFuncSetAttribute(attn_kernel<128, kAttnQCMax>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmemCap);
+    cudaFuncSetAttribute(attn_kernel<64, kAttnQCMax>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmemCap);
     configured = true;
   }
-  if (hd == 128)
-    attn_kernel<128><<<grid, 32 * kAttnNW, smem, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale, out);
+  if (hd == 128 && qc == 1)
+    attn_kernel<128, 1><<<grid, 32 * kAttnNW, smem, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale, out);
+  else if (hd == 128)
+    attn_kernel<128, kAttnQCMax><<<grid, 32 * kAttnNW, smem, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale,
+                                                                   out);
+  else if (qc == 1)
+    attn_kernel<64, 1><<<grid, 32 * kAttnNW, smem, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale, out);
   else
-    attn_kernel<64><<<grid, 32 * kAttnNW, smem, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale, out);
+    attn_kernel<64, kAttnQCMax><<<grid, 32 * kAttnNW, smem, st>>>(q, k_cache, v_cache, start, T, nh, nkv, S, scale,
+                                                                  out);
   return (int)cudaGetLastError();
 }
 
