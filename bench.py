@@ -349,7 +349,7 @@ def main():
         else:
             leader = True
             log(f"[bench] /dev/shm too small for shared pools: private pinned pools, distinct rows={distinct}")
-    eng = SpecMoEEngine(arch, hw, timings, policy, batch=cfg["batch"], max_tokens=cfg["prompt"] + 64 * (cfg["N"] + 1),
+    eng = SpecMoEEngine(arch, hw, timings, policy, batch=cfg["batch"], max_tokens=cfg["prompt"] + 96 * (cfg["N"] + 1),
                         window_tokens=cfg["N"], host_share=share, host_leader=leader, host_distinct=distinct,
                         ffn_impl=args.ffn_impl, host_codec=None if args.host_codec == "none" else "xc",
                         tc_min_tokens=args.tc_min_tokens)

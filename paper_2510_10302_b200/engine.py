@@ -303,6 +303,7 @@ class SpecMoEEngine:
         # finished timing events folded into plain numbers (_fold_events), so
         # a long generate() holds a bounded number of live CUDA events
         self._stall_done = {"prefetch": 0.0, "demand": 0.0}
+        self._prefetch_stall_by_layer: dict[int, float] = {}
         self._iters_done: list[tuple[float, float]] = []  # (draft ms, verify ms)
         self._k3_done: list[tuple[float, int, int, int]] = []  # (ms, bytes, experts, rows)
         self._k3_ev_ms: list[float] = []  # CUDA-event durations (time_k3 == "events")
@@ -329,11 +330,32 @@ class SpecMoEEngine:
             if self._owns_model:
                 self.host_pool.close()
 
-    def recalibrate(self, timings: ProfiledTimings | None = None) -> ProfiledTimings:
+    def _probe_cutoff(self, layer: int, steps: int) -> float | None:
+        """Run `steps` SD iterations with drafting-stage prefetch up to
+        `layer` and return the hidden fraction of `layer`'s prefetch copies
+        (the measurement state is reset before and after)."""
+        self.cutoff = layer
+        if self._graphs_ready:
+            torch.cuda.synchronize(self.device)
+            self._graphs_ready = False
+            self._ensure_graphs()
+        self._reset_run_state()
+        self.cache.clear_log()
+        for _ in range(steps):
+            self.step()
+        torch.cuda.synchronize(self.device)
+        hf = self.layer_hidden_fraction(layer)
+        self._reset_run_state()
+        self.cache.clear_log()
+        return hf
+
+    def recalibrate(self, timings: ProfiledTimings | None = None, probe_steps: int = 2) -> ProfiledTimings:
         """Replace the latency-model inputs with measurements of this engine
         (:func:`calibrate.measure_timings`), re-solve the cutoff layer and,
         if it moved, re-capture the draft-step graphs (they contain the
-        predictor launches of layers <= cutoff)."""
+        predictor launches of layers <= cutoff).  When the solver finds even
+        L = 0 infeasible, ``probe_steps`` iterations at L = 0 decide
+        (``cutoff_source`` records which rule set the cutoff)."""
         from .calibrate import measure_timings
 
         t = timings if timings is not None else measure_timings(self)
@@ -347,17 +369,19 @@ class SpecMoEEngine:
             self.k_eff = max(self.policy.prefetch_k, round(pre / (n_it * layers))) if layers else None
             new = effective_cutoff(self.model, self.hw, t, self.policy, self.window_tokens, self.k_eff)
             self.cutoff_source = "explicit" if self.policy.cutoff_layer is not None else "solver"
-            if new is None and self.policy.cutoff_layer is None and self.cutoff is not None:
+            if (new is None and self.policy.cutoff_layer is None and self.cutoff is not None and probe_steps > 0
+                    and self.seqs):
                 # the analytic window test failed even at L = 0 (k_eff copies
-                # do not fit in the measured drafting window).  The runs just
-                # measured ran WITH drafting-stage prefetch: if its copies
-                # were in fact hidden (the paper's >= 0.8 target), keep the
-                # first layer's prefetch instead of degenerating to on-demand
-                # with the link idle through the whole drafting stage.
-                hf = self.report().extras.get("hidden_prefetch_fraction")
+                # do not fit in the measured drafting window).  Measure
+                # instead: run `probe_steps` iterations at L = 0 and keep it
+                # if the verify waited on those prefetches for less than 0.2
+                # of their copy time (the paper's >= 0.8 hidden target),
+                # rather than degenerating to on-demand with the link idle
+                # through the whole drafting stage.
+                hf = self._probe_cutoff(0, probe_steps)
                 if hf is not None and hf >= 0.8:
                     new = 0
-                    self.cutoff_source = f"measured (solver infeasible; hidden fraction {hf:.2f} at cutoff {self.cutoff})"
+                    self.cutoff_source = f"measured (solver infeasible; L=0 prefetch copies {hf:.2f} hidden)"
             if self.ep is not None:
                 new = self.ep.agree(new)
             if new != self.cutoff:
@@ -367,6 +391,16 @@ class SpecMoEEngine:
                     self._graphs_ready = False
                     self._ensure_graphs()
         return t
+
+    def layer_hidden_fraction(self, layer: int) -> float | None:
+        """1 - (verify stalls on layer `layer`'s in-flight prefetches) /
+        (that layer's prefetch copy time), over the recorded run; None
+        without prefetches there."""
+        self._fold_events(force=True)
+        pre = sum(t.duration for t in self.transfers() if t.kind is TransferKind.PREFETCH and t.layer == layer) * 1e3
+        if pre <= 0:
+            return None
+        return 1.0 - self._prefetch_stall_by_layer.get(layer, 0.0) / pre
 
     @property
     def wire_ratio(self) -> float:
@@ -1017,7 +1051,10 @@ class SpecMoEEngine:
             return
         torch.cuda.synchronize(self.device)
         for s_ in self.stalls:
-            self._stall_done[s_.kind] += s_.a.elapsed_time(s_.b)
+            ms = s_.a.elapsed_time(s_.b)
+            self._stall_done[s_.kind] += ms
+            if s_.kind == "prefetch":
+                self._prefetch_stall_by_layer[s_.layer] = self._prefetch_stall_by_layer.get(s_.layer, 0.0) + ms
         self.stalls = []
         if self.k3_events:
             n = min(self._k3_span_next, self._k3_spans.shape[0])
