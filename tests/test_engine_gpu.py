@@ -196,6 +196,46 @@ def test_engine_deterministic(oracle, ffn_impl):
     assert outs[0][1] == outs[1][1], "cache counters differ"
 
 
+def test_recalibrate_solver_and_measured_fallback():
+    """engine.recalibrate: a feasible latency model sets the cutoff by the
+    solver; one where even L = 0 misses the drafting window probes L = 0 and
+    keeps it when its prefetch copies are hidden (tiny experts: they always
+    are), or falls back to no prefetch with probing disabled.  The token
+    stream is independent of all of it (caching never changes the math)."""
+    from paper_2510_10302_b200 import ProfiledTimings
+
+    ref = make_engine(record=False, capture=())
+    try:
+        ref.prefill(prompts(1))
+        for _ in range(8):
+            ref.step()
+        want = list(ref.seqs[0])
+    finally:
+        ref.close()
+    slow_link = ProfiledTimings(t_comp_target=1e-4, t_comp_draft=1e-6, t_io_expert=10.0)
+    fast_link = ProfiledTimings(t_comp_target=1e-4, t_comp_draft=1e-2, t_io_expert=1e-6)
+    for probe_steps in (2, 0):
+        eng = make_engine(cutoff=None, capture=())
+        try:
+            eng.prefill(prompts(1))
+            for _ in range(2):
+                eng.step()
+            assert eng.cutoff is not None
+            eng.recalibrate(timings=fast_link, probe_steps=probe_steps)
+            assert eng.cutoff_source == "solver" and eng.cutoff is not None and eng.cutoff >= 0
+            eng.recalibrate(timings=slow_link, probe_steps=probe_steps)
+            if probe_steps:
+                assert eng.cutoff == 0 and eng.cutoff_source.startswith("measured"), eng.cutoff_source
+            else:
+                assert eng.cutoff is None and eng.cutoff_source == "solver"
+            while len(eng.seqs[0]) < len(want):
+                eng.step()
+            torch.cuda.synchronize()
+            assert list(eng.seqs[0])[: len(want)] == want
+        finally:
+            eng.close()
+
+
 @pytest.mark.parametrize("tc_min", [2, 3])
 def test_engine_tokens_independent_of_launch_grouping(oracle, tc_min):
     """Which resident experts share a K3 launch depends on copy timing
