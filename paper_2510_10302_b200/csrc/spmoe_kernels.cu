@@ -283,19 +283,28 @@ __device__ __forceinline__ void stream_rows(const uint4* const (&wr)[NR], const 
 // memory (two float4 planes per 16-byte chunk: elements 0-3 and 4-7, so the
 // lanes' loads stay contiguous): no per-row bf16 unpack of the activations,
 // identical FMA order.
+template <int UNR>
+__device__ __forceinline__ void load_round(const uint4* wr, int base, int nchunks, int lane, uint4 (&w)[UNR]) {
+#pragma unroll
+  for (int i = 0; i < UNR; ++i) {
+    const int c = base + lane + 32 * i;
+    w[i] = (c < nchunks) ? ldg_stream(wr + c) : make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
 // Two weight rows per pass sharing every activation load (half the shared-
-// memory traffic per row); each row's FMA chains keep their order.
+// memory traffic per row); each row's FMA chains keep their order.  Software
+// pipelined: round r+1's loads are issued before round r's FMAs.
 template <int TT, int UNR>
 __device__ __forceinline__ void stream_rows2_f32(const uint4* wr0, const uint4* wr1, const float4* act, int nchunks,
                                                  int lane, float (&acc0)[TT], float (&acc1)[TT]) {
+  uint4 w0[UNR], w1[UNR];
+  load_round<UNR>(wr0, 0, nchunks, lane, w0);
+  load_round<UNR>(wr1, 0, nchunks, lane, w1);
   for (int base = 0; base < nchunks; base += 32 * UNR) {
-    uint4 w0[UNR], w1[UNR];
-#pragma unroll
-    for (int i = 0; i < UNR; ++i) {
-      const int c = base + lane + 32 * i;
-      w0[i] = (c < nchunks) ? ldg_stream(wr0 + c) : make_uint4(0u, 0u, 0u, 0u);
-      w1[i] = (c < nchunks) ? ldg_stream(wr1 + c) : make_uint4(0u, 0u, 0u, 0u);
-    }
+    uint4 n0[UNR], n1[UNR];
+    load_round<UNR>(wr0, base + 32 * UNR, nchunks, lane, n0);
+    load_round<UNR>(wr1, base + 32 * UNR, nchunks, lane, n1);
 #pragma unroll
     for (int i = 0; i < UNR; ++i) {
       const int c = base + lane + 32 * i;
@@ -315,19 +324,22 @@ __device__ __forceinline__ void stream_rows2_f32(const uint4* wr0, const uint4* 
         }
       }
     }
+#pragma unroll
+    for (int i = 0; i < UNR; ++i) {
+      w0[i] = n0[i];
+      w1[i] = n1[i];
+    }
   }
 }
 
 template <int TT, int UNR, bool FULL>
 __device__ __forceinline__ void stream_rows_f32(const uint4* wr, const float4* act, int nchunks, int nt, int lane,
                                                 float (&acc)[TT]) {
+  uint4 w[UNR];
+  load_round<UNR>(wr, 0, nchunks, lane, w);
   for (int base = 0; base < nchunks; base += 32 * UNR) {
-    uint4 w[UNR];
-#pragma unroll
-    for (int i = 0; i < UNR; ++i) {
-      const int c = base + lane + 32 * i;
-      w[i] = (c < nchunks) ? ldg_stream(wr + c) : make_uint4(0u, 0u, 0u, 0u);
-    }
+    uint4 nw[UNR];
+    load_round<UNR>(wr, base + 32 * UNR, nchunks, lane, nw);
 #pragma unroll
     for (int i = 0; i < UNR; ++i) {
       const int c = base + lane + 32 * i;
@@ -361,6 +373,8 @@ __device__ __forceinline__ void stream_rows_f32(const uint4* wr, const float4* a
         }
       }
     }
+#pragma unroll
+    for (int i = 0; i < UNR; ++i) w[i] = nw[i];
   }
 }
 
@@ -568,7 +582,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) linear_kernel(const LinParams 
         float acc0[TT], acc1[TT];
 #pragma unroll
         for (int t = 0; t < TT; ++t) acc0[t] = acc1[t] = 0.0f;
-        stream_rows2_f32<TT, 4>(reinterpret_cast<const uint4*>(p.w + (int64_t)row * p.K),
+        stream_rows2_f32<TT, (TT <= 2 ? 4 : 2)>(reinterpret_cast<const uint4*>(p.w + (int64_t)row * p.K),
                                 reinterpret_cast<const uint4*>(p.w + (int64_t)(row + kRowsPerTile) * p.K), s_actf,
                                 nchunks, lane, acc0, acc1);
         emit(row, acc0);
@@ -581,9 +595,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) linear_kernel(const LinParams 
 #pragma unroll
       for (int t = 0; t < TT; ++t) acc[t] = 0.0f;
       if (nt == TT)
-        stream_rows_f32<TT, 8, true>(wr, s_actf, nchunks, nt, lane, acc);
+        stream_rows_f32<TT, (TT <= 2 ? 8 : 4), true>(wr, s_actf, nchunks, nt, lane, acc);
       else
-        stream_rows_f32<TT, 8, false>(wr, s_actf, nchunks, nt, lane, acc);
+        stream_rows_f32<TT, (TT <= 2 ? 8 : 4), false>(wr, s_actf, nchunks, nt, lane, acc);
       emit(row, acc);
     }
   }
