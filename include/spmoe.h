@@ -286,8 +286,13 @@ int spmoe_attention(const uint16_t* q, const uint16_t* k_cache, const uint16_t* 
  *   y_f32  != NULL: y_f32[t*ldy + n] = y (fp32, e.g. lm_head logits)
  *   y_bf16 != NULL: y_bf16[t*N + n] = bf16(y), or with resid != NULL
  *                   bf16(resid[t*N + n] + bf16(y)) (resid may alias y_bf16)
- * Weight-streaming, one warp per weight row, activations staged in shared
- * memory 16 rows at a time.
+ * Weight-streaming (one warp per weight row pair, pipelined rounds),
+ * activations staged in shared memory as fp32, up to 8 token rows per
+ * register tile (16 beyond).  Launched with programmatic dependent launch:
+ * x and resid are read only after the previous kernel on `stream` has
+ * completed, but the first rounds of w are requested into L2 before that --
+ * w must not be written by the immediately preceding kernel on `stream`
+ * (weights are static in the engine; SPMOE_NO_PDL=1 launches without it).
  */
 int spmoe_linear(const uint16_t* w, const uint16_t* x, int64_t ldx, int T, int K, int N,
                  const uint16_t* norm_w, float eps, float* y_f32, int64_t ldy, uint16_t* y_bf16,

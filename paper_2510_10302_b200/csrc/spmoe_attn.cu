@@ -35,6 +35,7 @@ namespace {
 __global__ void __launch_bounds__(256) rms_norm_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w,
                                                        int rows, int H, float eps, uint16_t* __restrict__ out) {
   __shared__ float s_r;
+  grid_dep_trigger();  // a following K9 (lm_head) may start streaming its weights
   const int row = blockIdx.x;
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(32 * kAttnNW) attn_kernel(const uint16_t* __re
                                                          int S, float scale, uint16_t* __restrict__ out) {
   constexpr int NW = kAttnNW;
   constexpr int PL = HD / 32;  // dims per lane
+  grid_dep_trigger();  // the following K9 (W_o) may start streaming its weights
   extern __shared__ __align__(16) float sm[];
   float* s_p = sm;                        // [QC][S] scores, then probabilities
   float* s_acc = s_p + (int64_t)QC * S;   // [NW][QC][HD]

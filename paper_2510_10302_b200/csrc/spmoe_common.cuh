@@ -111,6 +111,14 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
   return r;
 }
 
+// Programmatic dependent launch for the non-tcgen05 kernels (spmoe_tc.cu
+// has its own copies): grid_dep_trigger lets the next kernel in the stream,
+// if launched with the attribute, get scheduled now; grid_dep_wait blocks
+// until the previous grid has completed and its writes are visible.  Both
+// are no-ops for kernels launched without the attribute.
+__device__ __forceinline__ void grid_dep_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // 16-byte load of re-used activations (L1-cached read-only path).
 __device__ __forceinline__ uint4 ldg_act(const uint4* p) { return __ldg(p); }
 

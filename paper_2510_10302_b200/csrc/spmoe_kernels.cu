@@ -6,6 +6,7 @@
 #include "../../include/spmoe.h"
 
 #include <stdio.h>
+#include <stdlib.h>
 
 using namespace spmoe;
 
@@ -297,10 +298,9 @@ __device__ __forceinline__ void load_round(const uint4* wr, int base, int nchunk
 // pipelined: round r+1's loads are issued before round r's FMAs.
 template <int TT, int UNR>
 __device__ __forceinline__ void stream_rows2_f32(const uint4* wr0, const uint4* wr1, const float4* act, int nchunks,
-                                                 int lane, float (&acc0)[TT], float (&acc1)[TT]) {
-  uint4 w0[UNR], w1[UNR];
-  load_round<UNR>(wr0, 0, nchunks, lane, w0);
-  load_round<UNR>(wr1, 0, nchunks, lane, w1);
+                                                 int lane, float (&acc0)[TT], float (&acc1)[TT],
+                                                 uint4 (&w0)[UNR], uint4 (&w1)[UNR]) {
+  // w0 / w1 arrive holding round 0 (the caller may have issued it early)
   for (int base = 0; base < nchunks; base += 32 * UNR) {
     uint4 n0[UNR], n1[UNR];
     load_round<UNR>(wr0, base + 32 * UNR, nchunks, lane, n0);
@@ -531,6 +531,29 @@ __global__ void __launch_bounds__(kFfnThreads, 1) linear_kernel(const LinParams 
   const int nchunks = p.K >> 3;
   const int r_begin = (int)((int64_t)p.N * blockIdx.x / gridDim.x);
   const int r_end = (int)((int64_t)p.N * (blockIdx.x + 1) / gridDim.x);
+  constexpr int U2 = TT <= 2 ? 4 : 2;  // pair rounds (more would spill at TT >= 3)
+  // Launched with programmatic stream serialization: the weights are not
+  // written by the preceding kernel, so the first two rounds of this warp's
+  // first row pair are requested into L2 before the grid dependency (x,
+  // resid) resolves -- while the previous kernel drains and during the
+  // activation stage below.
+  grid_dep_trigger();
+  {
+    const int row0 = r_begin + warp;
+    if (row0 + kRowsPerTile < r_end) {
+      const uint4* a = reinterpret_cast<const uint4*>(p.w + (int64_t)row0 * p.K);
+      const uint4* b = reinterpret_cast<const uint4*>(p.w + (int64_t)(row0 + kRowsPerTile) * p.K);
+#pragma unroll
+      for (int i = 0; i < 2 * U2; ++i) {
+        const int c = lane + 32 * i;
+        if (c < nchunks) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a + c));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(b + c));
+        }
+      }
+    }
+  }
+  grid_dep_wait();
   if (r_begin >= r_end) return;
   for (int t0 = 0; t0 < p.T; t0 += TT) {
     const int nt = min(TT, p.T - t0);
@@ -582,9 +605,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) linear_kernel(const LinParams 
         float acc0[TT], acc1[TT];
 #pragma unroll
         for (int t = 0; t < TT; ++t) acc0[t] = acc1[t] = 0.0f;
-        stream_rows2_f32<TT, (TT <= 2 ? 4 : 2)>(reinterpret_cast<const uint4*>(p.w + (int64_t)row * p.K),
-                                reinterpret_cast<const uint4*>(p.w + (int64_t)(row + kRowsPerTile) * p.K), s_actf,
-                                nchunks, lane, acc0, acc1);
+        const uint4* w0p = reinterpret_cast<const uint4*>(p.w + (int64_t)row * p.K);
+        const uint4* w1p = reinterpret_cast<const uint4*>(p.w + (int64_t)(row + kRowsPerTile) * p.K);
+        uint4 w0[U2], w1[U2];
+        load_round<U2>(w0p, 0, nchunks, lane, w0);
+        load_round<U2>(w1p, 0, nchunks, lane, w1);
+        stream_rows2_f32<TT, U2>(w0p, w1p, s_actf, nchunks, lane, acc0, acc1, w0, w1);
         emit(row, acc0);
         emit(row + kRowsPerTile, acc1);
       }
@@ -614,8 +640,19 @@ int launch_linear(const LinParams& p, cudaStream_t s) {
   }
   const int tiles = (p.N + 15) / 16;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  linear_kernel<TT><<<grid, kFfnThreads, smem, s>>>(p);
-  return launch_status();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kFfnThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  static const int no_pdl = getenv("SPMOE_NO_PDL") != nullptr;  // A/B switch
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, linear_kernel<TT>, p);
+  return e != cudaSuccess ? (int)e : launch_status();
 }
 
 // Register tile: the smallest of 1/2/4/8 covering the hint that also fits
@@ -674,6 +711,7 @@ __global__ void moe_combine_kernel(const float* __restrict__ y, const int32_t* _
                                    const float* __restrict__ w, int H, int k,
                                    const float* __restrict__ ys, const float* __restrict__ sg,
                                    const uint16_t* residual, uint16_t* out) {
+  grid_dep_trigger();  // a following K9 may start streaming its weights
   const int t = blockIdx.y;
   const int h0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (h0 >= H) return;
