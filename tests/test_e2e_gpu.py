@@ -122,7 +122,7 @@ def gpu_raw_expert(eng):
     return lambda l, e: eng.host_pool.raw_row(eng.host_pool.row_of(l, e), eng.device)
 
 
-def big_engine(arch_name, ffn_impl, model_state=None, N=4, budget=0.25, prompt=8, capture=()):
+def big_engine(arch_name, ffn_impl, model_state=None, N=4, budget=0.25, prompt=8, capture=(), batch=1, max_new=16):
     from paper_2510_10302_b200 import HardwareSpec, Policy, PolicySpec, ProfiledTimings
     from paper_2510_10302_b200.engine import SpecMoEEngine
     from paper_2510_10302_b200.model import get_arch
@@ -134,7 +134,7 @@ def big_engine(arch_name, ffn_impl, model_state=None, N=4, budget=0.25, prompt=8
     pk = 1 if a.num_experts <= 16 else a.top_k
     pol = PolicySpec(policy=Policy.DRAFT_PREFETCH, prefetch_k=pk, draft_length=N, acceptance_rate=1.0, seed=1234,
                      cutoff_layer=1, cache_capacity_experts=cap)
-    return SpecMoEEngine(a, hw, t, pol, batch=1, record=True, ffn_impl=ffn_impl, max_tokens=prompt + 16,
+    return SpecMoEEngine(a, hw, t, pol, batch=batch, record=True, ffn_impl=ffn_impl, max_tokens=prompt + max_new,
                          model_state=model_state, capture_layers=capture)
 
 
@@ -229,3 +229,63 @@ def test_e2e_real_shapes(arch_name):
         if eng2 is not None:
             eng2.close()
         eng.close()
+
+
+@pytest.mark.parametrize("arch_name,batch,N", [("qwen15_moe_a27b", 8, 8), ("qwen15_moe_a27b", 4, 2),
+                                               ("deepseek_v2_lite", 3, 8)])
+def test_e2e_config4_batch_and_draft_length(arch_name, batch, N):
+    """Config #4's grid corners (draft length N in {2, 8}, batch up to 8) at
+    the real shapes: exact mode == the CPU loop for 2 SD iterations per
+    sequence (tokens, fp32 logits, drafts, predictions) with sequences whose
+    lengths diverge, plus the policy replay; then the default engine
+    (tcgen05 K3; at batch 8 x 9 tokens some experts exceed the unit kernel's
+    16 tokens and take the split-plan path) on the same model: routing
+    bit-exact and the verify-MoE output within 2^-7 of the oracle at the
+    captured layers, policy replay exact."""
+    from oracle import tensor_oracle as O
+
+    O.set_threads(len(__import__("os").sched_getaffinity(0)))
+    n_tok = 2 * (N + 1)
+    eng = big_engine(arch_name, "cuda_core", N=N, batch=batch, max_new=n_tok + N + 2)
+    eng2 = None
+    try:
+        P = prompts(batch, P=8, vocab=eng.arch.vocab, seed=11)
+        state0 = run_engine(eng, P, n_tok)
+        sd = run_cpu(eng, P, n_tok, gpu_raw_expert(eng))
+        compare_exact(eng, sd)
+        check_policy_replay(eng, state0)
+        L = eng.arch.num_layers
+        eng2 = big_engine(arch_name, "auto", model_state=eng.model_state, N=N, batch=batch,
+                          max_new=n_tok + N + 2, capture=(0, L - 1))
+        eng2.prefill(P)
+        state2 = ([tuple(e) for e in eng2.cache.lru_order], [eng2.cache.slot_of(*e) for e in eng2.cache.lru_order])
+        eng2.step()
+        torch.cuda.synchronize()
+        raw = gpu_raw_expert(eng2)
+        a = eng2.arch
+        n_layers = 0
+        for c in (c for c in eng2.captures if "layer" in c):
+            l = c["layer"]
+            xn = bits(c["xn"])
+            lw = eng2.weights.layers[l]
+            w_o, idx_o, _, sg_o = O.router_topk(xn, bits(lw.router), a.top_k, a.renorm,
+                                                bits(lw.shared_gate) if lw.shared_gate is not None else None)
+            assert np.array_equal(bits(c["idx"]), idx_o), f"routing differs at layer {l}"
+            off, perm, inv = O.moe_permute(idx_o, a.num_experts)
+            used = sorted(set(idx_o.ravel().tolist()))
+            _, y = O.expert_ffn([raw(l, e) if e in used else None for e in range(a.num_experts)], xn, a.ffn, off,
+                                perm)
+            ys = None
+            if a.shared_ffn:
+                o1 = np.array([0, xn.shape[0]], np.int32)
+                _, ys = O.expert_ffn([bits(lw.shared)[0]], xn, a.shared_ffn, o1, np.arange(xn.shape[0], dtype=np.int32))
+            out = O.moe_combine(y, inv, w_o, xn.shape[0], a.hidden, a.top_k, ys=ys, sg=sg_o, residual=bits(c["resid"]))
+            got, ref = O.bf16_bits_to_f32(bits(c["out"])), O.bf16_bits_to_f32(out)
+            assert np.abs(got - ref).max() <= 2.0 ** -7 * np.abs(ref).max(), f"verify-MoE output off at layer {l}"
+            n_layers += 1
+        assert n_layers == 2
+        check_policy_replay(eng2, state2)
+    finally:
+        eng.close()
+        if eng2 is not None:
+            eng2.close()

@@ -36,7 +36,7 @@ __device__ __forceinline__ void wait_bar(uint64_t* b, uint32_t ph) {
 
 // mode 0: tensor boxes of BOXR rows; mode 1: bulk contiguous chunks
 template <int MODE, int BOXR, int S>
-__global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ CUtensorMap map, const char* base,
+__global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap map2, const char* base,
                                                        int tiles_per_cta, unsigned* sink,
                                                        unsigned long long* stamps) {
   constexpr int STAGE = BOXR * 64 * 2;
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
   }
   __syncthreads();
   const int kblocks = kCols / 64;
-  const int n_iter = tiles_per_cta * kblocks * (128 / BOXR > 0 ? 1 : 1);
+  const int n_iter = MODE == 2 ? 64 : MODE == 3 ? 192 : tiles_per_cta * kblocks;
   // tile rows per CTA: BOXR rows per tile
   if (threadIdx.x == 0) {
     int stage = 0;
@@ -67,7 +67,29 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
       wait_bar(&empty[stage], ph ^ 1);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[stage])), "r"(STAGE)
                    : "memory");
-      if (MODE == 0) {
+      if (MODE >= 2) {
+        // K3 unit stream: (MODE 3) W1 then W3 tile m over all 64 k-blocks,
+        // then (MODE 2, 3) W2's 128-column block m as 32 row tiles x 2 boxes
+        const int m = blockIdx.x % 112, ex = blockIdx.x / 112;
+        const int n_up = MODE == 3 ? 2 * kblocks : 0;
+        int c0, r0;
+        const CUtensorMap* mp;
+        if (it < n_up) {
+          mp = &map;
+          c0 = (it >> 1) * 64;
+          r0 = ex * 28672 + (it & 1) * 14336 + m * 128;
+        } else {
+          const int d = it - n_up;
+          mp = &map2;
+          c0 = m * 128 + (d & 1) * 64;
+          r0 = ex * 4096 + (d >> 1) * 128;
+        }
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+            "[%2];" ::"r"(su32(sm + stage * STAGE)),
+            "l"(mp), "r"(su32(&full[stage])), "r"(c0), "r"(r0)
+            : "memory");
+      } else if (MODE == 0) {
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
             "[%2];" ::"r"(su32(sm + stage * STAGE)),
@@ -121,6 +143,7 @@ static unsigned long long* g_stamps = nullptr;
 static bool g_graph = false;
 static float g_gap0 = 0, g_gap1 = 0;  // us: stamp kernel -> first CTA start, last CTA end -> stamp kernel  // launch the kernel as a pre-uploaded CUDA graph
 
+static CUtensorMap g_map2;  // W2-shaped [rows, 14336] map for MODE 2/3
 template <int MODE, int BOXR, int S>
 void run(const char* name, void* buf, size_t rows, unsigned* sink, EncodeFn enc, int per_cta_mb = 8,
          std::initializer_list<int> grids = {16, 32, 64, 112, 128, 148, 296}) {
@@ -139,6 +162,7 @@ void run(const char* name, void* buf, size_t rows, unsigned* sink, EncodeFn enc,
     int tpc = (int)(((size_t)per_cta_mb << 20) / tile_bytes);
     if (tpc < 1) tpc = 1;
     if ((size_t)G * tpc > (size_t)total_tiles) tpc = total_tiles / G;
+    if (MODE >= 2) tpc = 0;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -153,7 +177,7 @@ void run(const char* name, void* buf, size_t rows, unsigned* sink, EncodeFn enc,
         cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
         cudaGraph_t gr;
         cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
-        stream_kernel<MODE, BOXR, S><<<G, 64, smem, cs>>>(map, (const char*)buf, tpc, sink, g_stamps);
+        stream_kernel<MODE, BOXR, S><<<G, 64, smem, cs>>>(map, g_map2, (const char*)buf, tpc, sink, g_stamps);
         cudaStreamEndCapture(cs, &gr);
         cudaGraphInstantiate(&ge, gr, 0);
         cudaGraphUpload(ge, cs);
@@ -168,7 +192,7 @@ void run(const char* name, void* buf, size_t rows, unsigned* sink, EncodeFn enc,
       cudaEventRecord(a, cs);
       stamp_kernel<<<1, 1, 0, cs>>>(g_stamps + 2);
       if (g_graph) cudaGraphLaunch(ge, cs);
-      else stream_kernel<MODE, BOXR, S><<<G, 64, smem, cs>>>(map, (const char*)buf, tpc, sink, g_stamps);
+      else stream_kernel<MODE, BOXR, S><<<G, 64, smem, cs>>>(map, g_map2, (const char*)buf, tpc, sink, g_stamps);
       stamp_kernel<<<1, 1, 0, cs>>>(g_stamps + 3);
       cudaEventRecord(b, cs);
       cudaEventSynchronize(b);
@@ -186,7 +210,8 @@ void run(const char* name, void* buf, size_t rows, unsigned* sink, EncodeFn enc,
         g_gap1 = (float)(st[3] - st[1]) / 1e3f;
       }
     }
-    const double bytes = (double)G * tpc * tile_bytes;
+    const double bytes = MODE == 2 ? (double)G * 64 * STAGE : MODE == 3 ? (double)G * 192 * STAGE
+                                                                      : (double)G * tpc * tile_bytes;
     const int active = G > 148 ? 148 : G;
     printf("%-8s S=%2d stage=%5d B  G=%3d  %2d MB/CTA  %8.1f GB/s  %6.1f GB/s/SM  (%.1f us events, %.1f us first CTA start -> last CTA end; gaps %.1f / %.1f us)\n",
            name, S, STAGE, G, tpc * (int)(tile_bytes >> 20), bytes / best / 1e6, bytes / best / 1e6 / active, best * 1e3,
@@ -210,6 +235,26 @@ int main(int argc, char** argv) {
   unsigned* sink;
   cudaMalloc(&sink, 64);
   cudaMalloc(&g_stamps, 32);
+  if (argc > 1 && !strcmp(argv[1], "unit")) {
+    // K3's single-expert unit stream without math: up (W1|W3 tile m) 2 MB,
+    // down (W2 column block m, 256 B per row at a 28 KB stride) 1 MB
+    void* w2;
+    const size_t rows2 = 4096 * 12;
+    cudaMalloc(&w2, rows2 * 14336 * 2);
+    cudaMemset(w2, 1, rows2 * 14336 * 2);
+    cuuint64_t d[2] = {14336, (cuuint64_t)rows2}, st[1] = {14336 * 2};
+    cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+    enc(&g_map2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w2, d, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    for (int rep = 0; rep < 2; ++rep) {
+      run<0, 128, 12>("tile128", buf, rows, sink, enc, 2, {112});
+      run<0, 128, 12>("tile128", buf, rows, sink, enc, 3, {112});
+      run<2, 128, 12>("down", buf, rows, sink, enc, 1, {112, 224, 448});
+      run<3, 128, 12>("unit", buf, rows, sink, enc, 3, {112, 224});
+      run<3, 128, 8>("unit", buf, rows, sink, enc, 3, {112});
+    }
+    return 0;
+  }
   if (argc > 1 && !strcmp(argv[1], "h2dsrc")) {
     // does the pinned source's page size change the penalty?  cudaMallocHost
     // vs 2 MB-aligned THP-advised memory registered with cudaHostRegister vs
