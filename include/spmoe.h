@@ -166,8 +166,10 @@ int spmoe_expert_ffn_tc_fused(const uint16_t* pool, int64_t slot_elems, const in
  * expert): each work unit (expert, 128-feature block m) runs
  * W1/W3 rows of block m -> h block in shared memory -> the matching W2
  * column block -> partial y_m; a PDL-chained second launch sums the F/128
- * partials per element in a fixed order into y.  x_perm: [T*k, H] scratch
- * for the expert-grouped rows of x (as spmoe_expert_ffn_tc).  workspace:
+ * partials per element in a fixed order into y.  The kernel loads each
+ * unit's token rows straight from x (TMA gather4 over perm_token), so no
+ * row-gather launch precedes it; x_perm is unused (nullable, kept for the
+ * ABI).  workspace:
  * spmoe_expert_ffn_tc_units_workspace_floats(T*k, H, F) floats.
  * h_scratch (nullable) receives h.  Same
  * tolerance contract as spmoe_expert_ffn_tc; an expert's result never

@@ -120,6 +120,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// Four arbitrary rows of a 2-D map with box {64, 1}: 4 x 128 B land as
+// consecutive 128-byte rows at dst (the 128B swizzle follows the shared
+// memory address, so a group at a 512-byte offset is rows 4..7 of its atom).
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int r0, int r1,
+                                            int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+
 // K-major operand, 128-byte swizzle, 8-row atoms of 1024 bytes (SBO), LBO
 // unused (1), descriptor version 1 (sm100), layout type 2 = SWIZZLE_128B.
 __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
@@ -596,15 +608,40 @@ ffn_tc_fused_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_con
 // the launch.
 // Tokens per expert <= 16 (one N=16 MMA): the SD verify regime.
 constexpr int UN = 16;  // tokens per unit (MMA N)
+#ifndef SPMOE_UNIT_NY
+#define SPMOE_UNIT_NY 2
+#endif
+constexpr int kUnitNY = SPMOE_UNIT_NY;  // down-phase y accumulators in TMEM (ring)
+constexpr int kUnitTmemCols = 32 + 16 * kUnitNY <= 64 ? 64 : 32 + 16 * kUnitNY <= 128 ? 128 : 256;
 
 struct UnitParams {
   const int32_t* offsets;
+  const int32_t* perm_token;  // token (row of x) of every routed row, K2 order
+  DevSpan* span;
   uint16_t* h_out;      // [rows, F] bf16 (optional copy of h for callers/tests)
   float* y_part;        // [F/128][rows, H] fp32 partials
   int H, F, rows, n_active;
   int active[kMaxExperts];
   int slot[kMaxExperts];
 };
+
+#ifdef SPMOE_UNIT_STAMPS
+// diagnostic build only (tools/k3_unit_stamps.py): per-CTA globaltimer
+// stamps of the unit kernel's phases
+__device__ unsigned long long* g_unit_stamps = nullptr;
+#define UNIT_STAMP(i)                                                        \
+  do {                                                                       \
+    if (g_unit_stamps && u == (int)blockIdx.x) {                             \
+      unsigned long long t_;                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+      g_unit_stamps[blockIdx.x * 8 + (i)] = t_;                              \
+    }                                                                        \
+  } while (0)
+#else
+#define UNIT_STAMP(i) \
+  do {                \
+  } while (0)
+#endif
 
 template <int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -617,7 +654,7 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* hb = smem + STAGES * STAGE_BYTES;  // h block as the down MMA's B operand: 2 x [16 x 64]
-  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], gu_full, h_ready, y_full[2], y_empty[2];
+  __shared__ uint64_t full_bar[STAGES], empty_bar[STAGES], gu_full, h_ready, y_full[kUnitNY], y_empty[kUnitNY];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -626,14 +663,16 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
   const int mt_dn = p.H / BM;  // down M-tiles per unit
   const int n_units = p.n_active * mt_up;
   pdl_launch_dependents();
+  span_begin(p.span);
   if (threadIdx.x == 0) {
+    { const int u = blockIdx.x; UNIT_STAMP(0); }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     mbar_init(&gu_full, 1);
     mbar_init(&h_ready, 128);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kUnitNY; ++s) {
       mbar_init(&y_full[s], 1);
       mbar_init(&y_empty[s], 128);
     }
@@ -645,9 +684,9 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
   }
   if (warp == 1) {
-    // columns: g [0,16) | u [16,32) | y0 [32,48) | y1 [48,64)
+    // columns: g [0,16) | u [16,32) | y ring: kUnitNY x 16 from 32
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                 "r"(64));
+                 "r"(kUnitTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -657,20 +696,36 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
 
   if (warp == 0) {
     if (lane == 0) {
+      { const int u = blockIdx.x; UNIT_STAMP(1); }
       // ---------------- TMA producer: per unit, the up stream then the
       // W2 column block (weights never depend on h, so the down loads run
       // ahead while the epilogue turns the up accumulators into h).  x_perm
       // comes from the gather kernel this launch is PDL-chained to: the
       // weight boxes of the first STAGES stages go out before waiting for it.
+      // x rows come straight from x by TMA gather4 (rows perm_token[arow ..
+      // arow + 16), clamped to the unit's last token: the extra MMA columns
+      // are never read back), so no gather kernel precedes this one.
       int stage = 0;
       uint32_t phase = 0;
       bool waited = false;
-      int pend_stage[STAGES], pend_kb[STAGES], pend_row[STAGES], npend = 0;
+      int pend_stage[STAGES], pend_kb[STAGES], npend = 0;
+      int xr[UN];
       const uint64_t ef = l2_evict_first_policy();
+      auto x_rows = [&](int arow, int ntok) {
+#pragma unroll
+        for (int i = 0; i < UN; ++i) xr[i] = __ldg(p.perm_token + arow + min(i, ntok - 1));
+      };
+      auto load_x = [&](uint8_t* dst, uint64_t* bar, int kb) {
+#pragma unroll
+        for (int g = 0; g < UN / 4; ++g)
+          tma_gather4(dst + g * 512, &map_x, bar, kb * BK, xr[4 * g], xr[4 * g + 1], xr[4 * g + 2], xr[4 * g + 3]);
+      };
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int a = u / mt_up, m = u - a * mt_up;
         const int e = p.active[a], slot = p.slot[a];
         const int arow = p.offsets[e];
+        const int ntok = max(1, min(UN, p.offsets[e + 1] - arow));
+        if (waited) x_rows(arow, ntok);
         for (int kb = 0; kb < kb_up; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * STAGE_BYTES;
@@ -678,16 +733,17 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
           tma_load_3d_hint(st, &map_wu, &full_bar[stage], kb * BK, m * BM, slot, ef);
           tma_load_3d_hint(st + A_BYTES, &map_wu, &full_bar[stage], kb * BK, p.F + m * BM, slot, ef);
           if (waited) {
-            tma_load_2d(st + 2 * A_BYTES, &map_x, &full_bar[stage], kb * BK, arow);
+            load_x(st + 2 * A_BYTES, &full_bar[stage], kb);
           } else {
+            // the first stages' weights go out before the dependency on the
+            // producer of x / perm_token resolves
             pend_stage[npend] = stage;
             pend_kb[npend] = kb;
-            pend_row[npend] = arow;
             if (++npend == STAGES || kb + 1 == kb_up) {
               pdl_wait();
+              x_rows(arow, ntok);
               for (int i = 0; i < npend; ++i)
-                tma_load_2d(smem + pend_stage[i] * STAGE_BYTES + 2 * A_BYTES, &map_x, &full_bar[pend_stage[i]],
-                            pend_kb[i] * BK, pend_row[i]);
+                load_x(smem + pend_stage[i] * STAGE_BYTES + 2 * A_BYTES, &full_bar[pend_stage[i]], pend_kb[i]);
               npend = 0;
               waited = true;
             }
@@ -702,6 +758,7 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
           tma_load_3d_hint(st + A_BYTES, &map_wd, &full_bar[stage], m * BM + BK, j * BM, slot, ef);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        UNIT_STAMP(6);
       }
       if (!waited) pdl_wait();
     }
@@ -718,6 +775,7 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
         // after its h_ready, imply its epilogue has drained them)
         for (int kb = 0; kb < kb_up; ++kb) {
           mbar_wait(&full_bar[stage], phase);
+          if (kb == 0) UNIT_STAMP(2);
           tc_fence_after();
           uint8_t* st = smem + stage * STAGE_BYTES;
           const uint64_t a0 = smem_desc_sw128(st), a1 = smem_desc_sw128(st + A_BYTES);
@@ -732,9 +790,11 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         umma_commit(&gu_full);
+        UNIT_STAMP(3);
         // down: B = this unit's h block from shared memory
         mbar_wait(&h_ready, hphase);
         hphase ^= 1;
+        UNIT_STAMP(5);
         tc_fence_after();
         for (int j = 0; j < mt_dn; ++j) {
           mbar_wait(&y_empty[acc], aphase ^ 1);
@@ -750,7 +810,7 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
           umma_commit(&empty_bar[stage]);
           umma_commit(&y_full[acc]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
-          if (++acc == 2) { acc = 0; aphase ^= 1; }
+          if (++acc == kUnitNY) { acc = 0; aphase ^= 1; }
         }
       }
     }
@@ -788,6 +848,7 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
       tc_fence_before();
       mbar_arrive(&h_ready);
+      if (threadIdx.x == 64) UNIT_STAMP(4);
       float* yp = p.y_part + (int64_t)m * plane;
       for (int j = 0; j < mt_dn; ++j) {
         mbar_wait(&y_full[acc], aphase);
@@ -797,19 +858,20 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(&y_empty[acc]);
-        if (++acc == 2) { acc = 0; aphase ^= 1; }
+        if (++acc == kUnitNY) { acc = 0; aphase ^= 1; }
         const int col = j * BM + fl;
 #pragma unroll
         for (int n = 0; n < UN; ++n)
           if (n < ntok) __stcg(yp + (int64_t)(r0 + n) * p.H + col, y[n]);
       }
+      if (threadIdx.x == 64) UNIT_STAMP(7);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(64));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kUnitTmemCols));
   }
 }
 
@@ -1133,7 +1195,8 @@ extern "C" int spmoe_expert_ffn_tc_units(const uint16_t* pool, int64_t slot_elem
   if (H % BM || F % BM || max_tokens_per_expert < 0 || max_tokens_per_expert > UN)
     return (int)cudaErrorInvalidValue;
   if (T == 0 || expert_mask == 0) return 0;
-  if (!x || !perm_token || !x_perm || !y || !workspace) return (int)cudaErrorInvalidValue;
+  (void)x_perm;  // the unit kernel gathers x rows itself (TMA gather4); kept for the ABI
+  if (!x || !perm_token || !y || !workspace) return (int)cudaErrorInvalidValue;
   cudaStream_t s = (cudaStream_t)stream;
   int dev = 0, nsms = 148;
   cudaGetDevice(&dev);
@@ -1160,9 +1223,9 @@ extern "C" int spmoe_expert_ffn_tc_units(const uint16_t* pool, int64_t slot_elem
     const uint64_t d[3] = {(uint64_t)H, (uint64_t)2 * F, (uint64_t)max_slot + 1};
     const uint64_t str[2] = {(uint64_t)H * 2, sb};
     if (!make_map(&mwu, pool, 3, d, str, BM)) return (int)cudaErrorInvalidValue;
-    const uint64_t da[2] = {(uint64_t)H, (uint64_t)rows};
+    const uint64_t da[2] = {(uint64_t)H, (uint64_t)T};
     const uint64_t sa[1] = {(uint64_t)H * 2};
-    if (!make_map(&mx, x_perm, 2, da, sa, UN)) return (int)cudaErrorInvalidValue;
+    if (!make_map(&mx, x, 2, da, sa, 1)) return (int)cudaErrorInvalidValue;  // gather4 rows of x
     const uint64_t d2[3] = {(uint64_t)F, (uint64_t)H, (uint64_t)max_slot + 1};
     const uint64_t str2[2] = {(uint64_t)F * 2, sb};
     if (!make_map(&mwd, pool + (int64_t)2 * F * H, 3, d2, str2, BM)) return (int)cudaErrorInvalidValue;
@@ -1176,8 +1239,9 @@ extern "C" int spmoe_expert_ffn_tc_units(const uint16_t* pool, int64_t slot_elem
   }
   const int units = p.n_active * (F / BM);
   DevSpan* span = (DevSpan*)k3_timing().dspan;
+  p.perm_token = perm_token;
+  p.span = span;
   k3_timing_begin(s);
-  gather_rows_kernel<<<nsms, 256, 0, s>>>(x, perm_token, expert_offsets, E, H, x_perm, span);
   int st = (int)launch_pdl(ffn_tc_unit_kernel<STAGES>, dim3(min(units, nsms)), dim3(kThreads), smem, s, mwu, mx, mwd,
                            p);
   if (st) return st;
@@ -1186,6 +1250,13 @@ extern "C" int spmoe_expert_ffn_tc_units(const uint16_t* pool, int64_t slot_elem
   k3_timing_end(s);
   return st;
 }
+
+#ifdef SPMOE_UNIT_STAMPS
+extern "C" int spmoe_debug_unit_stamps(void* buf) {
+  unsigned long long* p = (unsigned long long*)buf;
+  return (int)cudaMemcpyToSymbol(tc::g_unit_stamps, &p, sizeof(p));
+}
+#endif
 
 /* floats of workspace: the F/128 partial planes of [rows, H] */
 extern "C" int64_t spmoe_expert_ffn_tc_units_workspace_floats(int rows, int H, int F) {

@@ -404,7 +404,7 @@ def expert_ffn_tc_units(
     need = tc_units_workspace_floats(T * top_k, H, ffn_dim)
     if workspace is None or workspace.numel() < need:
         raise ValueError(f"tcgen05 unit workspace needs {need} floats")
-    LAUNCHES["count"] += 3
+    LAUNCHES["count"] += 2  # unit kernel (x rows by TMA gather4) + fixed-order reduce
     _native.call(
         "spmoe_expert_ffn_tc_units",
         pool.data_ptr(),
