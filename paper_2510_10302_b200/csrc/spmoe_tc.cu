@@ -711,9 +711,13 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
       int pend_stage[STAGES], pend_kb[STAGES], npend = 0;
       int xr[UN];
       const uint64_t ef = l2_evict_first_policy();
-      auto x_rows = [&](int arow, int ntok) {
+      // offsets / perm_token are read only after griddepcontrol.wait, so
+      // whichever kernel precedes this one in the stream may produce them
+      auto x_rows = [&](int e) {
+        const int arow = p.offsets[e];
+        const int ntok = max(1, min(UN, p.offsets[e + 1] - arow));
 #pragma unroll
-        for (int i = 0; i < UN; ++i) xr[i] = __ldg(p.perm_token + arow + min(i, ntok - 1));
+        for (int i = 0; i < UN; ++i) xr[i] = p.perm_token[arow + min(i, ntok - 1)];
       };
       auto load_x = [&](uint8_t* dst, uint64_t* bar, int kb) {
 #pragma unroll
@@ -723,9 +727,7 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int a = u / mt_up, m = u - a * mt_up;
         const int e = p.active[a], slot = p.slot[a];
-        const int arow = p.offsets[e];
-        const int ntok = max(1, min(UN, p.offsets[e + 1] - arow));
-        if (waited) x_rows(arow, ntok);
+        if (waited) x_rows(e);
         for (int kb = 0; kb < kb_up; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * STAGE_BYTES;
@@ -741,7 +743,7 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
             pend_kb[npend] = kb;
             if (++npend == STAGES || kb + 1 == kb_up) {
               pdl_wait();
-              x_rows(arow, ntok);
+              x_rows(e);
               for (int i = 0; i < npend; ++i)
                 load_x(smem + pend_stage[i] * STAGE_BYTES + 2 * A_BYTES, &full_bar[pend_stage[i]], pend_kb[i]);
               npend = 0;
@@ -824,11 +826,11 @@ ffn_tc_unit_kernel(const __grid_constant__ CUtensorMap map_wu, const __grid_cons
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int a = u / mt_up, m = u - a * mt_up;
       const int e = p.active[a];
-      const int r0 = p.offsets[e];
-      const int ntok = min(UN, p.offsets[e + 1] - r0);
-      mbar_wait(&gu_full, gphase);
+      mbar_wait(&gu_full, gphase);  // after the producer's griddepcontrol.wait (x box -> MMA -> commit)
       gphase ^= 1;
       tc_fence_after();
+      const int r0 = p.offsets[e];
+      const int ntok = min(UN, p.offsets[e + 1] - r0);
       float g[16], v[16];
       const uint32_t lq = (uint32_t)(32 * q) << 16;
       tmem_ld16(tmem_base + lq, g);
