@@ -458,7 +458,7 @@ class SpecMoEEngine:
         path = use_tc if isinstance(use_tc, str) else self._k3_path(F, maxtok)
         rows = xn.shape[0] * k
         if path == "units":
-            K.expert_ffn_tc_units(pool, slots, mask, xn, F, k, offsets, perm, maxtok, s.xp[:rows], None, y, s.ysplit)
+            K.expert_ffn_tc_units(pool, slots, mask, xn, F, k, offsets, perm, maxtok, None, None, y, s.ysplit)
         elif path == "tc":
             # launch-independent split: bits do not depend on launch grouping
             su, sd = K.tc_plan_static(self.arch.hidden, F, self.num_sms)

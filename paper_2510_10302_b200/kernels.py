@@ -385,7 +385,7 @@ def expert_ffn_tc_units(
     offsets: torch.Tensor,
     perm: torch.Tensor,
     max_tokens_per_expert: int,
-    x_perm: torch.Tensor,
+    x_perm: torch.Tensor | None,
     h_scratch: torch.Tensor | None,
     y: torch.Tensor,
     workspace: torch.Tensor,
@@ -394,7 +394,9 @@ def expert_ffn_tc_units(
     """Unit-fused tcgen05 K3: one launch runs both phases per (expert,
     128-feature block) unit, a PDL-chained one sums the partials in a fixed
     order; experts with at most :data:`UNIT_MAX_TOKENS` routed tokens.
-    ``workspace``: f32 of :func:`tc_units_workspace_floats` elements."""
+    ``workspace``: f32 of :func:`tc_units_workspace_floats` elements.
+    ``x_perm`` is unused (the kernel gathers x rows itself by TMA gather4)
+    and may be None."""
     _need(pool, BF16, "pool", 2)
     _need(x, BF16, "x", 2)
     T, H = x.shape
@@ -420,7 +422,7 @@ def expert_ffn_tc_units(
         offsets.data_ptr(),
         perm.data_ptr(),
         max_tokens_per_expert,
-        x_perm.data_ptr(),
+        _ptr(x_perm),
         _ptr(h_scratch),
         y.data_ptr(),
         workspace.data_ptr(),
